@@ -1,0 +1,678 @@
+// libfmap_cuda — C ABI (include/fmap_cuda.h) over the sm_100a kernels.
+//
+// Error semantics follow the reference (solver.hpp:225-322, types.hpp):
+//   * validation failures -> FMAP_INVALID_ARGUMENT, before any result is exposed
+//   * memory cap          -> FMAP_MEMORY_CAP, before any allocation
+//   * singular systems    -> FMAP_SINGULAR with the LOWEST failing global index
+//   * no partial results on error (the caller's C buffer content is unspecified)
+// There is no CPU fallback: every numeric result comes from a device kernel.
+#include "../../include/fmap_cuda.h"
+#include "fmap_kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace fmap;
+
+struct fmap_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  // control block: [0] fail_min (u64) | [8] rcond bits (u32) | [12] flags (u32)
+  unsigned char* d_ctrl = nullptr;
+  unsigned char* h_ctrl = nullptr;  // pinned
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches = 0;
+  int max_smem_optin = 0;
+  int num_sms = 0;
+};
+
+namespace {
+
+constexpr unsigned long long kNoFail = ~0ull;
+
+int set_err(fmap_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  return code;
+}
+
+#define FMAP_CK(ctx, expr)                                                                   \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return set_err((ctx), FMAP_CUDA_ERROR,                                                 \
+                     std::string(#expr) + ": " + cudaGetErrorString(_e));                    \
+  } while (0)
+
+unsigned long long* d_fail(fmap_ctx* c) { return reinterpret_cast<unsigned long long*>(c->d_ctrl); }
+unsigned* d_rcond(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 8); }
+unsigned* d_flags(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 12); }
+
+// Grow-only device arena (BatchedWorkspace analogue, solver.hpp:86-93).
+// Growth preserves the contents so callers may stage data before reserving more.
+int arena_reserve(fmap_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->arena_bytes) return FMAP_OK;
+  const size_t rounded = (bytes + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
+  void* fresh = nullptr;
+  FMAP_CK(ctx, cudaMalloc(&fresh, rounded));
+  if (ctx->arena) {
+    FMAP_CK(ctx, cudaMemcpyAsync(fresh, ctx->arena, ctx->arena_bytes, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+    FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    FMAP_CK(ctx, cudaFree(ctx->arena));
+  }
+  ctx->arena = fresh;
+  ctx->arena_bytes = rounded;
+  return FMAP_OK;
+}
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+size_t carve_size(std::initializer_list<size_t> bytes) {
+  size_t off = 0;
+  for (size_t b : bytes) off = ((off + 255) & ~size_t(255)) + b;
+  return off;
+}
+
+int reset_ctrl(fmap_ctx* ctx) {
+  unsigned char init[16];
+  const unsigned long long nf = kNoFail;
+  const unsigned fmax = 0x7f7fffffu;  // FLT_MAX bits
+  const unsigned zero = 0;
+  std::memcpy(init, &nf, 8);
+  std::memcpy(init + 8, &fmax, 4);
+  std::memcpy(init + 12, &zero, 4);
+  std::memcpy(ctx->h_ctrl, init, 16);
+  FMAP_CK(ctx, cudaMemcpyAsync(ctx->d_ctrl, ctx->h_ctrl, 16, cudaMemcpyHostToDevice, ctx->stream));
+  return FMAP_OK;
+}
+
+int read_ctrl(fmap_ctx* ctx, unsigned long long* fail, float* rcond, unsigned* flags) {
+  FMAP_CK(ctx, cudaMemcpyAsync(ctx->h_ctrl + 16, ctx->d_ctrl, 16, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  std::memcpy(fail, ctx->h_ctrl + 16, 8);
+  unsigned rb;
+  std::memcpy(&rb, ctx->h_ctrl + 24, 4);
+  std::memcpy(rcond, &rb, 4);
+  std::memcpy(flags, ctx->h_ctrl + 28, 4);
+  return FMAP_OK;
+}
+
+void default_opts(fmap_solver_options* o) {
+  o->ridge = 0.f;
+  o->rcond_threshold = -1.f;
+  o->has_memory_cap = 0;
+  o->memory_cap_bytes = 0;
+  o->threads = 0;
+  o->inject_fault = 0;
+  o->compute_residual = 1;
+}
+
+void init_report(fmap_report* r) {
+  if (!r) return;
+  std::memset(r, 0, sizeof *r);
+  r->failing_system = -1;
+}
+
+std::string flags_message(unsigned f) {
+  // validate_problem order (solver.hpp:140-144); NaN masks fail the >= 0 test first.
+  if (f & 32u) return "resolvent mask needs a non-zero spectrum to normalize by";
+  if (f & 16u) return "eigenvalues must be non-negative and finite";
+  if (f & 8u) return "penalty mask entries must be non-negative";
+  if (f & 1u) return "gram contains non-finite entries";
+  if (f & 2u) return "rhs contains non-finite entries";
+  if (f & 4u) return "mask contains non-finite entries";
+  return "invalid input";
+}
+
+int max_resolution(fmap_ctx* ctx) {
+  int k = 4;
+  while (solver_smem_bytes(k + 4) <= (size_t)ctx->max_smem_optin) k += 4;
+  return k;
+}
+
+// Core solve on device buffers. mask_mode 0: d_mask; 1/2: from eigenvalues.
+int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float* R,
+               const float* M, const float* ev1, const float* ev2, int mask_mode, float sigma,
+               float lambda, const fmap_solver_options* o, float* C, fmap_report* rep,
+               bool device_validate, size_t host_staging_bytes) {
+  fmap_solver_options opts;
+  default_opts(&opts);
+  if (o) opts = *o;
+  init_report(rep);
+  if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
+  if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
+  if (!(lambda >= 0.f)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "lambda must be non-negative");
+  if (mask_mode == 1 && !(sigma > 0.f))
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "sigma must be positive");
+  if (!G || !R || !C || (mask_mode == 0 && !M) || (mask_mode != 0 && (!ev1 || !ev2)))
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
+  const int kmax = max_resolution(ctx);
+  if (k > kmax)
+    return set_err(ctx, FMAP_INVALID_ARGUMENT,
+                   "k = " + std::to_string(k) + " exceeds the single-CTA solver limit " +
+                       std::to_string(kmax) + " on this device");
+  const size_t kk = (size_t)k * k;
+  const size_t nsys = (size_t)b * k;
+  const bool need_mask_scratch = opts.compute_residual && mask_mode != 0;
+  const size_t res_partial = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
+  const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
+                                     need_mask_scratch ? (size_t)b * kk * sizeof(float) : 0,
+                                     (size_t)k * sizeof(float)});
+  const uint64_t required = (uint64_t)scratch + host_staging_bytes;
+  if (rep) rep->peak_extra_bytes = required;
+  if (opts.has_memory_cap && required > opts.memory_cap_bytes) {
+    if (rep) {
+      rep->required_bytes = required;
+      rep->cap_bytes = opts.memory_cap_bytes;
+    }
+    return set_err(ctx, FMAP_MEMORY_CAP,
+                   "cuda route needs " + std::to_string(required) +
+                       " bytes of device scratch, above the cap of " +
+                       std::to_string(opts.memory_cap_bytes));
+  }
+  int st = arena_reserve(ctx, scratch + host_staging_bytes);
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena) + host_staging_bytes};
+  double* partial = cv.take<double>(res_partial);
+  double* res_out = cv.take<double>((size_t)b);
+  float* mask_scratch = cv.take<float>(need_mask_scratch ? (size_t)b * kk : 0);
+  float* zrow = cv.take<float>((size_t)k);
+
+  if ((st = reset_ctrl(ctx))) return st;
+  ctx->launches = 0;
+  if (device_validate) {
+    if (mask_mode == 0) {
+      FMAP_CK(ctx, launch_validate(G, R, M, (size_t)b * kk, d_flags(ctx), ctx->stream));
+    } else {
+      FMAP_CK(ctx, launch_validate(G, R, nullptr, (size_t)b * kk, d_flags(ctx), ctx->stream));
+      FMAP_CK(ctx, launch_validate_ev(ev1, ev2, (size_t)b * k, d_flags(ctx), ctx->stream));
+      ctx->launches++;
+    }
+    ctx->launches++;
+  }
+
+  SolveParams p{};
+  p.gram = G;
+  p.rhs = R;
+  p.mask = M;
+  p.ev1 = ev1;
+  p.ev2 = ev2;
+  p.C = C;
+  p.k = (int)k;
+  p.K4 = ((int)k + 3) & ~3;
+  p.Rp = p.K4 + 4;
+  p.nsys = (int64_t)nsys;
+  p.sys_offset = 0;
+  p.lambda = lambda;
+  p.ridge = opts.ridge;
+  p.sigma = sigma;
+  p.rcond_thr = opts.rcond_threshold < 0.f ? 1e-7f : opts.rcond_threshold;
+  p.rhs_unit = -1;
+  p.fail_min = d_fail(ctx);
+  p.rcond_min_bits = d_rcond(ctx);
+  p.flags = d_flags(ctx);
+
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  FMAP_CK(ctx, launch_chol_solve(p, mask_mode, ctx->stream));
+  ctx->launches++;
+  if (opts.inject_fault) {
+    // solver.hpp:269-273: negate the largest-|.| entry of row 0 of system 0's
+    // assembled LHS.  Solved exactly as a rank-one update of the SPD system.
+    std::vector<float> g0(k);
+    float m00 = 0.f;
+    FMAP_CK(ctx, cudaMemcpyAsync(g0.data(), G, k * sizeof(float), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    if (mask_mode == 0) {
+      FMAP_CK(ctx, cudaMemcpyAsync(&m00, M, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+      std::vector<float> e1(k), e2(k);
+      FMAP_CK(ctx, cudaMemcpyAsync(e1.data(), ev1, k * sizeof(float), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+      FMAP_CK(ctx, cudaMemcpyAsync(e2.data(), ev2, k * sizeof(float), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+      FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+      if (mask_mode == 1) {
+        float emax = 0.f;
+        for (int64_t c = 0; c < k; ++c) emax = std::max(emax, std::max(e1[c], e2[c]));
+        const float s2 = sigma * sigma;
+        const float mu1 = e1[0] / emax, mu2 = e2[0] / emax;
+        const float re = mu2 / (mu2 * mu2 + s2) - mu1 / (mu1 * mu1 + s2);
+        const float im = sigma / (mu2 * mu2 + s2) - sigma / (mu1 * mu1 + s2);
+        m00 = re * re + im * im;
+      } else {
+        const float d = e2[0] - e1[0];
+        m00 = d * d;
+      }
+    }
+    FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    g0[0] += lambda * m00 + opts.ridge;
+    int w = 0;
+    float best = -1.f;
+    for (int64_t c = 0; c < k; ++c)
+      if (std::fabs(g0[c]) > best) {
+        best = std::fabs(g0[c]);
+        w = (int)c;
+      }
+    const float alpha = -2.f * g0[w];
+    SolveParams pz = p;
+    pz.C = zrow;  // system 0 writes its row at offset 0
+    pz.nsys = 1;
+    pz.rhs_unit = 0;
+    FMAP_CK(ctx, launch_chol_solve(pz, mask_mode, ctx->stream));
+    FMAP_CK(ctx, launch_fault_combine(C, zrow, (int)k, w, alpha, d_fail(ctx), 0ull, ctx->stream));
+    ctx->launches += 2;
+  }
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+
+  if (opts.compute_residual) {
+    const float* Muse = M;
+    if (mask_mode != 0) {
+      FMAP_CK(ctx, launch_mask(ev1, ev2, b, (int)k, mask_mode == 1 ? 1 : 0, sigma, mask_scratch,
+                               ctx->stream));
+      Muse = mask_scratch;
+      ctx->launches++;
+    }
+    FMAP_CK(ctx, launch_residual(C, G, R, Muse, b, (int)k, lambda, partial, res_out, ctx->stream));
+    ctx->launches += 2;
+  }
+
+  unsigned long long fail;
+  float rcond;
+  unsigned flags;
+  if ((st = read_ctrl(ctx, &fail, &rcond, &flags))) return st;
+  float ms = 0.f;
+  FMAP_CK(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (rep) {
+    rep->wall_seconds = ms * 1e-3;
+    rep->min_rcond = rcond;
+  }
+  if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, flags_message(flags));
+  if (fail != kNoFail) {
+    if (rep) rep->failing_system = (int64_t)fail;
+    return set_err(ctx, FMAP_SINGULAR,
+                   "row system " + std::to_string(fail) +
+                       " is numerically singular (Cholesky pivot / rcond estimate / non-finite "
+                       "solution)");
+  }
+  if (opts.compute_residual && rep) {
+    std::vector<double> res(b);
+    FMAP_CK(ctx, cudaMemcpy(res.data(), res_out, b * sizeof(double), cudaMemcpyDeviceToHost));
+    double mx = 0.0;
+    for (double v : res) mx = std::max(mx, v);
+    rep->max_residual = mx;
+  }
+  ctx->last_error.clear();
+  return FMAP_OK;
+}
+
+bool host_finite(const float* p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmap_abi_version(void) { return FMAP_CUDA_ABI_VERSION; }
+
+void fmap_default_options(fmap_solver_options* opts) {
+  if (opts) default_opts(opts);
+}
+
+int fmap_ctx_create(int device, fmap_ctx** out) {
+  if (!out) return FMAP_INVALID_ARGUMENT;
+  *out = nullptr;
+  fmap_ctx* ctx = new fmap_ctx();
+  ctx->device = device;
+  auto fail = [&](cudaError_t e) {
+    delete ctx;
+    (void)e;
+    return FMAP_CUDA_ERROR;
+  };
+  cudaError_t e;
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(e);
+  if ((e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e);
+  ctx->stream = ctx->own_stream;
+  if ((e = cudaMalloc(&ctx->d_ctrl, 64)) != cudaSuccess) return fail(e);
+  if ((e = cudaMallocHost(&ctx->h_ctrl, 64)) != cudaSuccess) return fail(e);
+  if ((e = cudaEventCreate(&ctx->ev0)) != cudaSuccess) return fail(e);
+  if ((e = cudaEventCreate(&ctx->ev1)) != cudaSuccess) return fail(e);
+  if ((e = cudaDeviceGetAttribute(&ctx->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                  device)) != cudaSuccess)
+    return fail(e);
+  if ((e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device)) !=
+      cudaSuccess)
+    return fail(e);
+  *out = ctx;
+  return FMAP_OK;
+}
+
+int fmap_ctx_destroy(fmap_ctx* ctx) {
+  if (!ctx) return FMAP_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->d_ctrl) cudaFree(ctx->d_ctrl);
+  if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return FMAP_OK;
+}
+
+int fmap_ctx_set_stream(fmap_ctx* ctx, void* s) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  ctx->stream = s ? reinterpret_cast<cudaStream_t>(s) : ctx->own_stream;
+  return FMAP_OK;
+}
+
+const char* fmap_last_error(const fmap_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "no context"; }
+
+int64_t fmap_max_resolution(fmap_ctx* ctx) { return ctx ? max_resolution(ctx) : 0; }
+
+int64_t fmap_last_launch_count(const fmap_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fmap_solve_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gram,
+                       const float* d_rhs, const float* d_mask, float lambda,
+                       const fmap_solver_options* opts, float* d_C, fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  return solve_core(ctx, b, k, d_gram, d_rhs, d_mask, nullptr, nullptr, 0, 0.f, lambda, opts,
+                    d_C, report, true, 0);
+}
+
+int fmap_solve_ev_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gram,
+                          const float* d_rhs, const float* d_ev1, const float* d_ev2,
+                          int mask_kind, float sigma, float lambda,
+                          const fmap_solver_options* opts, float* d_C, fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  if (mask_kind != FMAP_MASK_COMMUTATIVITY && mask_kind != FMAP_MASK_RESOLVENT)
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
+  return solve_core(ctx, b, k, d_gram, d_rhs, nullptr, d_ev1, d_ev2,
+                    mask_kind == FMAP_MASK_RESOLVENT ? 1 : 2, sigma, lambda, opts, d_C, report,
+                    true, 0);
+}
+
+int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const float* rhs,
+                   const float* mask, float lambda, const fmap_solver_options* opts,
+                   float* C_out, fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  init_report(report);
+  if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
+  if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
+  if (!gram || !rhs || !mask || !C_out) return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
+  if (!(lambda >= 0.f)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "lambda must be non-negative");
+  const size_t kk = (size_t)k * k;
+  // solver.hpp:132-145, per problem in order, before any device work
+  for (int64_t q = 0; q < b; ++q) {
+    const float* m = mask + q * kk;
+    for (size_t e = 0; e < kk; ++e)
+      if (!(m[e] >= 0.f))
+        return set_err(ctx, FMAP_INVALID_ARGUMENT, "penalty mask entries must be non-negative");
+    if (!host_finite(gram + q * kk, kk))
+      return set_err(ctx, FMAP_INVALID_ARGUMENT, "gram contains non-finite entries");
+    if (!host_finite(rhs + q * kk, kk))
+      return set_err(ctx, FMAP_INVALID_ARGUMENT, "rhs contains non-finite entries");
+    if (!host_finite(m, kk))
+      return set_err(ctx, FMAP_INVALID_ARGUMENT, "mask contains non-finite entries");
+  }
+  const size_t bytes = (size_t)b * kk * sizeof(float);
+  const size_t staging = carve_size({bytes, bytes, bytes, bytes});
+  fmap_solver_options o;
+  default_opts(&o);
+  if (opts) o = *opts;
+  if (o.has_memory_cap && staging > o.memory_cap_bytes) {
+    if (report) {
+      report->required_bytes = staging;
+      report->cap_bytes = o.memory_cap_bytes;
+      report->peak_extra_bytes = staging;
+    }
+    return set_err(ctx, FMAP_MEMORY_CAP,
+                   "cuda route needs " + std::to_string(staging) +
+                       " bytes of device staging, above the cap of " +
+                       std::to_string(o.memory_cap_bytes));
+  }
+  int st = arena_reserve(ctx, staging + (64u << 20));
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  float* dG = cv.take<float>((size_t)b * kk);
+  float* dR = cv.take<float>((size_t)b * kk);
+  float* dM = cv.take<float>((size_t)b * kk);
+  float* dC = cv.take<float>((size_t)b * kk);
+  FMAP_CK(ctx, cudaMemcpyAsync(dG, gram, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(dR, rhs, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(dM, mask, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  st = solve_core(ctx, b, k, dG, dR, dM, nullptr, nullptr, 0, 0.f, lambda, &o, dC, report, false,
+                  staging);
+  if (st) return st;
+  FMAP_CK(ctx, cudaMemcpyAsync(C_out, dC, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMAP_OK;
+}
+
+int fmap_mask_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_ev1,
+                      const float* d_ev2, int mask_kind, float sigma, float* d_mask_out) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalue vectors must be non-empty");
+  if (mask_kind != 0 && mask_kind != 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
+  if (mask_kind == 1 && !(sigma > 0.f))
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "sigma must be positive");
+  int st = reset_ctrl(ctx);
+  if (st) return st;
+  FMAP_CK(ctx, launch_validate_ev(d_ev1, d_ev2, (size_t)b * k, d_flags(ctx), ctx->stream));
+  FMAP_CK(ctx, launch_mask(d_ev1, d_ev2, b, (int)k, mask_kind, sigma, d_mask_out, ctx->stream));
+  ctx->launches = 2;
+  unsigned long long fail;
+  float rc;
+  unsigned flags;
+  if ((st = read_ctrl(ctx, &fail, &rc, &flags))) return st;
+  if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalues must be non-negative");
+  return FMAP_OK;
+}
+
+int fmap_mask_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* ev1, const float* ev2,
+                  int mask_kind, float sigma, float* mask_out) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalue vectors must be non-empty");
+  if (mask_kind != 0 && mask_kind != 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
+  // masks.hpp:48-53 / 79-89 validation order
+  if (!host_finite(ev1, (size_t)b * k))
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "ev1 contains non-finite entries");
+  if (!host_finite(ev2, (size_t)b * k))
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "ev2 contains non-finite entries");
+  for (int64_t e = 0; e < b * k; ++e)
+    if (!(ev1[e] >= 0.f) || !(ev2[e] >= 0.f))
+      return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalues must be non-negative");
+  if (mask_kind == 1) {
+    if (!(sigma > 0.f)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "sigma must be positive");
+    for (int64_t q = 0; q < b; ++q) {
+      float m = 0.f;
+      for (int64_t c = 0; c < k; ++c) m = std::max(m, std::max(ev1[q * k + c], ev2[q * k + c]));
+      if (!(m > 0.f))
+        return set_err(ctx, FMAP_INVALID_ARGUMENT,
+                       "resolvent mask needs a non-zero spectrum to normalize by");
+    }
+  }
+  const size_t evb = (size_t)b * k * sizeof(float), mb = (size_t)b * k * k * sizeof(float);
+  int st = arena_reserve(ctx, carve_size({evb, evb, mb}));
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  float* d1 = cv.take<float>((size_t)b * k);
+  float* d2 = cv.take<float>((size_t)b * k);
+  float* dm = cv.take<float>((size_t)b * k * k);
+  FMAP_CK(ctx, cudaMemcpyAsync(d1, ev1, evb, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(d2, ev2, evb, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, launch_mask(d1, d2, b, (int)k, mask_kind, sigma, dm, ctx->stream));
+  ctx->launches = 1;
+  FMAP_CK(ctx, cudaMemcpyAsync(mask_out, dm, mb, cudaMemcpyDeviceToHost, ctx->stream));
+  FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMAP_OK;
+}
+
+int fmap_normal_equations_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d,
+                                  const float* d_A, const float* d_B, float* d_gram,
+                                  float* d_rhs) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  if (b < 1 || k < 1 || d < 1)
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "descriptor A must be non-empty");
+  FMAP_CK(ctx, launch_gemm_nt(d_A, d_A, b, (int)k, (int)k, (int)d, d_gram, ctx->stream));
+  FMAP_CK(ctx, launch_gemm_nt(d_B, d_A, b, (int)k, (int)k, (int)d, d_rhs, ctx->stream));
+  ctx->launches = 2;
+  return FMAP_OK;
+}
+
+int fmap_normal_equations_f32(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d, const float* A,
+                              const float* B, float* gram_out, float* rhs_out) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  if (b < 1 || k < 1 || d < 1)
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "descriptor A must be non-empty");
+  const size_t nab = (size_t)b * k * d, ng = (size_t)b * k * k;
+  if (!host_finite(A, nab)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "A contains non-finite entries");
+  if (!host_finite(B, nab)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "B contains non-finite entries");
+  int st = arena_reserve(ctx, carve_size({nab * 4, nab * 4, ng * 4, ng * 4}));
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  float* dA = cv.take<float>(nab);
+  float* dB = cv.take<float>(nab);
+  float* dG = cv.take<float>(ng);
+  float* dR = cv.take<float>(ng);
+  FMAP_CK(ctx, cudaMemcpyAsync(dA, A, nab * 4, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(dB, B, nab * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = fmap_normal_equations_f32_dev(ctx, b, k, d, dA, dB, dG, dR))) return st;
+  FMAP_CK(ctx, cudaMemcpyAsync(gram_out, dG, ng * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(rhs_out, dR, ng * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMAP_OK;
+}
+
+int fmap_project_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d,
+                         const float* d_phi, const float* d_mass, const float* d_F,
+                         float* d_out) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  if (b < 1 || n < 1 || k < 1 || d < 1)
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "basis and features must be non-empty");
+  FMAP_CK(ctx, launch_project(d_phi, d_mass, d_F, b, n, (int)k, (int)d, d_out, ctx->stream));
+  ctx->launches = 1;
+  return FMAP_OK;
+}
+
+int fmap_residual_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_C,
+                          const float* d_gram, const float* d_rhs, const float* d_mask,
+                          float lambda, double* d_out) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
+  const size_t np = residual_partial_count(b, (int)k);
+  int st = arena_reserve(ctx, np * sizeof(double));
+  if (st) return st;
+  FMAP_CK(ctx, launch_residual(d_C, d_gram, d_rhs, d_mask, b, (int)k, lambda,
+                               reinterpret_cast<double*>(ctx->arena), d_out, ctx->stream));
+  ctx->launches = 2;
+  return FMAP_OK;
+}
+
+int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int64_t k,
+                          int64_t d, const float* d_phi1, const float* d_mass1,
+                          const float* d_F1, const float* d_ev1, const float* d_phi2,
+                          const float* d_mass2, const float* d_F2, const float* d_ev2,
+                          int mask_kind, float sigma, float lambda,
+                          const fmap_solver_options* opts, float* d_Cxy, float* d_Cyx,
+                          fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  init_report(report);
+  if (b < 1 || n1 < 1 || n2 < 1 || k < 1 || d < 1)
+    return set_err(ctx, FMAP_INVALID_ARGUMENT, "pipeline dimensions must be positive");
+  const size_t nab = (size_t)b * k * d, ng = (size_t)b * k * k;
+  const bool bidir = d_Cyx != nullptr;
+  const size_t scratch = carve_size({nab * 4, nab * 4, ng * 4, ng * 4, bidir ? ng * 4 : 0,
+                                     bidir ? ng * 4 : 0});
+  fmap_solver_options o;
+  default_opts(&o);
+  if (opts) o = *opts;
+  // the pipeline's own scratch lives below the solver's scratch in the arena
+  int st = arena_reserve(ctx, scratch + (64u << 20) +
+                                  (size_t)b * k * k * sizeof(float) * (o.compute_residual ? 1 : 0));
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  float* A = cv.take<float>(nab);
+  float* B = cv.take<float>(nab);
+  float* G = cv.take<float>(ng);
+  float* R = cv.take<float>(ng);
+  float* G2 = bidir ? cv.take<float>(ng) : nullptr;
+  float* R2 = bidir ? cv.take<float>(ng) : nullptr;
+  cudaEvent_t e0, e1;
+  FMAP_CK(ctx, cudaEventCreate(&e0));
+  FMAP_CK(ctx, cudaEventCreate(&e1));
+  FMAP_CK(ctx, cudaEventRecord(e0, ctx->stream));
+  FMAP_CK(ctx, launch_project(d_phi1, d_mass1, d_F1, b, n1, (int)k, (int)d, A, ctx->stream));
+  FMAP_CK(ctx, launch_project(d_phi2, d_mass2, d_F2, b, n2, (int)k, (int)d, B, ctx->stream));
+  FMAP_CK(ctx, launch_gemm_nt(A, A, b, (int)k, (int)k, (int)d, G, ctx->stream));
+  FMAP_CK(ctx, launch_gemm_nt(B, A, b, (int)k, (int)k, (int)d, R, ctx->stream));
+  if (bidir) {
+    FMAP_CK(ctx, launch_gemm_nt(B, B, b, (int)k, (int)k, (int)d, G2, ctx->stream));
+    FMAP_CK(ctx, launch_gemm_nt(A, B, b, (int)k, (int)k, (int)d, R2, ctx->stream));
+  }
+  int64_t pre = bidir ? 6 : 4;
+  // solve_core carves its own scratch after host_staging_bytes = our scratch
+  const int mm = mask_kind == FMAP_MASK_RESOLVENT ? 1 : 2;
+  st = solve_core(ctx, b, k, G, R, nullptr, d_ev1, d_ev2, mm, sigma, lambda, &o, d_Cxy, report,
+                  true, scratch);
+  int64_t launches = pre + ctx->launches;
+  if (st) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return st;
+  }
+  if (bidir) {
+    fmap_report r2;
+    // reverse direction: source/target swap, mask(ev2, ev1) = M^T
+    st = solve_core(ctx, b, k, G2, R2, nullptr, d_ev2, d_ev1, mm, sigma, lambda, &o, d_Cyx, &r2,
+                    true, scratch);
+    launches += ctx->launches;
+    if (st) {
+      if (report) *report = r2;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      return st;
+    }
+    if (report) {
+      report->max_residual = std::max(report->max_residual, r2.max_residual);
+      report->min_rcond = std::min(report->min_rcond, r2.min_rcond);
+    }
+  }
+  FMAP_CK(ctx, cudaEventRecord(e1, ctx->stream));
+  FMAP_CK(ctx, cudaEventSynchronize(e1));
+  float ms = 0.f;
+  FMAP_CK(ctx, cudaEventElapsedTime(&ms, e0, e1));
+  if (report) report->wall_seconds = ms * 1e-3;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->launches = launches;
+  return FMAP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,332 @@
+// Auxiliary kernels on the functional-map path (sm_100a):
+//   * mask construction            masks.hpp:13-89
+//   * input validation             solver.hpp:132-145 (device-side flags)
+//   * normal equations G, R        solver.hpp:95-103
+//   * projection Phi^T diag(M) F   north_star stage (1), SURVEY D1
+//   * stationarity residual        solver.hpp:116-128
+//   * fault-injection combine      solver.hpp:269-273 (Sherman–Morrison form)
+#include "fmap_kernels.cuh"
+
+#include <cfloat>
+
+namespace fmap {
+
+namespace {
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Mask: one CTA per (pair, 8-row chunk); M[q][i][j], rows = target ev2(i),
+// columns = source ev1(j).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) mask_kernel(const float* __restrict__ ev1,
+                                                   const float* __restrict__ ev2, int k, int kind,
+                                                   float sigma, float* __restrict__ out) {
+  __shared__ float red[8];
+  __shared__ float s_evmax;
+  const int q = blockIdx.y;
+  const float* e1 = ev1 + (size_t)q * k;
+  const float* e2 = ev2 + (size_t)q * k;
+  float ev_max = 0.f;
+  if (kind == 1) {
+    float m = 0.f;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) m = fmaxf(m, fmaxf(e1[c], e2[c]));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float mm = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, red[w]);
+      s_evmax = mm;
+    }
+    __syncthreads();
+    ev_max = s_evmax;
+  }
+  const float s2 = sigma * sigma;
+  const int r0 = blockIdx.x * 8;
+  for (int e = threadIdx.x; e < 8 * k; e += blockDim.x) {
+    const int i = r0 + e / k, j = e % k;
+    if (i >= k) break;
+    float v;
+    if (kind == 1) {
+      const float mu1 = e1[j] / ev_max, mu2 = e2[i] / ev_max;
+      const float re = mu2 / (mu2 * mu2 + s2) - mu1 / (mu1 * mu1 + s2);
+      const float im = sigma / (mu2 * mu2 + s2) - sigma / (mu1 * mu1 + s2);
+      v = re * re + im * im;
+    } else {
+      const float d = e2[i] - e1[j];
+      v = d * d;
+    }
+    out[((size_t)q * k + i) * k + j] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Validation flags: bit0 non-finite gram, bit1 non-finite rhs, bit2 non-finite
+// mask, bit3 negative mask, bit4 non-finite / negative eigenvalue.
+// ---------------------------------------------------------------------------
+__global__ void validate_kernel(const float* __restrict__ g, const float* __restrict__ r,
+                                const float* __restrict__ m, size_t n, unsigned* flags) {
+  unsigned f = 0;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    if (g && !(fabsf(g[e]) <= FLT_MAX)) f |= 1u;
+    if (r && !(fabsf(r[e]) <= FLT_MAX)) f |= 2u;
+    if (m) {
+      const float v = m[e];
+      if (!(fabsf(v) <= FLT_MAX)) f |= 4u;
+      if (v < 0.f) f |= 8u;
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+__global__ void validate_ev_kernel(const float* __restrict__ e1, const float* __restrict__ e2,
+                                   size_t n, unsigned* flags) {
+  unsigned f = 0;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const float a = e1[e], b = e2[e];
+    if (!(a >= 0.f && a <= FLT_MAX) || !(b >= 0.f && b <= FLT_MAX)) f |= 16u;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+// ---------------------------------------------------------------------------
+// Batched "NT" GEMM family, FP32 SIMT, 64x64 CTA tile, 4x4 per thread:
+//   out[q][m][n] = sum_t X[q][m][t] * Y[q][n][t]          (gram, rhs)
+// ---------------------------------------------------------------------------
+constexpr int GT = 64, GK = 16;
+
+__global__ void __launch_bounds__(256) gemm_nt_kernel(const float* __restrict__ X,
+                                                      const float* __restrict__ Y, int M, int N,
+                                                      int K, float* __restrict__ out) {
+  __shared__ __align__(16) float xs[GK][GT + 4];
+  __shared__ __align__(16) float ys[GK][GT + 4];
+  const int q = blockIdx.z;
+  const float* Xq = X + (size_t)q * M * K;
+  const float* Yq = Y + (size_t)q * N * K;
+  const int m0 = blockIdx.y * GT, n0 = blockIdx.x * GT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int t0 = 0; t0 < K; t0 += GK) {
+    for (int e = threadIdx.x; e < GT * GK; e += 256) {
+      const int row = e / GK, t = e % GK;
+      const int gm = m0 + row, gn = n0 + row, gt = t0 + t;
+      xs[t][row] = (gm < M && gt < K) ? Xq[(size_t)gm * K + gt] : 0.f;
+      ys[t][row] = (gn < N && gt < K) ? Yq[(size_t)gn * K + gt] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < GK; ++t) {
+      const float4 a = *reinterpret_cast<const float4*>(&xs[t][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&ys[t][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(av[u], bv[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+  float* o = out + (size_t)q * M * N;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int gm = m0 + ty * 4 + u;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int gn = n0 + tx * 4 + v;
+      if (gn < N) o[(size_t)gm * N + gn] = acc[u][v];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Projection out[q][i][t] = sum_v Phi[q][v][i] * mass[q][v] * F[q][v][t]
+// ("TN" GEMM over the vertex dimension), FP32 SIMT, deterministic (no split-K
+// atomics): one CTA per (64 x 64) output tile.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ phi,
+                                                      const float* __restrict__ mass,
+                                                      const float* __restrict__ F, int64_t n,
+                                                      int k, int d, float* __restrict__ out) {
+  __shared__ __align__(16) float ps[GK][GT + 4];
+  __shared__ __align__(16) float fs[GK][GT + 4];
+  const int q = blockIdx.z;
+  const float* Pq = phi + (size_t)q * n * k;
+  const float* Fq = F + (size_t)q * n * d;
+  const float* Mq = mass + (size_t)q * n;
+  const int i0 = blockIdx.y * GT, t0 = blockIdx.x * GT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int64_t v0 = 0; v0 < n; v0 += GK) {
+    for (int e = threadIdx.x; e < GT * GK; e += 256) {
+      const int vv = e / GT, c = e % GT;  // coalesced along the row of Phi / F
+      const int64_t gv = v0 + vv;
+      const bool inb = gv < n;
+      ps[vv][c] = (inb && i0 + c < k) ? Pq[gv * k + i0 + c] : 0.f;
+      fs[vv][c] = (inb && t0 + c < d) ? Mq[gv] * Fq[gv * d + t0 + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int vv = 0; vv < GK; ++vv) {
+      const float4 a = *reinterpret_cast<const float4*>(&ps[vv][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&fs[vv][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[u][w] = fmaf(av[u], bv[w], acc[u][w]);
+    }
+    __syncthreads();
+  }
+  float* o = out + (size_t)q * k * d;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int gi = i0 + ty * 4 + u;
+    if (gi >= k) continue;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int gt = t0 + tx * 4 + w;
+      if (gt < d) o[(size_t)gi * d + gt] = acc[u][w];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Residual: partial[q][chunk] = sum over rows of the chunk of
+//   (C G + lambda M.*C - R)(i,j)^2  in fp64; then a fixed-order reduction.
+// ---------------------------------------------------------------------------
+constexpr int RES_ROWS = 8;
+
+__global__ void __launch_bounds__(256) residual_partial_kernel(
+    const float* __restrict__ C, const float* __restrict__ G, const float* __restrict__ R,
+    const float* __restrict__ M, int k, float lambda, double* __restrict__ partial) {
+  extern __shared__ float cs[];  // RES_ROWS x k rows of C
+  __shared__ double red[8];
+  const int q = blockIdx.y;
+  const int r0 = blockIdx.x * RES_ROWS;
+  const size_t kk = (size_t)k * k;
+  const float* Cq = C + q * kk;
+  for (int e = threadIdx.x; e < RES_ROWS * k; e += blockDim.x) {
+    const int rr = e / k, c = e % k;
+    cs[e] = (r0 + rr < k) ? Cq[(size_t)(r0 + rr) * k + c] : 0.f;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < RES_ROWS * k; e += blockDim.x) {
+    const int rr = e / k, j = e % k;
+    const int i = r0 + rr;
+    if (i >= k) continue;
+    const float* Gq = G + q * kk;
+    float s = 0.f;
+    for (int t = 0; t < k; ++t) s = fmaf(cs[rr * k + t], Gq[(size_t)t * k + j], s);
+    const size_t idx = (size_t)i * k + j;
+    const float v = s + lambda * (M[q * kk + idx] * cs[rr * k + j]) - R[q * kk + idx];
+    acc += (double)v * (double)v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    partial[(size_t)q * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void residual_finish_kernel(const double* __restrict__ partial, int nchunk, int b,
+                                       double* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= b) return;
+  double t = 0.0;
+  for (int c = 0; c < nchunk; ++c) t += partial[(size_t)q * nchunk + c];
+  out[q] = sqrt(t);
+}
+
+// x' = x - z * (alpha * x_w) / (1 + alpha * z_w)  — the exact solution of the
+// faulted system S' = S + alpha e_0 e_w^T given x = S^{-1} r, z = S^{-1} e_0.
+__global__ void fault_combine_kernel(float* __restrict__ x, const float* __restrict__ z, int k,
+                                     int w, float alpha, unsigned long long* fail_min,
+                                     unsigned long long sys) {
+  __shared__ float coef;
+  if (threadIdx.x == 0) {
+    const float den = 1.f + alpha * z[w];
+    coef = alpha * x[w] / den;
+    if (!(fabsf(den) > 0.f) || !(fabsf(coef) <= FLT_MAX)) atomicMin(fail_min, sys);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) x[c] = x[c] - z[c] * coef;
+}
+
+}  // namespace
+
+cudaError_t launch_mask(const float* ev1, const float* ev2, int64_t b, int k, int kind,
+                        float sigma, float* out, cudaStream_t st) {
+  dim3 grid((k + 7) / 8, (unsigned)b);
+  mask_kernel<<<grid, 256, 0, st>>>(ev1, ev2, k, kind, sigma, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const float* g, const float* r, const float* m, size_t n,
+                            unsigned* flags, cudaStream_t st) {
+  const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 8);
+  validate_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(g, r, m, n, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsigned* flags,
+                               cudaStream_t st) {
+  const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 4);
+  validate_ev_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(e1, e2, n, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_nt(const float* X, const float* Y, int64_t b, int M, int N, int K,
+                           float* out, cudaStream_t st) {
+  dim3 grid((N + GT - 1) / GT, (M + GT - 1) / GT, (unsigned)b);
+  gemm_nt_kernel<<<grid, 256, 0, st>>>(X, Y, M, N, K, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_project(const float* phi, const float* mass, const float* F, int64_t b,
+                           int64_t n, int k, int d, float* out, cudaStream_t st) {
+  dim3 grid((d + GT - 1) / GT, (k + GT - 1) / GT, (unsigned)b);
+  project_kernel<<<grid, 256, 0, st>>>(phi, mass, F, n, k, d, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_residual(const float* C, const float* G, const float* R, const float* M,
+                            int64_t b, int k, float lambda, double* partial, double* out,
+                            cudaStream_t st) {
+  const int nchunk = (k + RES_ROWS - 1) / RES_ROWS;
+  dim3 grid(nchunk, (unsigned)b);
+  residual_partial_kernel<<<grid, 256, RES_ROWS * k * sizeof(float), st>>>(C, G, R, M, k, lambda,
+                                                                          partial);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, nchunk, (int)b,
+                                                                      out);
+  return cudaGetLastError();
+}
+
+size_t residual_partial_count(int64_t b, int k) {
+  return (size_t)b * ((k + RES_ROWS - 1) / RES_ROWS);
+}
+
+cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,
+                                 unsigned long long* fail_min, unsigned long long sys,
+                                 cudaStream_t st) {
+  fault_combine_kernel<<<1, 256, 0, st>>>(x, z, k, w, alpha, fail_min, sys);
+  return cudaGetLastError();
+}
+
+}  // namespace fmap

@@ -1,0 +1,32 @@
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+#include "fmap_solver.cuh"
+
+namespace fmap {
+
+cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream);
+
+cudaError_t launch_mask(const float* ev1, const float* ev2, int64_t b, int k, int kind,
+                        float sigma, float* out, cudaStream_t st);
+cudaError_t launch_validate(const float* g, const float* r, const float* m, size_t n,
+                            unsigned* flags, cudaStream_t st);
+cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsigned* flags,
+                               cudaStream_t st);
+cudaError_t launch_gemm_nt(const float* X, const float* Y, int64_t b, int M, int N, int K,
+                           float* out, cudaStream_t st);
+cudaError_t launch_project(const float* phi, const float* mass, const float* F, int64_t b,
+                           int64_t n, int k, int d, float* out, cudaStream_t st);
+cudaError_t launch_residual(const float* C, const float* G, const float* R, const float* M,
+                            int64_t b, int k, float lambda, double* partial, double* out,
+                            cudaStream_t st);
+size_t residual_partial_count(int64_t b, int k);
+cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,
+                                 unsigned long long* fail_min, unsigned long long sys,
+                                 cudaStream_t st);
+
+}  // namespace fmap
