@@ -79,19 +79,20 @@ int arena_reserve(fmap_ctx* ctx, size_t bytes) {
 struct Carve {
   char* base;
   size_t off = 0;
+  // 256-byte aligned absolute addresses regardless of where `base` starts
   template <typename T>
   T* take(size_t n) {
-    off = (off + 255) & ~size_t(255);
-    T* p = reinterpret_cast<T*>(base + off);
-    off += n * sizeof(T);
-    return p;
+    uintptr_t a = reinterpret_cast<uintptr_t>(base) + off;
+    a = (a + 255) & ~uintptr_t(255);
+    off = a - reinterpret_cast<uintptr_t>(base) + n * sizeof(T);
+    return reinterpret_cast<T*>(a);
   }
 };
 
 size_t carve_size(std::initializer_list<size_t> bytes) {
   size_t off = 0;
   for (size_t b : bytes) off = ((off + 255) & ~size_t(255)) + b;
-  return off;
+  return off + 256;
 }
 
 int reset_ctrl(fmap_ctx* ctx) {
