@@ -474,8 +474,15 @@ int full_impl(int k, const S* gram, const S* rhs, const S* mask, S lambda, S rid
         v[row] = rhs[(size_t)i * k + j];
       }
     std::vector<S> copy = sys;
+    S amax = 0;
+    for (S e : sys) amax = std::max(amax, std::abs(e));
     LU<S> lu(sys.data(), n);
-    if (lu.has_zero_pivot()) throw Singular(0, "k^2 x k^2 oracle system is numerically singular");
+    // SparseLU reports a numerically zero pivot as a failed factorization; the
+    // dense restatement uses the standard relative test |u_jj| <= n eps max|A|.
+    const S ptol = S(n) * std::numeric_limits<S>::epsilon() * amax;
+    bool tiny = lu.has_zero_pivot();
+    for (int i = 0; i < n && !tiny; ++i) tiny = std::abs(sys[(size_t)i * n + i]) <= ptol;
+    if (tiny) throw Singular(0, "k^2 x k^2 oracle system is numerically singular");
     lu.solve(v.data(), x.data());
     if (!all_finite(x.data(), x.size()))
       throw Singular(0, "k^2 x k^2 oracle solve produced non-finite values");

@@ -381,3 +381,11 @@ def test_golden_solutions_fixture(oracle):
         G, R, M, lam, C = (z[f"{name}__{s}"] for s in ("G", "R", "M", "lam", "C"))
         out = oracle.solve(G, R, M, float(lam)).maps
         assert maxabs(out - C) <= 1e-12 * max(1.0, maxabs(C))
+
+
+def test_generator_golden(oracle):
+    # pins the libstdc++ engine/distribution stream the reference generator uses
+    z = np.load(GOLDEN / "generator.npz")
+    a, b, e1, e2 = oracle.generate_instance(5, 10, 123)
+    assert np.array_equal(a, z["a"]) and np.array_equal(b, z["b"])
+    assert np.array_equal(e1, z["ev1"]) and np.array_equal(e2, z["ev2"])
