@@ -443,6 +443,9 @@ cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t 
   }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  // ask for the full shared-memory carveout so two ~86 KB CTAs co-reside per SM
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
   fn<<<(unsigned)p.nsys, NT, smem, stream>>>(p);
   return cudaGetLastError();
 }
