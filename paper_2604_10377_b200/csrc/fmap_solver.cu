@@ -43,8 +43,25 @@ __device__ __forceinline__ float mask_entry(const SolveParams& p, int64_t q, int
   }
 }
 
+// Offsets inside one panel.  For a panel starting at column j (multiple of 16),
+// column j+t begins at colbase(j+t) = base0 + t*stride - S4(t) with
+//   base0 = col_off(j) - j, stride = Rp - j, S4(t) = sum_{u<t}(u&~3) + (t&~3)
+// so with t known at compile time every address is one IMAD + immediate.
+__host__ __device__ constexpr int S4(int t) {
+  int s = 0;
+  for (int u = 0; u < t; ++u) s += u & ~3;
+  return s + (t & ~3);
+}
+
+struct Panel {
+  int base0, stride, j;
+  __device__ __forceinline__ Panel(int j_, int Rp) : base0(col_off(j_, Rp) - j_), stride(Rp - j_), j(j_) {}
+  // start of column j+t (add the absolute row index)
+  __device__ __forceinline__ int col(int t) const { return base0 + t * stride - S4(t); }
+};
+
 // 8x8 lower-triangular block in registers (36 values, row-major packed).
-__device__ __forceinline__ int tri(int r, int c) { return r * (r + 1) / 2 + c; }
+__host__ __device__ constexpr int tri(int r, int c) { return r * (r + 1) / 2 + c; }
 
 // Cholesky of an 8x8 SPD block followed by the in-place inverse of its factor.
 // On return t[] holds L^{-1} (lower); pivots feed pivmin / bad.
@@ -76,143 +93,120 @@ __device__ __forceinline__ void chol8_inv(float (&t)[36], float& pivmin, bool& b
     }
 }
 
-// Element (r, c) of the diagonal block at (j, j), local indices, with identity
-// padding beyond nbe (only the last panel has nbe < 16).
-struct DiagView {
-  float* A;
-  int Rp, j, nbe;
-  __device__ __forceinline__ int at(int r, int c) const { return colbase(j + c, Rp) + j + r; }
-  __device__ __forceinline__ float ld(int r, int c) const {
-    return (r < nbe && c < nbe) ? A[at(r, c)] : (r == c ? 1.f : 0.f);
-  }
-  __device__ __forceinline__ void st(int r, int c, float v) const {
-    if (r < nbe && c < nbe) A[at(r, c)] = v;
-  }
-};
-
 // Factor the 16x16 diagonal block at (j, j) with warp 0 and overwrite its lower
 // triangle with L11^{-1}.  Blocked 2x2 over 8x8 sub-blocks:
 //   L00 = chol(A00); L10 = A10 L00^{-T}; A11 -= L10 L10^T; L11 = chol(A11);
 //   Linv = [[L00^{-1}, 0], [-L11^{-1} L10 L00^{-1}, L11^{-1}]].
-// Single-thread 8x8 factorizations, 8-lane parallel TRSM / SYRK / combine.
-// pivmin / bad are accumulated in lane 0.
-__device__ __noinline__ void diag_factor(float* A, int Rp, int j, int nbe, int lane,
+// The 8x8 factorizations run replicated in every lane (no communication, no
+// single-lane serialization); the row-parallel steps use lanes 0..7 and an
+// 8x8 scratch (row-major L10).  FULL = the block is 16 wide (all but possibly
+// the last panel); otherwise rows/cols >= nbe behave as identity padding.
+template <bool FULL>
+__device__ __noinline__ void diag_factor(float* A, int Rp, int j, int nbe, float* scr, int lane,
                                          float& pivmin, bool& bad) {
-  const DiagView V{A, Rp, j, nbe};
+  const Panel P(j, Rp);
+  auto at = [&](int r, int c) { return P.col(c) + j + r; };
+  auto ok = [&](int r, int c) { return FULL || (r < nbe && c < nbe); };
   float t[36];
-  // 1. L00^{-1}
-  if (lane == 0) {
+  // 1. L00^{-1}, replicated
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+  for (int c = 0; c < 8; ++c)
 #pragma unroll
-      for (int c = 0; c <= r; ++c) t[tri(r, c)] = V.ld(r, c);
-    chol8_inv(t, pivmin, bad);
+    for (int r = c; r < 8; ++r) t[tri(r, c)] = ok(r, c) ? A[at(r, c)] : (r == c ? 1.f : 0.f);
+  chol8_inv(t, pivmin, bad);
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+  for (int c = 0; c < 8; ++c)
 #pragma unroll
-      for (int c = 0; c <= r; ++c) V.st(r, c, t[tri(r, c)]);
-  }
-  __syncwarp();
-  // 2. lane r < 8: row r of L10 = A10[r,:] * L00^{-T}
-  float l10[8];
+    for (int r = c; r < 8; ++r)
+      if (lane == (tri(r, c) & 31) && ok(r, c)) A[at(r, c)] = t[tri(r, c)];
+  // 2. lanes 0..7: row `lane` of L10 = A10[lane,:] L00^{-T}
   if (lane < 8) {
     float a[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) a[c] = V.ld(8 + lane, c);
+    for (int u = 0; u < 8; ++u) a[u] = ok(8 + lane, u) ? A[at(8 + lane, u)] : 0.f;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       float acc = 0.f;
 #pragma unroll
-      for (int u = 0; u <= c; ++u) acc = fmaf(a[u], V.ld(c, u), acc);  // Linv00[c][u]
-      l10[c] = acc;
+      for (int u = 0; u <= c; ++u) acc = fmaf(a[u], t[tri(c, u)], acc);
+      scr[lane * 8 + c] = acc;
     }
   }
   __syncwarp();
-  if (lane < 8) {
+  // 3. A11 - L10 L10^T, replicated, then L11^{-1}
 #pragma unroll
-    for (int c = 0; c < 8; ++c) V.st(8 + lane, c, l10[c]);
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = c; r < 8; ++r)
+      t[tri(r, c)] = ok(8 + r, 8 + c) ? A[at(8 + r, 8 + c)] : (r == c ? 1.f : 0.f);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    float col[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) col[r] = scr[r * 8 + u];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int r = c; r < 8; ++r) t[tri(r, c)] = fmaf(-col[r], col[c], t[tri(r, c)]);
   }
-  __syncwarp();
-  // 3. lane r < 8: A11[r, 0..r] -= L10[r,:] L10[0..r,:]^T
-  if (lane < 8) {
-    float a11[8];
+  chol8_inv(t, pivmin, bad);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) a11[c] = (c <= lane) ? V.ld(8 + lane, 8 + c) : 0.f;
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = c; r < 8; ++r)
+      if (lane == (tri(r, c) & 31) && ok(8 + r, 8 + c)) A[at(8 + r, 8 + c)] = t[tri(r, c)];
+  __syncwarp();
+  // 4. lanes 0..7: row `lane` of X = -(L11^{-1} L10) L00^{-1}
+  if (lane < 8) {
+    float y[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) y[c] = 0.f;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float lcu = V.ld(8 + c, u);  // L10[c][u], broadcast
-        if (c <= lane) a11[c] = fmaf(-l10[u], lcu, a11[c]);
+      if (u <= lane) {
+        const float li = A[at(8 + lane, 8 + u)];  // L11^{-1}[lane][u]
+        const float4 l0 = *reinterpret_cast<const float4*>(scr + u * 8);
+        const float4 l1 = *reinterpret_cast<const float4*>(scr + u * 8 + 4);
+        y[0] = fmaf(li, l0.x, y[0]);
+        y[1] = fmaf(li, l0.y, y[1]);
+        y[2] = fmaf(li, l0.z, y[2]);
+        y[3] = fmaf(li, l0.w, y[3]);
+        y[4] = fmaf(li, l1.x, y[4]);
+        y[5] = fmaf(li, l1.y, y[5]);
+        y[6] = fmaf(li, l1.z, y[6]);
+        y[7] = fmaf(li, l1.w, y[7]);
       }
     }
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (c <= lane) V.st(8 + lane, 8 + c, a11[c]);
-  }
-  __syncwarp();
-  // 4. L11^{-1}
-  if (lane == 0) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int c = 0; c <= r; ++c) t[tri(r, c)] = V.ld(8 + r, 8 + c);
-    chol8_inv(t, pivmin, bad);
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int c = 0; c <= r; ++c) V.st(8 + r, 8 + c, t[tri(r, c)]);
-  }
-  __syncwarp();
-  // 5. X = -L11^{-1} (L10 L00^{-1});  lane r: row r of T = L10 L00^{-1} first
-  float trow[8];
-  if (lane < 8) {
-#pragma unroll
     for (int c = 0; c < 8; ++c) {
       float acc = 0.f;
 #pragma unroll
-      for (int u = c; u < 8; ++u) acc = fmaf(l10[u], V.ld(u, c), acc);  // Linv00[u][c]
-      trow[c] = acc;
+      for (int u = c; u < 8; ++u) acc = fmaf(y[u], A[at(u, c)], acc);  // L00^{-1}[u][c]
+      if (ok(8 + lane, c)) A[at(8 + lane, c)] = -acc;
     }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) V.st(8 + lane, c, trow[c]);
-  }
-  __syncwarp();
-  if (lane < 8) {
-    float x[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) x[c] = 0.f;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const float li = (u <= lane) ? V.ld(8 + lane, 8 + u) : 0.f;  // Linv11[r][u]
-#pragma unroll
-      for (int c = 0; c < 8; ++c) x[c] = fmaf(-li, V.ld(8 + u, c), x[c]);  // T[u][c]
-    }
-    __syncwarp(0xffu);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) V.st(8 + lane, c, x[c]);
   }
   __syncwarp();
 }
 
-// Rows [r_lo, Rp) of panel [j, j+nbe):  L21 = A21 * L11^{-T}.
-template <int NT>
+// Rows [r_lo, Rp) of panel [j, j+nbe):  L21 = A21 * L11^{-T}  (L11^{-1} stored in
+// the diagonal block).  One row per thread; L11^{-1} reads are warp broadcasts.
+template <int NT, bool FULL>
 __device__ __forceinline__ void panel_trsm(float* A, int Rp, int j, int nbe, int r_lo, int tid) {
+  const Panel P(j, Rp);
   for (int r = r_lo + tid; r < Rp; r += NT) {
     float a[kNB], x[kNB];
 #pragma unroll
     for (int t = 0; t < kNB; ++t) {
-      a[t] = (t < nbe) ? A[colbase(j + t, Rp) + r] : 0.f;
+      a[t] = (FULL || t < nbe) ? A[P.col(t) + r] : 0.f;
       x[t] = 0.f;
     }
 #pragma unroll
     for (int t = 0; t < kNB; ++t) {
-      if (t < nbe) {
-        const int base = colbase(j + t, Rp) + j;
+      if (FULL || t < nbe) {
 #pragma unroll
         for (int c4 = (t & ~3); c4 < kNB; c4 += 4) {
-          if (c4 < nbe) {
-            const float4 l = ld4(A + base + c4);  // Linv[c4..c4+3][t]
+          if (FULL || c4 < nbe) {
+            const float4 l = ld4(A + P.col(t) + j + c4);  // Linv[c4..c4+3][t]
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (c4 + u >= t) x[c4 + u] = fmaf(a[t], f4get(l, u), x[c4 + u]);
@@ -222,39 +216,59 @@ __device__ __forceinline__ void panel_trsm(float* A, int Rp, int j, int nbe, int
     }
 #pragma unroll
     for (int c = 0; c < kNB; ++c)
-      if (c < nbe) A[colbase(j + c, Rp) + r] = x[c];
+      if (FULL || c < nbe) A[P.col(c) + r] = x[c];
   }
 }
 
 // 4x4 register tile: A[r0..r0+3][c0..c0+3] -= sum_{t<nbe} L[r][j+t] L[c][j+t].
-__device__ __forceinline__ void syrk_tile(float* A, int Rp, int j, int nbe, int r0, int c0) {
+// Operand pointers advance by stride - ((t+1)&~3) per column of the panel.
+template <bool FULL>
+__device__ __forceinline__ void syrk_tile(float* A, int Rp, const Panel& P, int nbe, int r0,
+                                          int c0) {
   float acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-  int base = colbase(j, Rp);
-#pragma unroll 4
-  for (int t = 0; t < nbe; ++t) {
-    const float4 x = ld4(A + base + r0);
-    const float4 y = ld4(A + base + c0);
-    const float xr[4] = {x.x, x.y, x.z, x.w};
-    const float yr[4] = {y.x, y.y, y.z, y.w};
+  const float* pr = A + P.base0 + r0;
+  const float* pc = A + P.base0 + c0;
+  if (FULL) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int t = 0; t < kNB; ++t) {
+      const float4 x = ld4(pr + t * P.stride - S4(t));
+      const float4 y = ld4(pc + t * P.stride - S4(t));
+      const float xr[4] = {x.x, x.y, x.z, x.w};
+      const float yr[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xr[a], yr[b], acc[a][b]);
-    base += Rp - ((j + t + 1) & ~3);
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xr[a], yr[b], acc[a][b]);
+    }
+  } else {
+    for (int t = 0; t < nbe; ++t) {
+      const float4 x = ld4(pr);
+      const float4 y = ld4(pc);
+      const float xr[4] = {x.x, x.y, x.z, x.w};
+      const float yr[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xr[a], yr[b], acc[a][b]);
+      const int step = P.stride - ((t + 1) & ~3);
+      pr += step;
+      pc += step;
+    }
   }
+  float* q = A + col_off(c0, Rp) - c0 + r0;  // column c0 (multiple of 4), row r0
+  const int qs = Rp - c0;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    float* p = A + colbase(c0 + b, Rp) + r0;
-    float4 v = ld4(p);
+    float4 v = ld4(q + b * qs);
     v.x -= acc[0][b];
     v.y -= acc[1][b];
     v.z -= acc[2][b];
     v.w -= acc[3][b];
-    st4(p, v);
+    st4(q + b * qs, v);
   }
 }
 
@@ -269,6 +283,7 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
   float* A = smem;
   float* xv = smem + P;
   unsigned int* sc = reinterpret_cast<unsigned int*>(xv + K4);
+  float* scr = xv + K4 + 32;  // 64-float diag scratch
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t s = p.sys_offset + blockIdx.x;
   const int64_t q = s / k;
@@ -331,15 +346,20 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
 
   float pivmin = FLT_MAX;
   bool bad = false;
-  if (warp == 0) diag_factor(A, Rp, 0, min(kNB, K4), lane, pivmin, bad);
+  if (warp == 0) {
+    if (K4 >= kNB) diag_factor<true>(A, Rp, 0, kNB, scr, lane, pivmin, bad);
+    else diag_factor<false>(A, Rp, 0, K4, scr, lane, pivmin, bad);
+  }
   __syncthreads();
 
   for (int j = 0; j < K4; j += kNB) {
     const int nbe = min(kNB, K4 - j);
     const int jn = j + nbe;
     const int nbn = min(kNB, K4 - jn);
+    const Panel Pj(j, Rp);
     // B: panel rows below the diagonal block (incl. the augmented rhs row)
-    panel_trsm<NT>(A, Rp, j, nbe, jn, tid);
+    if (nbe == kNB) panel_trsm<NT, true>(A, Rp, j, nbe, jn, tid);
+    else panel_trsm<NT, false>(A, Rp, j, nbe, jn, tid);
     __syncthreads();
     if (nbn <= 0) break;
     // C: lookahead — update the next panel's columns [jn, jn+nbn)
@@ -354,13 +374,15 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
           ++cc;
         }
         const int Ct = C0 + cc;
-        syrk_tile(A, Rp, j, nbe, (Ct + l) << 2, Ct << 2);
+        if (nbe == kNB) syrk_tile<true>(A, Rp, Pj, nbe, (Ct + l) << 2, Ct << 2);
+        else syrk_tile<false>(A, Rp, Pj, nbe, (Ct + l) << 2, Ct << 2);
       }
     }
     __syncthreads();
     // D: warp 0 factors the next diagonal block while the others update the rest
     if (warp == 0) {
-      diag_factor(A, Rp, jn, nbn, lane, pivmin, bad);
+      if (nbn == kNB) diag_factor<true>(A, Rp, jn, nbn, scr, lane, pivmin, bad);
+      else diag_factor<false>(A, Rp, jn, nbn, scr, lane, pivmin, bad);
     } else {
       const int cstart = jn + nbn;
       if (cstart < K4) {
@@ -373,7 +395,10 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
           for (; v < nrb; v += NW - 1) {
             const int r0 = cb + (v << 5) + (lr << 2);
             const int c0 = cb + (lc << 2);
-            if (c0 < K4 && r0 < Rp && r0 >= c0) syrk_tile(A, Rp, j, nbe, r0, c0);
+            if (c0 < K4 && r0 < Rp && r0 >= c0) {
+              if (nbe == kNB) syrk_tile<true>(A, Rp, Pj, nbe, r0, c0);
+              else syrk_tile<false>(A, Rp, Pj, nbe, r0, c0);
+            }
           }
           v -= nrb;
         }
