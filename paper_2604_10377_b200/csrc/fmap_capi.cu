@@ -15,6 +15,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -235,8 +236,29 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   p.rcond_min_bits = d_rcond(ctx);
   p.flags = d_flags(ctx);
 
+  // debug: FMAP_TRACE_FILE=<path> dumps per-warp clock64 phase stamps of one block
+  const char* trace_file = std::getenv("FMAP_TRACE_FILE");
+  long long* d_trace = nullptr;
+  if (trace_file) {
+    FMAP_CK(ctx, cudaMalloc(&d_trace, 8 * 1024 * sizeof(long long)));
+    FMAP_CK(ctx, cudaMemsetAsync(d_trace, 0, 8 * 1024 * sizeof(long long), ctx->stream));
+    p.trace = d_trace;
+    const char* tb = std::getenv("FMAP_TRACE_BLOCK");
+    p.trace_block = tb ? std::atoi(tb) : 0;
+  }
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, launch_chol_solve(p, mask_mode, ctx->stream));
+  if (d_trace) {
+    std::vector<long long> h(8 * 1024);
+    FMAP_CK(ctx, cudaMemcpyAsync(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (FILE* f = std::fopen(trace_file, "wb")) {
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+    cudaFree(d_trace);
+    p.trace = nullptr;
+  }
   ctx->launches++;
   if (opts.inject_fault) {
     // solver.hpp:269-273: negate the largest-|.| entry of row 0 of system 0's

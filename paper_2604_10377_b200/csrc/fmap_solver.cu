@@ -274,6 +274,14 @@ __device__ __forceinline__ void syrk_tile(float* A, int Rp, const Panel& P, int 
 
 }  // namespace
 
+// Optional phase tracing (debug): p.trace != nullptr records clock64() per warp
+// for block p.trace_block at fixed slots.
+#define FMAP_TRACE(slot)                                                        \
+  do {                                                                          \
+    if (p.trace && blockIdx.x == (unsigned)p.trace_block && lane == 0)          \
+      p.trace[warp * 1024 + (slot)] = clock64();                                \
+  } while (0)
+
 template <int MASK_MODE, int NT>
 __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
   extern __shared__ __align__(16) float smem[];
@@ -344,6 +352,7 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
   }
   __syncthreads();
 
+  FMAP_TRACE(0);
   float pivmin = FLT_MAX;
   bool bad = false;
   if (warp == 0) {
@@ -351,8 +360,10 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
     else diag_factor<false>(A, Rp, 0, K4, scr, lane, pivmin, bad);
   }
   __syncthreads();
+  FMAP_TRACE(1);
 
   for (int j = 0; j < K4; j += kNB) {
+    const int ts = 8 + (j / kNB) * 8;
     const int nbe = min(kNB, K4 - j);
     const int jn = j + nbe;
     const int nbn = min(kNB, K4 - jn);
@@ -360,7 +371,9 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
     // B: panel rows below the diagonal block (incl. the augmented rhs row)
     if (nbe == kNB) panel_trsm<NT, true>(A, Rp, j, nbe, jn, tid);
     else panel_trsm<NT, false>(A, Rp, j, nbe, jn, tid);
+    FMAP_TRACE(ts + 0);
     __syncthreads();
+    FMAP_TRACE(ts + 1);
     if (nbn <= 0) break;
     // C: lookahead — update the next panel's columns [jn, jn+nbn)
     {
@@ -378,7 +391,9 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
         else syrk_tile<false>(A, Rp, Pj, nbe, (Ct + l) << 2, Ct << 2);
       }
     }
+    FMAP_TRACE(ts + 2);
     __syncthreads();
+    FMAP_TRACE(ts + 3);
     // D: warp 0 factors the next diagonal block while the others update the rest
     if (warp == 0) {
       if (nbn == kNB) diag_factor<true>(A, Rp, jn, nbn, scr, lane, pivmin, bad);
@@ -404,8 +419,11 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
         }
       }
     }
+    FMAP_TRACE(ts + 4);
     __syncthreads();
+    FMAP_TRACE(ts + 5);
   }
+  FMAP_TRACE(1000);
 
   // ---- back substitution L^T x = y by warp 0; y sits in the augmented row ----
   if (warp != 0) return;
@@ -446,6 +464,7 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
     Crow[c] = x;
   }
   nonfinite = __any_sync(0xffffffffu, nonfinite);
+  FMAP_TRACE(1001);
   if (lane == 0) {
     const float dmax = __uint_as_float(sc[0]);
     float rc = dmax > 0.f ? pivmin / dmax : 0.f;

@@ -54,6 +54,8 @@ struct SolveParams {
   unsigned long long* fail_min;  // lowest failing global system index
   unsigned int* rcond_min_bits;  // float bits of the smallest rcond estimate
   unsigned int* flags;           // validation flags (bit 5: empty spectrum)
+  long long* trace;              // debug phase trace (nullptr = off)
+  int trace_block;
 };
 
 __host__ __device__ __forceinline__ int col_off(int c, int Rp) {
