@@ -1,5 +1,24 @@
 // Batched in-shared-memory Cholesky solver for the regularized functional map
 // (see fmap_solver.cuh for the layout and the algorithm outline).
+//
+// Work split inside one CTA (256 threads, 8 warps), per 16-column panel p
+// (columns [j, jn), next panel [jn, jn + nbn)):
+//
+//   step A  TRSM(p): L21 = A21 L11^{-T} by forward substitution, one row per
+//           thread.  Warp 7 takes the next diagonal block's rows [jn, jn+nbn),
+//           warps 0..6 the rows below (incl. the augmented rhs row).
+//   ---- barrier ----
+//   step B  warp 7 ("panel warp", the critical path): rank-16 update of the
+//           next diagonal block, then its 16x16 Cholesky; afterwards it joins
+//           the bulk.  Warps 0..6 (then 7): SYRK(p) of the trailing matrix in
+//           32x16 warp tiles of 4x4 register tiles, pulled from a shared-memory
+//           atomic counter (dynamic balance), skipping the diagonal block.
+//   ---- barrier ----
+//
+// This replaces the reference's per-system PartialPivLU
+// (/root/reference/proj/include/fmsolve/solver.hpp:147-170); for SPD systems the
+// solution is the same.  Singular = non-positive / non-finite pivot, rcond
+// estimate min(pivot)/max|diag| below the threshold, or a non-finite solution.
 #include "fmap_solver.cuh"
 
 #include <cuda_runtime.h>
@@ -11,6 +30,10 @@ namespace fmap {
 
 namespace {
 
+constexpr int kNT = 256;
+constexpr int kNW = kNT / 32;
+constexpr int kPW = kNW - 1;  // panel warp
+
 __device__ __forceinline__ int colbase(int c, int Rp) { return col_off(c, Rp) - (c & ~3); }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
@@ -19,6 +42,23 @@ __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<floa
 __device__ __forceinline__ float f4get(const float4& v, int u) {
   return u == 0 ? v.x : (u == 1 ? v.y : (u == 2 ? v.z : v.w));
 }
+
+__device__ __forceinline__ float rsqrt_fast(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // Diagonal mask entry m_i(c) for the three mask sources.
 template <int MASK_MODE>
@@ -43,10 +83,9 @@ __device__ __forceinline__ float mask_entry(const SolveParams& p, int64_t q, int
   }
 }
 
-// Offsets inside one panel.  For a panel starting at column j (multiple of 16),
-// column j+t begins at colbase(j+t) = base0 + t*stride - S4(t) with
-//   base0 = col_off(j) - j, stride = Rp - j, S4(t) = sum_{u<t}(u&~3) + (t&~3)
-// so with t known at compile time every address is one IMAD + immediate.
+// Offsets inside one panel.  Column j+t (j a multiple of 16) starts at
+//   colbase(j+t) = base0 + t*stride - S4(t),  base0 = col_off(j) - j, stride = Rp - j,
+//   S4(t) = sum_{u<t}(u&~3) + (t&~3);  element (r, j+t) is at colbase(j+t) + r.
 __host__ __device__ constexpr int S4(int t) {
   int s = 0;
   for (int u = 0; u < t; ++u) s += u & ~3;
@@ -56,172 +95,166 @@ __host__ __device__ constexpr int S4(int t) {
 struct Panel {
   int base0, stride, j;
   __device__ __forceinline__ Panel(int j_, int Rp) : base0(col_off(j_, Rp) - j_), stride(Rp - j_), j(j_) {}
-  // start of column j+t (add the absolute row index)
   __device__ __forceinline__ int col(int t) const { return base0 + t * stride - S4(t); }
 };
 
-// 8x8 lower-triangular block in registers (36 values, row-major packed).
 __host__ __device__ constexpr int tri(int r, int c) { return r * (r + 1) / 2 + c; }
 
-// Cholesky of an 8x8 SPD block followed by the in-place inverse of its factor.
-// On return t[] holds L^{-1} (lower); pivots feed pivmin / bad.
-__device__ __forceinline__ void chol8_inv(float (&t)[36], float& pivmin, bool& bad) {
+// Branch-free 8x8 Cholesky in registers (lower, row-major packed):
+// t <- L (t[tri(p,p)] = L_pp), inv[p] = 1/L_pp.
+__device__ __forceinline__ void chol8(float (&t)[36], float (&inv)[8], float& pivmin,
+                                      unsigned& bad) {
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const float d = t[tri(p, p)];
     pivmin = fminf(pivmin, d);
-    bad |= !(d > 0.f) || !(d < FLT_MAX);
-    const float sinv = rsqrtf(d);
-    t[tri(p, p)] = sinv;  // keeps 1/L_pp
+    bad |= (unsigned)(!(d > 0.f)) | (unsigned)(!(d <= FLT_MAX));
+    const float s = rsqrt_fast(d);
+    inv[p] = s;
+    t[tri(p, p)] = d * s;
 #pragma unroll
-    for (int r = p + 1; r < 8; ++r) t[tri(r, p)] *= sinv;
+    for (int r = p + 1; r < 8; ++r) t[tri(r, p)] *= s;
 #pragma unroll
     for (int c = p + 1; c < 8; ++c)
 #pragma unroll
       for (int r = c; r < 8; ++r) t[tri(r, c)] = fmaf(-t[tri(r, p)], t[tri(c, p)], t[tri(r, c)]);
   }
-  // Linv[r][p] = -Linv[r][r] * (L[r][p] Linv[p][p] + sum_{p<u<r} L[r][u] Linv[u][p]),
-  // columns left to right, rows top-down (in place).
-#pragma unroll
-  for (int p = 0; p < 8; ++p)
-#pragma unroll
-    for (int r = p + 1; r < 8; ++r) {
-      float acc = t[tri(r, p)] * t[tri(p, p)];
-#pragma unroll
-      for (int u = p + 1; u < r; ++u) acc = fmaf(t[tri(r, u)], t[tri(u, p)], acc);
-      t[tri(r, p)] = -acc * t[tri(r, r)];
-    }
 }
 
-// Factor the 16x16 diagonal block at (j, j) with warp 0 and overwrite its lower
-// triangle with L11^{-1}.  Blocked 2x2 over 8x8 sub-blocks:
-//   L00 = chol(A00); L10 = A10 L00^{-T}; A11 -= L10 L10^T; L11 = chol(A11);
-//   Linv = [[L00^{-1}, 0], [-L11^{-1} L10 L00^{-1}, L11^{-1}]].
-// The 8x8 factorizations run replicated in every lane (no communication, no
-// single-lane serialization); the row-parallel steps use lanes 0..7 and an
-// 8x8 scratch (row-major L10).  FULL = the block is 16 wide (all but possibly
-// the last panel); otherwise rows/cols >= nbe behave as identity padding.
+// Load / store the lower triangle of an 8x8 sub-block (local rows r0.., cols c0..)
+// of the panel at j, in 4-row groups (LDS.128 / STS.128).  Positions above the
+// diagonal inside the 4x4 diagonal pieces are layout junk and are written 0.
 template <bool FULL>
-__device__ __noinline__ void diag_factor(float* A, int Rp, int j, int nbe, float* scr, int lane,
-                                         float& pivmin, bool& bad) {
-  const Panel P(j, Rp);
-  auto at = [&](int r, int c) { return P.col(c) + j + r; };
-  auto ok = [&](int r, int c) { return FULL || (r < nbe && c < nbe); };
-  float t[36];
-  // 1. L00^{-1}, replicated
+__device__ __forceinline__ void ld_tri8(const float* A, const Panel& P, int r0, int c0, int nbe,
+                                        float (&t)[36]) {
 #pragma unroll
   for (int c = 0; c < 8; ++c)
 #pragma unroll
-    for (int r = c; r < 8; ++r) t[tri(r, c)] = ok(r, c) ? A[at(r, c)] : (r == c ? 1.f : 0.f);
-  chol8_inv(t, pivmin, bad);
+    for (int g = (c & ~3); g < 8; g += 4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (FULL || (c0 + c < nbe && r0 + g < nbe)) v = ld4(A + P.col(c0 + c) + P.j + r0 + g);
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
-#pragma unroll
-    for (int r = c; r < 8; ++r)
-      if (lane == (tri(r, c) & 31) && ok(r, c)) A[at(r, c)] = t[tri(r, c)];
-  // 2. lanes 0..7: row `lane` of L10 = A10[lane,:] L00^{-T}
-  if (lane < 8) {
-    float a[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] = ok(8 + lane, u) ? A[at(8 + lane, u)] : 0.f;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      float acc = 0.f;
-#pragma unroll
-      for (int u = 0; u <= c; ++u) acc = fmaf(a[u], t[tri(c, u)], acc);
-      scr[lane * 8 + c] = acc;
-    }
-  }
-  __syncwarp();
-  // 3. A11 - L10 L10^T, replicated, then L11^{-1}
-#pragma unroll
-  for (int c = 0; c < 8; ++c)
-#pragma unroll
-    for (int r = c; r < 8; ++r)
-      t[tri(r, c)] = ok(8 + r, 8 + c) ? A[at(8 + r, 8 + c)] : (r == c ? 1.f : 0.f);
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    float col[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) col[r] = scr[r * 8 + u];
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-#pragma unroll
-      for (int r = c; r < 8; ++r) t[tri(r, c)] = fmaf(-col[r], col[c], t[tri(r, c)]);
-  }
-  chol8_inv(t, pivmin, bad);
-#pragma unroll
-  for (int c = 0; c < 8; ++c)
-#pragma unroll
-    for (int r = c; r < 8; ++r)
-      if (lane == (tri(r, c) & 31) && ok(8 + r, 8 + c)) A[at(8 + r, 8 + c)] = t[tri(r, c)];
-  __syncwarp();
-  // 4. lanes 0..7: row `lane` of X = -(L11^{-1} L10) L00^{-1}
-  if (lane < 8) {
-    float y[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) y[c] = 0.f;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (u <= lane) {
-        const float li = A[at(8 + lane, 8 + u)];  // L11^{-1}[lane][u]
-        const float4 l0 = *reinterpret_cast<const float4*>(scr + u * 8);
-        const float4 l1 = *reinterpret_cast<const float4*>(scr + u * 8 + 4);
-        y[0] = fmaf(li, l0.x, y[0]);
-        y[1] = fmaf(li, l0.y, y[1]);
-        y[2] = fmaf(li, l0.z, y[2]);
-        y[3] = fmaf(li, l0.w, y[3]);
-        y[4] = fmaf(li, l1.x, y[4]);
-        y[5] = fmaf(li, l1.y, y[5]);
-        y[6] = fmaf(li, l1.z, y[6]);
-        y[7] = fmaf(li, l1.w, y[7]);
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      float acc = 0.f;
-#pragma unroll
-      for (int u = c; u < 8; ++u) acc = fmaf(y[u], A[at(u, c)], acc);  // L00^{-1}[u][c]
-      if (ok(8 + lane, c)) A[at(8 + lane, c)] = -acc;
-    }
-  }
-  __syncwarp();
-}
-
-// Rows [r_lo, Rp) of panel [j, j+nbe):  L21 = A21 * L11^{-T}  (L11^{-1} stored in
-// the diagonal block).  One row per thread; L11^{-1} reads are warp broadcasts.
-template <int NT, bool FULL>
-__device__ __forceinline__ void panel_trsm(float* A, int Rp, int j, int nbe, int r_lo, int tid) {
-  const Panel P(j, Rp);
-  for (int r = r_lo + tid; r < Rp; r += NT) {
-    float a[kNB], x[kNB];
-#pragma unroll
-    for (int t = 0; t < kNB; ++t) {
-      a[t] = (FULL || t < nbe) ? A[P.col(t) + r] : 0.f;
-      x[t] = 0.f;
-    }
-#pragma unroll
-    for (int t = 0; t < kNB; ++t) {
-      if (FULL || t < nbe) {
-#pragma unroll
-        for (int c4 = (t & ~3); c4 < kNB; c4 += 4) {
-          if (FULL || c4 < nbe) {
-            const float4 l = ld4(A + P.col(t) + j + c4);  // Linv[c4..c4+3][t]
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (c4 + u >= t) x[c4 + u] = fmaf(a[t], f4get(l, u), x[c4 + u]);
-          }
+      for (int u = 0; u < 4; ++u) {
+        const int r = g + u;
+        if (r >= c) {
+          float x = f4get(v, u);
+          if (!FULL && !(c0 + c < nbe && r0 + r < nbe)) x = (r == c) ? 1.f : 0.f;
+          t[tri(r, c)] = x;
         }
       }
     }
+}
+
+template <bool FULL>
+__device__ __forceinline__ void st_tri8(float* A, const Panel& P, int r0, int c0, int nbe,
+                                        const float (&t)[36]) {
 #pragma unroll
-    for (int c = 0; c < kNB; ++c)
-      if (FULL || c < nbe) A[P.col(c) + r] = x[c];
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int g = (c & ~3); g < 8; g += 4) {
+      if (FULL || (c0 + c < nbe && r0 + g < nbe)) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = (g + u >= c) ? t[tri(g + u, c)] : 0.f;
+        st4(A + P.col(c0 + c) + P.j + r0 + g, make_float4(v[0], v[1], v[2], v[3]));
+      }
+    }
+}
+
+// Cholesky of the 16x16 diagonal block at (j, j) by one warp (all lanes):
+//   L00 = chol(A00);  L10 = A10 L00^{-T};  L11 = chol(A11 - L10 L10^T)
+// The 8x8 factorizations run replicated in every lane (no communication); the
+// L10 rows are computed by lanes 0..7 and exchanged through `scr` (8x8 row-major).
+// Writes L into the block and 1/L_tt into sinv[j..j+16).
+template <bool FULL>
+__device__ __noinline__ void diag16(float* A, int Rp, int j, int nbe, float* scr, float* sinv,
+                                    int lane, float& pivmin, unsigned& bad) {
+  const Panel P(j, Rp);
+  float t[36], inv0[8], inv1[8];
+  ld_tri8<FULL>(A, P, 0, 0, nbe, t);
+  chol8(t, inv0, pivmin, bad);
+  if (lane == 0) st_tri8<FULL>(A, P, 0, 0, nbe, t);
+  {  // L10 row (8 + rr): forward substitution against L00 (every lane, row lane&7)
+    const int rr = lane & 7;
+    float a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      a[u] = (FULL || (8 + rr < nbe && u < nbe)) ? A[P.col(u) + j + 8 + rr] : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a[u] *= inv0[u];
+#pragma unroll
+      for (int v = u + 1; v < 8; ++v) a[v] = fmaf(-a[u], t[tri(v, u)], a[v]);
+    }
+    if (lane < 8) {
+      st4(scr + rr * 8, make_float4(a[0], a[1], a[2], a[3]));
+      st4(scr + rr * 8 + 4, make_float4(a[4], a[5], a[6], a[7]));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (FULL || (8 + rr < nbe && u < nbe)) A[P.col(u) + j + 8 + rr] = a[u];
+    }
   }
+  __syncwarp();
+  ld_tri8<FULL>(A, P, 8, 8, nbe, t);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const float4 x0 = ld4(scr + r * 8), x1 = ld4(scr + r * 8 + 4);
+    const float lr[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int c = 0; c <= r; ++c) {
+      const float4 y0 = ld4(scr + c * 8), y1 = ld4(scr + c * 8 + 4);
+      float acc = t[tri(r, c)];
+      acc = fmaf(-lr[0], y0.x, acc);
+      acc = fmaf(-lr[1], y0.y, acc);
+      acc = fmaf(-lr[2], y0.z, acc);
+      acc = fmaf(-lr[3], y0.w, acc);
+      acc = fmaf(-lr[4], y1.x, acc);
+      acc = fmaf(-lr[5], y1.y, acc);
+      acc = fmaf(-lr[6], y1.z, acc);
+      acc = fmaf(-lr[7], y1.w, acc);
+      t[tri(r, c)] = acc;
+    }
+  }
+  chol8(t, inv1, pivmin, bad);
+  if (lane == 0) {
+    st_tri8<FULL>(A, P, 8, 8, nbe, t);
+    st4(sinv + j, make_float4(inv0[0], inv0[1], inv0[2], inv0[3]));
+    st4(sinv + j + 4, make_float4(inv0[4], inv0[5], inv0[6], inv0[7]));
+    st4(sinv + j + 8, make_float4(inv1[0], inv1[1], inv1[2], inv1[3]));
+    st4(sinv + j + 12, make_float4(inv1[4], inv1[5], inv1[6], inv1[7]));
+  }
+  __syncwarp();
+}
+
+// TRSM of one row r of panel [j, j+nbe): x = a L11^{-T} by forward substitution
+// (right-looking over the columns of L11, LDS.128 broadcasts).
+template <bool FULL>
+__device__ __forceinline__ void trsm_row(float* A, const Panel& P, const float* sinv, int nbe,
+                                         int r) {
+  float a[kNB];
+#pragma unroll
+  for (int t = 0; t < kNB; ++t) a[t] = (FULL || t < nbe) ? A[P.col(t) + r] : 0.f;
+#pragma unroll
+  for (int u = 0; u < kNB; ++u) {
+    if (FULL || u < nbe) {
+      a[u] *= sinv[P.j + u];
+#pragma unroll
+      for (int g = ((u + 1) & ~3); g < kNB; g += 4) {
+        if (FULL || g < nbe) {
+          const float4 l = ld4(A + P.col(u) + P.j + g);  // L11[g..g+3][u]
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+            if (g + w > u) a[g + w] = fmaf(-a[u], f4get(l, w), a[g + w]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kNB; ++t)
+    if (FULL || t < nbe) A[P.col(t) + r] = a[t];
 }
 
 // 4x4 register tile: A[r0..r0+3][c0..c0+3] -= sum_{t<nbe} L[r][j+t] L[c][j+t].
-// Operand pointers advance by stride - ((t+1)&~3) per column of the panel.
 template <bool FULL>
 __device__ __forceinline__ void syrk_tile(float* A, int Rp, const Panel& P, int nbe, int r0,
                                           int c0) {
@@ -272,92 +305,125 @@ __device__ __forceinline__ void syrk_tile(float* A, int Rp, const Panel& P, int 
   }
 }
 
+// Bulk SYRK(p) over columns [c_lo, K4), rows >= column, skipping the diagonal
+// block [db, db+dbn)^2 (handled by the panel warp).  Warp tiles of 32 rows x 16
+// columns (lanes 8 x 4, 4x4 each) are pulled from *counter.
+template <bool FULL>
+__device__ __forceinline__ void syrk_bulk(float* A, int Rp, int K4, const Panel& P, int nbe,
+                                          int c_lo, int db, int dbn, int* counter, int lane) {
+  const int ncb = (K4 - c_lo + 15) >> 4;
+  const int lr = lane & 7, lc = lane >> 3;
+  while (true) {
+    int w = 0;
+    if (lane == 0) w = atomicAdd(counter, 1);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    int u = 0, cb = c_lo, nrb = (Rp - cb + 31) >> 5;
+    while (u < ncb && w >= nrb) {
+      w -= nrb;
+      ++u;
+      cb += 16;
+      nrb = (Rp - cb + 31) >> 5;
+    }
+    if (u >= ncb) break;
+    const int r0 = cb + (w << 5) + (lr << 2);
+    const int c0 = cb + (lc << 2);
+    const bool in_diag = (r0 < db + dbn) && (c0 < db + dbn);
+    if (c0 < K4 && r0 < Rp && r0 >= c0 && !in_diag) syrk_tile<FULL>(A, Rp, P, nbe, r0, c0);
+  }
+}
+
 }  // namespace
 
 // Optional phase tracing (debug): p.trace != nullptr records clock64() per warp
-// for block p.trace_block at fixed slots.
+// for block p.trace_block at fixed slots (end-of-work stamps only).
 #define FMAP_TRACE(slot)                                                        \
   do {                                                                          \
     if (p.trace && blockIdx.x == (unsigned)p.trace_block && lane == 0)          \
       p.trace[warp * 1024 + (slot)] = clock64();                                \
   } while (0)
 
-template <int MASK_MODE, int NT>
-__global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
+template <int MASK_MODE>
+__global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
   extern __shared__ __align__(16) float smem[];
-  constexpr int NW = NT / 32;
   const int k = p.k, K4 = p.K4, Rp = p.Rp;
-  const int P = packed_size(K4);
+  const int P_ = packed_size(K4);
   float* A = smem;
-  float* xv = smem + P;
-  unsigned int* sc = reinterpret_cast<unsigned int*>(xv + K4);
-  float* scr = xv + K4 + 32;  // 64-float diag scratch
+  float* xv = smem + P_;   // K4: back-substitution vector
+  float* sinv = xv + K4;   // K4: 1/L_tt
+  float* scr = sinv + K4;  // 64: diag scratch
+  unsigned* sc = reinterpret_cast<unsigned*>(scr + 64);  // 32 words of scalars
+  int* counter = reinterpret_cast<int*>(sc + 4);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t s = p.sys_offset + blockIdx.x;
   const int64_t q = s / k;
   const int i = (int)(s - q * k);
 
   if (tid == 0) {
-    sc[0] = 0u;  // max diagonal (float bits, non-negative)
+    sc[0] = 0u;  // max |diag| (float bits)
     sc[1] = 0u;  // ev_max bits
+    *counter = 0;
   }
-  __syncthreads();
-
+  // ---- stage G (row c of G == column c, symmetric) with cp.async; padding + rhs row ----
+  {
+    const float* Gq = p.gram + (size_t)q * k * k;
+    const float* Rrow = p.rhs + ((size_t)q * k + i) * k;
+    const bool vec = (k & 3) == 0;
+    for (int c = warp; c < K4; c += kNW) {
+      const int c4 = c & ~3;
+      float* col = A + colbase(c, Rp);
+      if (c < k) {
+        const float* g = Gq + (size_t)c * k;
+        if (vec) {
+          for (int r = c4 + 4 * lane; r < k; r += 128) cp_async16(col + r, g + r);
+        } else {
+          for (int r = c4 + lane; r < k; r += 32) cp_async4(col + r, g + r);
+        }
+        for (int r = k + lane; r < Rp; r += 32)
+          col[r] = (r == K4) ? (p.rhs_unit < 0 ? Rrow[c] : (c == p.rhs_unit ? 1.f : 0.f)) : 0.f;
+      } else {
+        for (int r = c4 + lane; r < Rp; r += 32) col[r] = (r == c) ? 1.f : 0.f;
+      }
+    }
+  }
   float ev_max = 0.f;
   if constexpr (MASK_MODE == 1) {
     float m = 0.f;
-    for (int c = tid; c < k; c += NT)
+    for (int c = tid; c < k; c += kNT)
       m = fmaxf(m, fmaxf(p.ev1[(size_t)q * k + c], p.ev2[(size_t)q * k + c]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __syncthreads();  // sc[] initialised
     if (lane == 0) atomicMax(&sc[1], __float_as_uint(m));
-    __syncthreads();
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if constexpr (MASK_MODE == 1) {
     ev_max = __uint_as_float(sc[1]);
     if (!(ev_max > 0.f)) {
       if (tid == 0) atomicOr(p.flags, 32u);
       return;  // masks.hpp:59: needs a non-zero spectrum to normalize by
     }
   }
-
-  // ---- stage S = G + lambda*diag(m_i) + ridge*I and the rhs row into smem ----
-  {
-    const float* Gq = p.gram + (size_t)q * k * k;
-    const float* Rrow = p.rhs + ((size_t)q * k + i) * k;
+  {  // diagonal: + lambda * m_i(c) + ridge
     float dmax = 0.f;
-    for (int c = warp; c < K4; c += NW) {
-      const int c4 = c & ~3;
-      float* col = A + colbase(c, Rp);
-      if (c < k) {
-        const float* g = Gq + (size_t)c * k;  // row c of G == column c (symmetric)
-        for (int r = c4 + lane; r < Rp; r += 32) {
-          float v = 0.f;
-          if (r < k) {
-            v = g[r];
-            if (r == c) {
-              v += p.lambda * mask_entry<MASK_MODE>(p, q, i, c, ev_max) + p.ridge;
-              dmax = fmaxf(dmax, fabsf(v));
-            }
-          } else if (r == K4) {
-            v = p.rhs_unit < 0 ? Rrow[c] : (c == p.rhs_unit ? 1.f : 0.f);
-          }
-          col[r] = v;
-        }
-      } else {
-        for (int r = c4 + lane; r < Rp; r += 32) col[r] = (r == c) ? 1.f : 0.f;
-      }
+    for (int c = tid; c < k; c += kNT) {
+      float* d = A + colbase(c, Rp) + c;
+      const float v = *d + (p.lambda * mask_entry<MASK_MODE>(p, q, i, c, ev_max) + p.ridge);
+      *d = v;
+      dmax = fmaxf(dmax, fabsf(v));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     if (lane == 0) atomicMax(&sc[0], __float_as_uint(dmax));
   }
   __syncthreads();
-
   FMAP_TRACE(0);
+
   float pivmin = FLT_MAX;
-  bool bad = false;
-  if (warp == 0) {
-    if (K4 >= kNB) diag_factor<true>(A, Rp, 0, kNB, scr, lane, pivmin, bad);
-    else diag_factor<false>(A, Rp, 0, K4, scr, lane, pivmin, bad);
+  unsigned bad = 0u;
+  if (warp == kPW) {
+    if (K4 >= kNB) diag16<true>(A, Rp, 0, kNB, scr, sinv, lane, pivmin, bad);
+    else diag16<false>(A, Rp, 0, K4, scr, sinv, lane, pivmin, bad);
   }
   __syncthreads();
   FMAP_TRACE(1);
@@ -368,80 +434,89 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
     const int jn = j + nbe;
     const int nbn = min(kNB, K4 - jn);
     const Panel Pj(j, Rp);
-    // B: panel rows below the diagonal block (incl. the augmented rhs row)
-    if (nbe == kNB) panel_trsm<NT, true>(A, Rp, j, nbe, jn, tid);
-    else panel_trsm<NT, false>(A, Rp, j, nbe, jn, tid);
+    const bool full = nbe == kNB;
+    // A: TRSM(p).  Panel warp: the next diagonal block's rows; others: the rest.
+    if (warp == kPW) {
+      if (lane < nbn) {
+        if (full) trsm_row<true>(A, Pj, sinv, nbe, jn + lane);
+        else trsm_row<false>(A, Pj, sinv, nbe, jn + lane);
+      }
+    } else {
+      for (int r = jn + max(nbn, 0) + tid; r < Rp; r += kNT - 32) {
+        if (full) trsm_row<true>(A, Pj, sinv, nbe, r);
+        else trsm_row<false>(A, Pj, sinv, nbe, r);
+      }
+    }
+    if (tid == 0) *counter = 0;
     FMAP_TRACE(ts + 0);
     __syncthreads();
-    FMAP_TRACE(ts + 1);
     if (nbn <= 0) break;
-    // C: lookahead — update the next panel's columns [jn, jn+nbn)
-    {
-      const int C0 = jn >> 2, nR = Rp >> 2, ncol = nbn >> 2;
-      int ntile = 0;
-      for (int cc = 0; cc < ncol; ++cc) ntile += nR - (C0 + cc);
-      for (int L = tid; L < ntile; L += NT) {
-        int cc = 0, l = L;
-        while (l >= nR - (C0 + cc)) {
-          l -= nR - (C0 + cc);
-          ++cc;
+    // B: panel warp -> diagonal-block update + Cholesky, then bulk; others -> bulk SYRK(p)
+    if (warp == kPW) {
+      const int nt4 = nbn >> 2;  // 1..4 tile rows in the diagonal block
+      const int tcount = nt4 * (nt4 + 1) / 2;
+      if (lane < tcount) {
+        int a = 0, l = lane;
+        while (l > a) {
+          l -= a + 1;
+          ++a;
         }
-        const int Ct = C0 + cc;
-        if (nbe == kNB) syrk_tile<true>(A, Rp, Pj, nbe, (Ct + l) << 2, Ct << 2);
-        else syrk_tile<false>(A, Rp, Pj, nbe, (Ct + l) << 2, Ct << 2);
+        if (full) syrk_tile<true>(A, Rp, Pj, nbe, jn + 4 * a, jn + 4 * l);
+        else syrk_tile<false>(A, Rp, Pj, nbe, jn + 4 * a, jn + 4 * l);
       }
+      __syncwarp();
+      if (nbn == kNB) diag16<true>(A, Rp, jn, nbn, scr, sinv, lane, pivmin, bad);
+      else diag16<false>(A, Rp, jn, nbn, scr, sinv, lane, pivmin, bad);
+      FMAP_TRACE(ts + 2);
     }
-    FMAP_TRACE(ts + 2);
-    __syncthreads();
-    FMAP_TRACE(ts + 3);
-    // D: warp 0 factors the next diagonal block while the others update the rest
-    if (warp == 0) {
-      if (nbn == kNB) diag_factor<true>(A, Rp, jn, nbn, scr, lane, pivmin, bad);
-      else diag_factor<false>(A, Rp, jn, nbn, scr, lane, pivmin, bad);
-    } else {
-      const int cstart = jn + nbn;
-      if (cstart < K4) {
-        const int ncb = (K4 - cstart + 15) >> 4;
-        const int lr = lane & 7, lc = lane >> 3;
-        int v = warp - 1;
-        for (int u = 0; u < ncb; ++u) {
-          const int cb = cstart + (u << 4);
-          const int nrb = (Rp - cb + 31) >> 5;
-          for (; v < nrb; v += NW - 1) {
-            const int r0 = cb + (v << 5) + (lr << 2);
-            const int c0 = cb + (lc << 2);
-            if (c0 < K4 && r0 < Rp && r0 >= c0) {
-              if (nbe == kNB) syrk_tile<true>(A, Rp, Pj, nbe, r0, c0);
-              else syrk_tile<false>(A, Rp, Pj, nbe, r0, c0);
-            }
-          }
-          v -= nrb;
-        }
-      }
-    }
+    if (full) syrk_bulk<true>(A, Rp, K4, Pj, nbe, jn, jn, nbn, counter, lane);
+    else syrk_bulk<false>(A, Rp, K4, Pj, nbe, jn, jn, nbn, counter, lane);
     FMAP_TRACE(ts + 4);
     __syncthreads();
-    FMAP_TRACE(ts + 5);
   }
   FMAP_TRACE(1000);
 
-  // ---- back substitution L^T x = y by warp 0; y sits in the augmented row ----
-  if (warp != 0) return;
-  for (int c = lane; c < K4; c += 32) xv[c] = A[colbase(c, Rp) + K4];
-  __syncwarp();
+  // ---- back substitution L^T x = y (y = augmented row K4) ----
+  for (int c = tid; c < K4; c += kNT) xv[c] = A[colbase(c, Rp) + K4];
+  __syncthreads();
   for (int jb = ((K4 - 1) / kNB) * kNB; jb >= 0; jb -= kNB) {
     const int nbe = min(kNB, K4 - jb);
-    float xc = 0.f;
-    if (lane < nbe) {
-      const int base = colbase(jb + lane, Rp) + jb;
+    if (warp == kPW) {
+      // x_B = L_BB^{-T} y_B, replicated in every lane (descending columns)
+      const Panel P(jb, Rp);
+      float y[kNB];
 #pragma unroll
-      for (int r = 0; r < kNB; ++r)
-        if (r >= lane && r < nbe) xc = fmaf(A[base + r], xv[jb + r], xc);
+      for (int g = 0; g < kNB; g += 4) {
+        const float4 v = (g < nbe) ? ld4(xv + jb + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+        y[g] = v.x;
+        y[g + 1] = v.y;
+        y[g + 2] = v.z;
+        y[g + 3] = v.w;
+      }
+#pragma unroll
+      for (int c = kNB - 1; c >= 0; --c) {
+        if (c < nbe) {
+          float acc = y[c];
+#pragma unroll
+          for (int g = ((c + 1) & ~3); g < kNB; g += 4) {
+            if (g < nbe) {
+              const float4 l = ld4(A + P.col(c) + jb + g);  // L[g..g+3][c]
+#pragma unroll
+              for (int w = 0; w < 4; ++w)
+                if (g + w > c) acc = fmaf(-f4get(l, w), y[g + w], acc);
+            }
+          }
+          y[c] = acc * sinv[jb + c];
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int g = 0; g < kNB; g += 4)
+          if (g < nbe) st4(xv + jb + g, make_float4(y[g], y[g + 1], y[g + 2], y[g + 3]));
+      }
     }
-    __syncwarp();
-    if (lane < nbe) xv[jb + lane] = xc;
-    __syncwarp();
-    for (int c = lane; c < jb; c += 32) {
+    __syncthreads();
+    for (int c = tid; c < jb; c += kNT) {
       const float* col = A + colbase(c, Rp) + jb;
       float acc = 0.f;
       for (int r = 0; r < nbe; r += 4) {
@@ -454,43 +529,43 @@ __global__ void __launch_bounds__(NT, 2) chol_solve_kernel(SolveParams p) {
       }
       xv[c] -= acc;
     }
-    __syncwarp();
+    __syncthreads();
   }
   bool nonfinite = false;
   float* Crow = p.C + ((size_t)q * k + i) * k;
-  for (int c = lane; c < k; c += 32) {
+  for (int c = tid; c < k; c += kNT) {
     const float x = xv[c];
     nonfinite |= !(fabsf(x) <= FLT_MAX);
     Crow[c] = x;
   }
-  nonfinite = __any_sync(0xffffffffu, nonfinite);
-  FMAP_TRACE(1001);
-  if (lane == 0) {
-    const float dmax = __uint_as_float(sc[0]);
-    float rc = dmax > 0.f ? pivmin / dmax : 0.f;
-    if (!(rc >= 0.f)) rc = 0.f;
-    if (bad || nonfinite || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)s);
-    atomicMin(p.rcond_min_bits, __float_as_uint(rc));
+  if (nonfinite) atomicMin(p.fail_min, (unsigned long long)s);
+  if (warp == kPW) {
+    FMAP_TRACE(1001);
+    if (lane == 0) {
+      const float dmax = __uint_as_float(sc[0]);
+      float rc = dmax > 0.f ? pivmin / dmax : 0.f;
+      if (!(rc >= 0.f)) rc = 0.f;
+      if (bad || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)s);
+      atomicMin(p.rcond_min_bits, __float_as_uint(rc));
+    }
   }
 }
 
 // Host-side launcher.
 cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream) {
-  constexpr int NT = 256;
   const size_t smem = solver_smem_bytes(p.k);
   if (p.nsys <= 0) return cudaSuccess;
   void (*fn)(SolveParams) = nullptr;
   switch (mask_mode) {
-    case 0: fn = chol_solve_kernel<0, NT>; break;
-    case 1: fn = chol_solve_kernel<1, NT>; break;
-    default: fn = chol_solve_kernel<2, NT>; break;
+    case 0: fn = chol_solve_kernel<0>; break;
+    case 1: fn = chol_solve_kernel<1>; break;
+    default: fn = chol_solve_kernel<2>; break;
   }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // ask for the full shared-memory carveout so two ~86 KB CTAs co-reside per SM
   e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  fn<<<(unsigned)p.nsys, NT, smem, stream>>>(p);
+  fn<<<(unsigned)p.nsys, kNT, smem, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -1,21 +1,34 @@
-"""Print per-panel phase durations from an FMAP_TRACE_FILE dump (8 warps x 1024 int64)."""
+"""Per-panel phase durations from an FMAP_TRACE_FILE dump (8 warps x 1024 int64).
+
+End-of-work stamps only (a clock64() right after __syncthreads() records the
+barrier's issue time, not its release):  slot 0 staging done, 1 first diag done,
+8+8p+0 TRSM(p) done, +2 panel warp's diag(p+1) done, +4 bulk SYRK(p) done,
+1000 factorization done, 1001 back-substitution done (panel warp)."""
 import sys
+
 import numpy as np
 
 t = np.fromfile(sys.argv[1], dtype=np.int64).reshape(8, 1024)
-t0 = t[0, 0]
-print("setup (load+diag0): ", t[0, 1] - t0)
-print("panel  B_max  B_w0  barB   C_max  barC   D_w0  D_others_max  barD  (cycles)")
+PW = 7
+t0 = t[:, 0].min()
+print("staging:", t[:, 0].max() - t0, " first diag:", t[PW, 1] - t[:, 0].max())
+prev = t[:, 1].max()
+print("panel    trsm   diag(w7)   bulk_end   panel_total")
 p = 0
 while True:
     b = 8 + 8 * p
-    if t[0, b] == 0:
+    if t[:, b].max() == 0:
         break
-    start = t[0, b - 3] if p > 0 else t[0, 1]
-    row = [t[:, b].max() - start, t[0, b] - start, t[0, b + 1] - t[:, b].max()]
-    if t[0, b + 2]:
-        row += [t[:, b + 2].max() - t[0, b + 1], t[0, b + 3] - t[:, b + 2].max(),
-                t[0, b + 4] - t[0, b + 3], t[1:, b + 4].max() - t[0, b + 3], t[0, b + 5] - t[:, b + 4].max()]
-    print(p, *row)
+    eA = t[:, b].max()
+    row = [eA - prev]
+    if t[:, b + 4].max():
+        row += [t[PW, b + 2] - eA, t[:, b + 4].max() - eA]
+        nxt = t[:, b + 4].max()
+    else:
+        row += [0, 0]
+        nxt = eA
+    row.append(nxt - prev)
+    print(f"{p:5d}", "  ".join(f"{x:9d}" for x in row))
+    prev = nxt
     p += 1
-print("backsub:", t[0, 1001] - t[0, 1000], " total:", t[0, 1001] - t0)
+print("backsub:", t[PW, 1001] - t[:, 1000].max(), " total:", t[PW, 1001] - t0)
