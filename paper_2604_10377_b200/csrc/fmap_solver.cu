@@ -195,24 +195,56 @@ __device__ __noinline__ void diag16(float* A, int Rp, int j, int nbe, float* scr
     }
   }
   __syncwarp();
-  ld_tri8<FULL>(A, P, 8, 8, nbe, t);
+  // A11 - L10 L10^T: lane e < 36 computes packed element e (r, c) and publishes
+  // it through scr[64..100); then every lane loads the updated block.
+  {
+    int r = 0, c = lane;
+    while (c > r) {
+      c -= r + 1;
+      ++r;
+    }
+    if (lane < 36) {
+      const float4 a0 = ld4(scr + r * 8), a1 = ld4(scr + r * 8 + 4);
+      const float4 b0 = ld4(scr + c * 8), b1 = ld4(scr + c * 8 + 4);
+      float acc = (FULL || (8 + r < nbe && 8 + c < nbe)) ? A[P.col(8 + c) + j + 8 + r] : (r == c ? 1.f : 0.f);
+      acc = fmaf(-a0.x, b0.x, acc);
+      acc = fmaf(-a0.y, b0.y, acc);
+      acc = fmaf(-a0.z, b0.z, acc);
+      acc = fmaf(-a0.w, b0.w, acc);
+      acc = fmaf(-a1.x, b1.x, acc);
+      acc = fmaf(-a1.y, b1.y, acc);
+      acc = fmaf(-a1.z, b1.z, acc);
+      acc = fmaf(-a1.w, b1.w, acc);
+      scr[64 + lane] = acc;
+    }
+    __syncwarp();
+    if (lane < 4) {  // lanes 32..35 are out of range; 4 lanes cover the last four
+      int rr = 0, cc = 32 + lane;
+      while (cc > rr) {
+        cc -= rr + 1;
+        ++rr;
+      }
+      const float4 a0 = ld4(scr + rr * 8), a1 = ld4(scr + rr * 8 + 4);
+      const float4 b0 = ld4(scr + cc * 8), b1 = ld4(scr + cc * 8 + 4);
+      float acc = (FULL || (8 + rr < nbe && 8 + cc < nbe)) ? A[P.col(8 + cc) + j + 8 + rr] : (rr == cc ? 1.f : 0.f);
+      acc = fmaf(-a0.x, b0.x, acc);
+      acc = fmaf(-a0.y, b0.y, acc);
+      acc = fmaf(-a0.z, b0.z, acc);
+      acc = fmaf(-a0.w, b0.w, acc);
+      acc = fmaf(-a1.x, b1.x, acc);
+      acc = fmaf(-a1.y, b1.y, acc);
+      acc = fmaf(-a1.z, b1.z, acc);
+      acc = fmaf(-a1.w, b1.w, acc);
+      scr[96 + lane] = acc;
+    }
+    __syncwarp();
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const float4 x0 = ld4(scr + r * 8), x1 = ld4(scr + r * 8 + 4);
-    const float lr[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-    for (int c = 0; c <= r; ++c) {
-      const float4 y0 = ld4(scr + c * 8), y1 = ld4(scr + c * 8 + 4);
-      float acc = t[tri(r, c)];
-      acc = fmaf(-lr[0], y0.x, acc);
-      acc = fmaf(-lr[1], y0.y, acc);
-      acc = fmaf(-lr[2], y0.z, acc);
-      acc = fmaf(-lr[3], y0.w, acc);
-      acc = fmaf(-lr[4], y1.x, acc);
-      acc = fmaf(-lr[5], y1.y, acc);
-      acc = fmaf(-lr[6], y1.z, acc);
-      acc = fmaf(-lr[7], y1.w, acc);
-      t[tri(r, c)] = acc;
+    for (int e = 0; e < 36; e += 4) {
+      const float4 v = ld4(scr + 64 + e);
+      t[e] = v.x;
+      t[e + 1] = v.y;
+      t[e + 2] = v.z;
+      t[e + 3] = v.w;
     }
   }
   chol8(t, inv1, pivmin, bad);
@@ -350,8 +382,8 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
   float* A = smem;
   float* xv = smem + P_;   // K4: back-substitution vector
   float* sinv = xv + K4;   // K4: 1/L_tt
-  float* scr = sinv + K4;  // 64: diag scratch
-  unsigned* sc = reinterpret_cast<unsigned*>(scr + 64);  // 32 words of scalars
+  float* scr = sinv + K4;  // 104: diag scratch (L10 8x8 + updated A11)
+  unsigned* sc = reinterpret_cast<unsigned*>(scr + 104);  // 32 words of scalars
   int* counter = reinterpret_cast<int*>(sc + 4);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t s = p.sys_offset + blockIdx.x;
@@ -476,78 +508,71 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
   }
   FMAP_TRACE(1000);
 
-  // ---- back substitution L^T x = y (y = augmented row K4) ----
-  for (int c = tid; c < K4; c += kNT) xv[c] = A[colbase(c, Rp) + K4];
-  __syncthreads();
+  // ---- back substitution L^T x = y (y = augmented row K4), panel warp only ----
+  // Per 16-row block B (descending): x_B = L_BB^{-T} y_B right-looking and
+  // replicated in every lane (FMUL -> FFMA chain per column), then the lanes
+  // update y_c -= L[B][c] . x_B for the columns c < jb.  No CTA barriers.
+  if (warp != kPW) return;
+  for (int c = lane; c < K4; c += 32) xv[c] = A[colbase(c, Rp) + K4];
+  __syncwarp();
   for (int jb = ((K4 - 1) / kNB) * kNB; jb >= 0; jb -= kNB) {
     const int nbe = min(kNB, K4 - jb);
-    if (warp == kPW) {
-      // x_B = L_BB^{-T} y_B, replicated in every lane (descending columns)
-      const Panel P(jb, Rp);
-      float y[kNB];
+    const Panel P(jb, Rp);
+    float y[kNB];
 #pragma unroll
-      for (int g = 0; g < kNB; g += 4) {
-        const float4 v = (g < nbe) ? ld4(xv + jb + g) : make_float4(0.f, 0.f, 0.f, 0.f);
-        y[g] = v.x;
-        y[g + 1] = v.y;
-        y[g + 2] = v.z;
-        y[g + 3] = v.w;
-      }
+    for (int g = 0; g < kNB; g += 4) {
+      const float4 v = (g < nbe) ? ld4(xv + jb + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+      y[g] = v.x;
+      y[g + 1] = v.y;
+      y[g + 2] = v.z;
+      y[g + 3] = v.w;
+    }
 #pragma unroll
-      for (int c = kNB - 1; c >= 0; --c) {
-        if (c < nbe) {
-          float acc = y[c];
+    for (int c = kNB - 1; c >= 0; --c) {
+      if (c < nbe) {
+        y[c] *= sinv[jb + c];  // x_c
 #pragma unroll
-          for (int g = ((c + 1) & ~3); g < kNB; g += 4) {
-            if (g < nbe) {
-              const float4 l = ld4(A + P.col(c) + jb + g);  // L[g..g+3][c]
-#pragma unroll
-              for (int w = 0; w < 4; ++w)
-                if (g + w > c) acc = fmaf(-f4get(l, w), y[g + w], acc);
-            }
-          }
-          y[c] = acc * sinv[jb + c];
-        }
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int g = 0; g < kNB; g += 4)
-          if (g < nbe) st4(xv + jb + g, make_float4(y[g], y[g + 1], y[g + 2], y[g + 3]));
+        for (int g = 0; g < c; ++g) y[g] = fmaf(-A[P.col(g) + jb + c], y[c], y[g]);  // L[c][g]
       }
     }
-    __syncthreads();
-    for (int c = tid; c < jb; c += kNT) {
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int g = 0; g < kNB; g += 4)
+        if (g < nbe) st4(xv + jb + g, make_float4(y[g], y[g + 1], y[g + 2], y[g + 3]));
+    }
+    for (int c = lane; c < jb; c += 32) {
       const float* col = A + colbase(c, Rp) + jb;
       float acc = 0.f;
-      for (int r = 0; r < nbe; r += 4) {
-        const float4 l = ld4(col + r);
-        const float4 xx = ld4(xv + jb + r);
-        acc = fmaf(l.x, xx.x, acc);
-        acc = fmaf(l.y, xx.y, acc);
-        acc = fmaf(l.z, xx.z, acc);
-        acc = fmaf(l.w, xx.w, acc);
+#pragma unroll
+      for (int r = 0; r < kNB; r += 4) {
+        if (r < nbe) {
+          const float4 l = ld4(col + r);
+          acc = fmaf(l.x, y[r], acc);
+          acc = fmaf(l.y, y[r + 1], acc);
+          acc = fmaf(l.z, y[r + 2], acc);
+          acc = fmaf(l.w, y[r + 3], acc);
+        }
       }
       xv[c] -= acc;
     }
-    __syncthreads();
+    __syncwarp();
   }
+  FMAP_TRACE(1001);
   bool nonfinite = false;
   float* Crow = p.C + ((size_t)q * k + i) * k;
-  for (int c = tid; c < k; c += kNT) {
+  for (int c = lane; c < k; c += 32) {
     const float x = xv[c];
     nonfinite |= !(fabsf(x) <= FLT_MAX);
     Crow[c] = x;
   }
-  if (nonfinite) atomicMin(p.fail_min, (unsigned long long)s);
-  if (warp == kPW) {
-    FMAP_TRACE(1001);
-    if (lane == 0) {
-      const float dmax = __uint_as_float(sc[0]);
-      float rc = dmax > 0.f ? pivmin / dmax : 0.f;
-      if (!(rc >= 0.f)) rc = 0.f;
-      if (bad || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)s);
-      atomicMin(p.rcond_min_bits, __float_as_uint(rc));
-    }
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  if (lane == 0) {
+    const float dmax = __uint_as_float(sc[0]);
+    float rc = dmax > 0.f ? pivmin / dmax : 0.f;
+    if (!(rc >= 0.f)) rc = 0.f;
+    if (bad || nonfinite || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)s);
+    atomicMin(p.rcond_min_bits, __float_as_uint(rc));
   }
 }
 

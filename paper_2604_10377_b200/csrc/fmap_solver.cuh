@@ -68,7 +68,7 @@ __host__ __device__ __forceinline__ int packed_size(int K4) { return col_off(K4,
 // Shared-memory bytes of one system (packed matrix + x vector + scalars).
 __host__ __device__ __forceinline__ size_t solver_smem_bytes(int k) {
   const int K4 = (k + 3) & ~3;
-  return (size_t)(packed_size(K4) + 2 * K4 + 64 + 32) * sizeof(float);
+  return (size_t)(packed_size(K4) + 2 * K4 + 104 + 32) * sizeof(float);
 }
 
 }  // namespace fmap
