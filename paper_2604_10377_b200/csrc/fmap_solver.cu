@@ -485,16 +485,37 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
     if (nbn <= 0) break;
     // B: panel warp -> diagonal-block update + Cholesky, then bulk; others -> bulk SYRK(p)
     if (warp == kPW) {
-      const int nt4 = nbn >> 2;  // 1..4 tile rows in the diagonal block
-      const int tcount = nt4 * (nt4 + 1) / 2;
-      if (lane < tcount) {
-        int a = 0, l = lane;
+      // rank-nbe update of the diagonal block [jn, jn+nbn)^2 in 2x2 tiles (36 for
+      // a full block) spread over the 32 lanes
+      const int nt2 = nbn >> 1;
+      const int tcount = nt2 * (nt2 + 1) / 2;
+      for (int e = lane; e < tcount; e += 32) {
+        int a = 0, l = e;
         while (l > a) {
           l -= a + 1;
           ++a;
         }
-        if (full) syrk_tile<true>(A, Rp, Pj, nbe, jn + 4 * a, jn + 4 * l);
-        else syrk_tile<false>(A, Rp, Pj, nbe, jn + 4 * a, jn + 4 * l);
+        const int r0 = jn + 2 * a, c0 = jn + 2 * l;
+        float acc00 = 0.f, acc01 = 0.f, acc10 = 0.f, acc11 = 0.f;
+        const float* pr = A + Pj.base0 + r0;
+        const float* pc = A + Pj.base0 + c0;
+        for (int t = 0; t < nbe; ++t) {
+          const float2 x = *reinterpret_cast<const float2*>(pr);
+          const float2 y = *reinterpret_cast<const float2*>(pc);
+          acc00 = fmaf(x.x, y.x, acc00);
+          acc01 = fmaf(x.x, y.y, acc01);
+          acc10 = fmaf(x.y, y.x, acc10);
+          acc11 = fmaf(x.y, y.y, acc11);
+          const int step = Pj.stride - ((t + 1) & ~3);
+          pr += step;
+          pc += step;
+        }
+        float* q0 = A + colbase(c0, Rp) + r0;
+        float* q1 = A + colbase(c0 + 1, Rp) + r0;
+        q0[0] -= acc00;
+        q0[1] -= acc10;
+        q1[0] -= acc01;
+        q1[1] -= acc11;
       }
       __syncwarp();
       if (nbn == kNB) diag16<true>(A, Rp, jn, nbn, scr, sinv, lane, pivmin, bad);
@@ -508,56 +529,106 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
   }
   FMAP_TRACE(1000);
 
-  // ---- back substitution L^T x = y (y = augmented row K4), panel warp only ----
-  // Per 16-row block B (descending): x_B = L_BB^{-T} y_B right-looking and
-  // replicated in every lane (FMUL -> FFMA chain per column), then the lanes
-  // update y_c -= L[B][c] . x_B for the columns c < jb.  No CTA barriers.
-  if (warp != kPW) return;
-  for (int c = lane; c < K4; c += 32) xv[c] = A[colbase(c, Rp) + K4];
-  __syncwarp();
+  // ---- back substitution L^T x = y (y = augmented row K4) ----
+  // Blocks of 16 rows, last to first.  Step s: the panel warp solves block s
+  // (lane g holds y_g; column c: x_c = y_c / L_cc, one SHFL broadcast, lanes
+  // g < c subtract L[c][g] x_c — ~3 instructions per column) and applies x_s to
+  // block s+1's entries; meanwhile the other warps apply x_{s-1} to all rows
+  // above block s+1.  One barrier per block; every entry of block s has all
+  // contributions of blocks < s before step s starts.
+  for (int c = tid; c < K4; c += kNT) xv[c] = A[colbase(c, Rp) + K4];
+  __syncthreads();
+  float* xs = scr;  // x of the previous block (16 floats)
+  int jprev = -1, nprev = 0;
   for (int jb = ((K4 - 1) / kNB) * kNB; jb >= 0; jb -= kNB) {
     const int nbe = min(kNB, K4 - jb);
-    const Panel P(jb, Rp);
-    float y[kNB];
+    const int jnext = jb - kNB;  // next block (above), may be < 0
+    if (warp == kPW) {
+      // column g of L_BB below the diagonal, preloaded per lane: L[jb+r][jb+g], r > g
+      const int g = lane;
+      float lcol[kNB];
+      const float* colg = A + colbase(jb + min(g, kNB - 1), Rp) + jb;
 #pragma unroll
-    for (int g = 0; g < kNB; g += 4) {
-      const float4 v = (g < nbe) ? ld4(xv + jb + g) : make_float4(0.f, 0.f, 0.f, 0.f);
-      y[g] = v.x;
-      y[g + 1] = v.y;
-      y[g + 2] = v.z;
-      y[g + 3] = v.w;
-    }
-#pragma unroll
-    for (int c = kNB - 1; c >= 0; --c) {
-      if (c < nbe) {
-        y[c] *= sinv[jb + c];  // x_c
-#pragma unroll
-        for (int g = 0; g < c; ++g) y[g] = fmaf(-A[P.col(g) + jb + c], y[c], y[g]);  // L[c][g]
+      for (int r4 = 0; r4 < kNB; r4 += 4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g < nbe && r4 + 3 >= (g & ~3) && r4 < nbe) v = ld4(colg + r4);
+        lcol[r4] = v.x;
+        lcol[r4 + 1] = v.y;
+        lcol[r4 + 2] = v.z;
+        lcol[r4 + 3] = v.w;
       }
-    }
-    __syncwarp();
-    if (lane == 0) {
+      float y = (g < nbe) ? xv[jb + g] : 0.f;
+      const float sg = (g < nbe) ? sinv[jb + g] : 0.f;
 #pragma unroll
-      for (int g = 0; g < kNB; g += 4)
-        if (g < nbe) st4(xv + jb + g, make_float4(y[g], y[g + 1], y[g + 2], y[g + 3]));
-    }
-    for (int c = lane; c < jb; c += 32) {
-      const float* col = A + colbase(c, Rp) + jb;
-      float acc = 0.f;
-#pragma unroll
-      for (int r = 0; r < kNB; r += 4) {
-        if (r < nbe) {
-          const float4 l = ld4(col + r);
-          acc = fmaf(l.x, y[r], acc);
-          acc = fmaf(l.y, y[r + 1], acc);
-          acc = fmaf(l.z, y[r + 2], acc);
-          acc = fmaf(l.w, y[r + 3], acc);
+      for (int c = kNB - 1; c >= 0; --c) {
+        if (c < nbe) {
+          const float xc = __shfl_sync(0xffffffffu, y * sg, c);
+          if (g == c) y = xc;
+          if (g < c) y = fmaf(-lcol[c], xc, y);
         }
       }
-      xv[c] -= acc;
+      if (g < nbe) {
+        xv[jb + g] = y;
+        xs[16 + g] = y;  // publish x_s for the lagged bulk update of the next step
+      }
+      __syncwarp();
+      // x_s and the lagged x_{s-1} applied to block s+1's entries (lanes 0..15);
+      // the other warps cover x_{s-1} only for rows above block s+1.
+      if (jnext >= 0 && g < kNB) {
+        const float* col = A + colbase(jnext + g, Rp);
+        float acc = 0.f;
+#pragma unroll
+        for (int r = 0; r < kNB; r += 4) {
+          if (r < nbe) {
+            const float4 l = ld4(col + jb + r);
+            const float4 xx = ld4(xs + 16 + r);
+            acc = fmaf(l.x, xx.x, acc);
+            acc = fmaf(l.y, xx.y, acc);
+            acc = fmaf(l.z, xx.z, acc);
+            acc = fmaf(l.w, xx.w, acc);
+          }
+        }
+        if (jprev >= 0) {
+#pragma unroll
+          for (int r = 0; r < kNB; r += 4) {
+            if (r < nprev) {
+              const float4 l = ld4(col + jprev + r);
+              const float4 xx = ld4(xs + r);
+              acc = fmaf(l.x, xx.x, acc);
+              acc = fmaf(l.y, xx.y, acc);
+              acc = fmaf(l.z, xx.z, acc);
+              acc = fmaf(l.w, xx.w, acc);
+            }
+          }
+        }
+        xv[jnext + g] -= acc;
+      }
+    } else if (jprev >= 0) {
+      // lagged: x_{s-1} (block at jprev) applied to rows c < jnext
+      for (int c = tid; c < jnext; c += kNT - 32) {
+        const float* col = A + colbase(c, Rp) + jprev;
+        float acc = 0.f;
+#pragma unroll
+        for (int r = 0; r < kNB; r += 4) {
+          if (r < nprev) {
+            const float4 l = ld4(col + r);
+            const float4 xx = ld4(xs + r);
+            acc = fmaf(l.x, xx.x, acc);
+            acc = fmaf(l.y, xx.y, acc);
+            acc = fmaf(l.z, xx.z, acc);
+            acc = fmaf(l.w, xx.w, acc);
+          }
+        }
+        xv[c] -= acc;
+      }
     }
-    __syncwarp();
+    __syncthreads();
+    if (warp == kPW && lane < 4) st4(xs + 4 * lane, ld4(xs + 16 + 4 * lane));  // x_s -> lag slot
+    jprev = jb;
+    nprev = nbe;
+    __syncthreads();
   }
+  if (warp != kPW) return;
   FMAP_TRACE(1001);
   bool nonfinite = false;
   float* Crow = p.C + ((size_t)q * k + i) * k;
