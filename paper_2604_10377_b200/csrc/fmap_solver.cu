@@ -32,7 +32,14 @@ namespace {
 
 constexpr int kNT = 256;
 constexpr int kNW = kNT / 32;
-constexpr int kPW = kNW - 1;  // panel warp
+constexpr int kPW = kNW - 1;  // panel warp (SMSP 3)
+// Warp 3 shares SMSP 3 with the panel warp and is kept idle so the critical path
+// gets that scheduler (the arbiter is fair per SMSP): bulk = warps 0-2, 4-6.
+constexpr int kIdleW = 3;
+constexpr int kBulkThreads = (kNW - 2) * 32;
+__device__ __forceinline__ int bulk_thread(int warp, int lane) {
+  return ((warp < kIdleW) ? warp : warp - 1) * 32 + lane;
+}
 
 __device__ __forceinline__ int colbase(int c, int Rp) { return col_off(c, Rp) - (c & ~3); }
 
@@ -258,6 +265,48 @@ __device__ __noinline__ void diag16(float* A, int Rp, int j, int nbe, float* scr
   __syncwarp();
 }
 
+// Cholesky of the 16x16 diagonal block at (j, j), lane r (< 16) owning row r:
+// per column t one SHFL of the pivot, rsqrt, a scale, then (15 - t) SHFL + FFMA
+// for the rank-1 update — ~290 instructions for the whole block, which matters
+// because the panel warp shares its scheduler with busy SYRK warps.  Lanes
+// 16..31 mirror lanes 0..15 (their results are discarded).  Writes L into the
+// block and 1/L_tt into sinv[j..j+16).
+template <bool FULL>
+__device__ __noinline__ void diag16_shfl(float* A, int Rp, int j, int nbe, float* sinv, int lane,
+                                         float& pivmin, unsigned& bad) {
+  const Panel P(j, Rp);
+  const int r = lane & 15;
+  float a[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    float v = (r == c) ? 1.f : 0.f;
+    if (c <= r && (FULL || (r < nbe && c < nbe))) v = A[P.col(c) + j + r];
+    a[c] = v;
+  }
+  float sv = 0.f;  // lane t ends up holding 1/L_tt
+#pragma unroll
+  for (int t = 0; t < kNB; ++t) {
+    const float d = __shfl_sync(0xffffffffu, a[t], t);
+    pivmin = fminf(pivmin, d);
+    bad |= (unsigned)(!(d > 0.f)) | (unsigned)(!(d <= FLT_MAX));
+    const float s = rsqrt_fast(d);
+    if (r == t) sv = s;
+    a[t] *= s;  // L[r][t] (lane t: sqrt(d))
+#pragma unroll
+    for (int c = t + 1; c < kNB; ++c) {
+      const float l = __shfl_sync(0xffffffffu, a[t], c);  // L[c][t]
+      a[c] = fmaf(-a[t], l, a[c]);
+    }
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int c = 0; c < kNB; ++c)
+      if (c <= r && (FULL || (r < nbe && c < nbe))) A[P.col(c) + j + r] = a[c];
+    if (FULL || r < nbe) sinv[j + r] = sv;
+  }
+  __syncwarp();
+}
+
 // TRSM of one row r of panel [j, j+nbe): x = a L11^{-T} by forward substitution
 // (right-looking over the columns of L11, LDS.128 broadcasts).
 template <bool FULL>
@@ -473,8 +522,8 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
         if (full) trsm_row<true>(A, Pj, sinv, nbe, jn + lane);
         else trsm_row<false>(A, Pj, sinv, nbe, jn + lane);
       }
-    } else {
-      for (int r = jn + max(nbn, 0) + tid; r < Rp; r += kNT - 32) {
+    } else if (warp != kIdleW) {
+      for (int r = jn + max(nbn, 0) + bulk_thread(warp, lane); r < Rp; r += kBulkThreads) {
         if (full) trsm_row<true>(A, Pj, sinv, nbe, r);
         else trsm_row<false>(A, Pj, sinv, nbe, r);
       }
@@ -522,8 +571,10 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
       else diag16<false>(A, Rp, jn, nbn, scr, sinv, lane, pivmin, bad);
       FMAP_TRACE(ts + 2);
     }
-    if (full) syrk_bulk<true>(A, Rp, K4, Pj, nbe, jn, jn, nbn, counter, lane);
-    else syrk_bulk<false>(A, Rp, K4, Pj, nbe, jn, jn, nbn, counter, lane);
+    if (warp != kIdleW) {
+      if (full) syrk_bulk<true>(A, Rp, K4, Pj, nbe, jn, jn, nbn, counter, lane);
+      else syrk_bulk<false>(A, Rp, K4, Pj, nbe, jn, jn, nbn, counter, lane);
+    }
     FMAP_TRACE(ts + 4);
     __syncthreads();
   }
@@ -603,9 +654,9 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
         }
         xv[jnext + g] -= acc;
       }
-    } else if (jprev >= 0) {
+    } else if (jprev >= 0 && warp != kIdleW) {
       // lagged: x_{s-1} (block at jprev) applied to rows c < jnext
-      for (int c = tid; c < jnext; c += kNT - 32) {
+      for (int c = bulk_thread(warp, lane); c < jnext; c += kBulkThreads) {
         const float* col = A + colbase(c, Rp) + jprev;
         float acc = 0.f;
 #pragma unroll
