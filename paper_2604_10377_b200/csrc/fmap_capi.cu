@@ -240,16 +240,17 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   const char* trace_file = std::getenv("FMAP_TRACE_FILE");
   long long* d_trace = nullptr;
   if (trace_file) {
-    FMAP_CK(ctx, cudaMalloc(&d_trace, 8 * 1024 * sizeof(long long)));
-    FMAP_CK(ctx, cudaMemsetAsync(d_trace, 0, 8 * 1024 * sizeof(long long), ctx->stream));
+    FMAP_CK(ctx, cudaMalloc(&d_trace, 16 * 1024 * sizeof(long long)));
+    FMAP_CK(ctx, cudaMemsetAsync(d_trace, 0, 16 * 1024 * sizeof(long long), ctx->stream));
     p.trace = d_trace;
     const char* tb = std::getenv("FMAP_TRACE_BLOCK");
     p.trace_block = tb ? std::atoi(tb) : 0;
   }
+  p.force_single = std::getenv("FMAP_FORCE_SINGLE") ? 1 : 0;
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, launch_chol_solve(p, mask_mode, ctx->stream));
   if (d_trace) {
-    std::vector<long long> h(8 * 1024);
+    std::vector<long long> h(16 * 1024);
     FMAP_CK(ctx, cudaMemcpyAsync(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
     FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
     if (FILE* f = std::fopen(trace_file, "wb")) {

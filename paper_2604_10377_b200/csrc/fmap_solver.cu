@@ -273,7 +273,7 @@ __device__ __noinline__ void diag16(float* A, int Rp, int j, int nbe, float* scr
 // block and 1/L_tt into sinv[j..j+16).
 template <bool FULL>
 __device__ __noinline__ void diag16_shfl(float* A, int Rp, int j, int nbe, float* sinv, int lane,
-                                         float& pivmin, unsigned& bad) {
+                                         float& pivmin, unsigned& bad, int width = 32) {
   const Panel P(j, Rp);
   const int r = lane & 15;
   float a[kNB];
@@ -286,7 +286,7 @@ __device__ __noinline__ void diag16_shfl(float* A, int Rp, int j, int nbe, float
   float sv = 0.f;  // lane t ends up holding 1/L_tt
 #pragma unroll
   for (int t = 0; t < kNB; ++t) {
-    const float d = __shfl_sync(0xffffffffu, a[t], t);
+    const float d = __shfl_sync(0xffffffffu, a[t], t, width);
     pivmin = fminf(pivmin, d);
     bad |= (unsigned)(!(d > 0.f)) | (unsigned)(!(d <= FLT_MAX));
     const float s = rsqrt_fast(d);
@@ -294,11 +294,11 @@ __device__ __noinline__ void diag16_shfl(float* A, int Rp, int j, int nbe, float
     a[t] *= s;  // L[r][t] (lane t: sqrt(d))
 #pragma unroll
     for (int c = t + 1; c < kNB; ++c) {
-      const float l = __shfl_sync(0xffffffffu, a[t], c);  // L[c][t]
+      const float l = __shfl_sync(0xffffffffu, a[t], c, width);  // L[c][t]
       a[c] = fmaf(-a[t], l, a[c]);
     }
   }
-  if (lane < 16) {
+  if (lane < 16 || width == 16) {
 #pragma unroll
     for (int c = 0; c < kNB; ++c)
       if (c <= r && (FULL || (r < nbe && c < nbe))) A[P.col(c) + j + r] = a[c];
@@ -698,21 +698,371 @@ __global__ void __launch_bounds__(kNT, 2) chol_solve_kernel(SolveParams p) {
   }
 }
 
-// Host-side launcher.
+
+// ===========================================================================
+// Two systems per CTA in lockstep (1 CTA / SM, 16 warps).  The panel warp (15)
+// factors both systems' diagonal blocks at once (lanes 0..15: system 0,
+// 16..31: system 1), which halves the per-system cost of the latency-bound
+// critical path; warps 0..14 share TRSM / SYRK / back-substitution work of both
+// systems.  Per panel:
+//   A  TRSM(p), all rows >= jn of both systems        (bulk)
+//   B  SYRK of the next panel's columns [jn, jn+nbn)  (bulk, incl. diag block)
+//   C  panel warp: 16x16 Cholesky of both next diagonal blocks
+//      bulk:       SYRK(p) of the remaining trailing matrix (dynamic tiles)
+// ===========================================================================
+constexpr int kNT2 = 512;
+constexpr int kNW2 = kNT2 / 32;
+constexpr int kPW2 = kNW2 - 1;
+constexpr int kBulk2 = kNT2 - 32;
+
+__host__ __device__ __forceinline__ int pair_stride_floats(int K4) {
+  return packed_size(K4) + 2 * K4 + 32;  // matrix, xv, sinv, 32 scratch floats
+}
+
+template <int MASK_MODE>
+__global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
+  extern __shared__ __align__(16) float smem[];
+  const int k = p.k, K4 = p.K4, Rp = p.Rp;
+  const int Pn = packed_size(K4);
+  const int SYS = pair_stride_floats(K4);
+  unsigned* sc = reinterpret_cast<unsigned*>(smem + 2 * SYS);  // shared scalars
+  // sc[0..1] dmax per system, sc[2..3] ev_max per system, sc[4] tile counter
+  int* counter = reinterpret_cast<int*>(sc + 4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t s0 = p.sys_offset + 2 * (int64_t)blockIdx.x;
+  const int64_t slast = p.sys_offset + p.nsys - 1;
+  int64_t sys[2] = {s0, s0 + 1 <= slast ? s0 + 1 : s0};
+  const bool valid1 = s0 + 1 <= slast;
+  auto Ah = [&](int h) { return smem + h * SYS; };
+  auto xvh = [&](int h) { return smem + h * SYS + Pn; };
+  auto sinvh = [&](int h) { return smem + h * SYS + Pn + K4; };
+
+  if (tid < 5) sc[tid] = 0u;
+  // ---- staging (both systems) ----
+  {
+    const bool vec = (k & 3) == 0;
+    for (int cc = warp; cc < 2 * K4; cc += kNW2) {
+      const int h = cc >= K4, c = cc - h * K4;
+      const int64_t s = sys[h];
+      const int64_t q = s / k;
+      const int i = (int)(s - q * k);
+      const int c4 = c & ~3;
+      float* col = Ah(h) + colbase(c, Rp);
+      if (c < k) {
+        const float* g = p.gram + ((size_t)q * k + c) * k;
+        if (vec) {
+          for (int r = c4 + 4 * lane; r < k; r += 128) cp_async16(col + r, g + r);
+        } else {
+          for (int r = c4 + lane; r < k; r += 32) cp_async4(col + r, g + r);
+        }
+        const float* Rrow = p.rhs + ((size_t)q * k + i) * k;
+        for (int r = k + lane; r < Rp; r += 32)
+          col[r] = (r == K4) ? (p.rhs_unit < 0 ? Rrow[c] : (c == p.rhs_unit ? 1.f : 0.f)) : 0.f;
+      } else {
+        for (int r = c4 + lane; r < Rp; r += 32) col[r] = (r == c) ? 1.f : 0.f;
+      }
+    }
+  }
+  float evmax[2] = {0.f, 0.f};
+  if constexpr (MASK_MODE == 1) {
+    __syncthreads();  // sc[] initialised
+    for (int h = 0; h < 2; ++h) {
+      const int64_t q = sys[h] / k;
+      float m = 0.f;
+      for (int c = tid; c < k; c += kNT2)
+        m = fmaxf(m, fmaxf(p.ev1[(size_t)q * k + c], p.ev2[(size_t)q * k + c]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) atomicMax(&sc[2 + h], __float_as_uint(m));
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if constexpr (MASK_MODE == 1) {
+    evmax[0] = __uint_as_float(sc[2]);
+    evmax[1] = __uint_as_float(sc[3]);
+    if (!(evmax[0] > 0.f) || !(evmax[1] > 0.f)) {
+      if (tid == 0) atomicOr(p.flags, 32u);
+      return;
+    }
+  }
+  {  // diagonal: + lambda * m_i(c) + ridge
+    float dm[2] = {0.f, 0.f};
+    for (int e = tid; e < 2 * k; e += kNT2) {
+      const int h = e >= k, c = e - h * k;
+      const int64_t q = sys[h] / k;
+      const int i = (int)(sys[h] - q * k);
+      float* d = Ah(h) + colbase(c, Rp) + c;
+      const float v = *d + (p.lambda * mask_entry<MASK_MODE>(p, q, i, c, evmax[h]) + p.ridge);
+      *d = v;
+      dm[h] = fmaxf(dm[h], fabsf(v));
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float m = dm[h];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) atomicMax(&sc[h], __float_as_uint(m));
+    }
+  }
+  __syncthreads();
+  FMAP_TRACE(0);
+
+  const int hp = lane >> 4;  // panel warp: system of this half-warp
+  float pivmin = FLT_MAX;
+  unsigned bad = 0u;
+  if (warp == kPW2) {
+    if (K4 >= kNB) diag16_shfl<true>(Ah(hp), Rp, 0, kNB, sinvh(hp), lane, pivmin, bad, 16);
+    else diag16_shfl<false>(Ah(hp), Rp, 0, K4, sinvh(hp), lane, pivmin, bad, 16);
+  }
+  __syncthreads();
+  FMAP_TRACE(1);
+
+  for (int j = 0; j < K4; j += kNB) {
+    const int ts = 8 + (j / kNB) * 8;
+    const int nbe = min(kNB, K4 - j);
+    const int jn = j + nbe;
+    const int nbn = min(kNB, K4 - jn);
+    const Panel Pj(j, Rp);
+    const bool full = nbe == kNB;
+    // A: TRSM(p) of all rows >= jn, both systems
+    if (warp != kPW2) {
+      const int nr = Rp - jn;
+      for (int e = tid; e < 2 * nr; e += kBulk2) {
+        const int h = e >= nr, r = jn + e - h * nr;
+        if (full) trsm_row<true>(Ah(h), Pj, sinvh(h), nbe, r);
+        else trsm_row<false>(Ah(h), Pj, sinvh(h), nbe, r);
+      }
+    }
+    if (tid == 0) *counter = 0;
+    FMAP_TRACE(ts + 0);
+    __syncthreads();
+    if (nbn <= 0) break;
+    // B: SYRK of the next panel's columns (incl. its diagonal block), both systems
+    if (warp != kPW2) {
+      const int C0 = jn >> 2, nR = Rp >> 2, ncol = nbn >> 2;
+      int ntile = 0;
+      for (int cc = 0; cc < ncol; ++cc) ntile += nR - (C0 + cc);
+      for (int L = tid; L < 2 * ntile; L += kBulk2) {
+        const int h = L >= ntile;
+        int l = L - h * ntile, cc = 0;
+        while (l >= nR - (C0 + cc)) {
+          l -= nR - (C0 + cc);
+          ++cc;
+        }
+        const int Ct = C0 + cc;
+        if (full) syrk_tile<true>(Ah(h), Rp, Pj, nbe, (Ct + l) << 2, Ct << 2);
+        else syrk_tile<false>(Ah(h), Rp, Pj, nbe, (Ct + l) << 2, Ct << 2);
+      }
+    }
+    FMAP_TRACE(ts + 1);
+    __syncthreads();
+    // C: panel warp -> both next diagonal blocks; bulk -> SYRK(p) of the rest
+    if (warp == kPW2) {
+      if (nbn == kNB) diag16_shfl<true>(Ah(hp), Rp, jn, nbn, sinvh(hp), lane, pivmin, bad, 16);
+      else diag16_shfl<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), lane, pivmin, bad, 16);
+      FMAP_TRACE(ts + 2);
+    } else {
+      const int cs = jn + nbn;
+      if (cs < K4) {
+        const int ncb = (K4 - cs + 15) >> 4;
+        int W = 0;
+        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 31) >> 5;
+        const int lr = lane & 7, lc = lane >> 3;
+        while (true) {
+          int w = 0;
+          if (lane == 0) w = atomicAdd(counter, 1);
+          w = __shfl_sync(0xffffffffu, w, 0);
+          if (w >= 2 * W) break;
+          const int h = w >= W;
+          w -= h * W;
+          int cb = cs, nrb = (Rp - cb + 31) >> 5;
+          while (w >= nrb) {
+            w -= nrb;
+            cb += 16;
+            nrb = (Rp - cb + 31) >> 5;
+          }
+          const int r0 = cb + (w << 5) + (lr << 2);
+          const int c0 = cb + (lc << 2);
+          if (c0 < K4 && r0 < Rp && r0 >= c0) {
+            if (full) syrk_tile<true>(Ah(h), Rp, Pj, nbe, r0, c0);
+            else syrk_tile<false>(Ah(h), Rp, Pj, nbe, r0, c0);
+          }
+        }
+      }
+    }
+    FMAP_TRACE(ts + 4);
+    __syncthreads();
+  }
+  FMAP_TRACE(1000);
+
+  // ---- back substitution, both systems (see chol_solve_kernel) ----
+  for (int e = tid; e < 2 * K4; e += kNT2) {
+    const int h = e >= K4, c = e - h * K4;
+    xvh(h)[c] = Ah(h)[colbase(c, Rp) + K4];
+  }
+  __syncthreads();
+  int jprev = -1, nprev = 0;
+  for (int jb = ((K4 - 1) / kNB) * kNB; jb >= 0; jb -= kNB) {
+    const int nbe = min(kNB, K4 - jb);
+    const int jnext = jb - kNB;
+    if (warp == kPW2) {
+      const int g = lane & 15;
+      float* A = Ah(hp);
+      float* xv = xvh(hp);
+      float* xs = xv + K4 + K4;  // this system's 32 scratch floats
+      float lcol[kNB];
+      const float* colg = A + colbase(jb + min(g, nbe - 1), Rp) + jb;
+#pragma unroll
+      for (int r4 = 0; r4 < kNB; r4 += 4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g < nbe && r4 + 3 >= (g & ~3) && r4 < nbe) v = ld4(colg + r4);
+        lcol[r4] = v.x;
+        lcol[r4 + 1] = v.y;
+        lcol[r4 + 2] = v.z;
+        lcol[r4 + 3] = v.w;
+      }
+      float y = (g < nbe) ? xv[jb + g] : 0.f;
+      const float sg = (g < nbe) ? sinvh(hp)[jb + g] : 0.f;
+#pragma unroll
+      for (int c = kNB - 1; c >= 0; --c) {
+        if (c < nbe) {
+          const float xc = __shfl_sync(0xffffffffu, y * sg, c, 16);
+          if (g == c) y = xc;
+          if (g < c) y = fmaf(-lcol[c], xc, y);
+        }
+      }
+      if (g < nbe) {
+        xv[jb + g] = y;
+        xs[16 + g] = y;
+      }
+      __syncwarp();
+      if (jnext >= 0) {
+        const float* col = A + colbase(jnext + g, Rp);
+        float acc = 0.f;
+#pragma unroll
+        for (int r = 0; r < kNB; r += 4) {
+          if (r < nbe) {
+            const float4 l = ld4(col + jb + r);
+            const float4 xx = ld4(xs + 16 + r);
+            acc = fmaf(l.x, xx.x, acc);
+            acc = fmaf(l.y, xx.y, acc);
+            acc = fmaf(l.z, xx.z, acc);
+            acc = fmaf(l.w, xx.w, acc);
+          }
+        }
+        if (jprev >= 0) {
+#pragma unroll
+          for (int r = 0; r < kNB; r += 4) {
+            if (r < nprev) {
+              const float4 l = ld4(col + jprev + r);
+              const float4 xx = ld4(xs + r);
+              acc = fmaf(l.x, xx.x, acc);
+              acc = fmaf(l.y, xx.y, acc);
+              acc = fmaf(l.z, xx.z, acc);
+              acc = fmaf(l.w, xx.w, acc);
+            }
+          }
+        }
+        xv[jnext + g] -= acc;
+      }
+    } else if (jprev >= 0 && jnext > 0) {
+      for (int e = tid; e < 2 * jnext; e += kBulk2) {
+        const int h = e >= jnext, c = e - h * jnext;
+        const float* col = Ah(h) + colbase(c, Rp) + jprev;
+        const float* xs = xvh(h) + 2 * K4;
+        float acc = 0.f;
+#pragma unroll
+        for (int r = 0; r < kNB; r += 4) {
+          if (r < nprev) {
+            const float4 l = ld4(col + r);
+            const float4 xx = ld4(xs + r);
+            acc = fmaf(l.x, xx.x, acc);
+            acc = fmaf(l.y, xx.y, acc);
+            acc = fmaf(l.z, xx.z, acc);
+            acc = fmaf(l.w, xx.w, acc);
+          }
+        }
+        xvh(h)[c] -= acc;
+      }
+    }
+    __syncthreads();
+    if (warp == kPW2 && (lane & 15) < 4) {
+      float* xs = xvh(hp) + 2 * K4;
+      st4(xs + 4 * (lane & 15), ld4(xs + 16 + 4 * (lane & 15)));
+    }
+    jprev = jb;
+    nprev = nbe;
+    __syncthreads();
+  }
+  if (warp != kPW2) return;
+  FMAP_TRACE(1001);
+  {
+    const int h = hp, g = lane & 15;
+    const int64_t s = sys[h];
+    const int64_t q = s / k;
+    const int i = (int)(s - q * k);
+    const bool write = h == 0 || valid1;
+    bool nonfinite = false;
+    float* Crow = p.C + ((size_t)q * k + i) * k;
+    for (int c = g; c < k; c += 16) {
+      const float x = xvh(h)[c];
+      nonfinite |= !(fabsf(x) <= FLT_MAX);
+      if (write) Crow[c] = x;
+    }
+    const unsigned nf = __ballot_sync(0xffffffffu, nonfinite);
+    if (g == 0 && write) {
+      const bool my_nf = (nf >> (16 * h)) & 0xffffu;
+      const float dmax = __uint_as_float(sc[h]);
+      float rc = dmax > 0.f ? pivmin / dmax : 0.f;
+      if (!(rc >= 0.f)) rc = 0.f;
+      if (bad || my_nf || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)s);
+      atomicMin(p.rcond_min_bits, __float_as_uint(rc));
+    }
+  }
+}
+
+size_t pair_smem_bytes(int k) {
+  const int K4 = (k + 3) & ~3;
+  return (size_t)(2 * pair_stride_floats(K4) + 8) * sizeof(float);
+}
+
+// Host-side launcher: two systems per CTA when both fit in one SM's shared
+// memory (k <= ~228 on B200), else one system per CTA.
 cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream) {
-  const size_t smem = solver_smem_bytes(p.k);
   if (p.nsys <= 0) return cudaSuccess;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t smem2 = pair_smem_bytes(p.k);
+  const bool pair = smem2 <= (size_t)optin && !p.force_single;
   void (*fn)(SolveParams) = nullptr;
-  switch (mask_mode) {
-    case 0: fn = chol_solve_kernel<0>; break;
-    case 1: fn = chol_solve_kernel<1>; break;
-    default: fn = chol_solve_kernel<2>; break;
+  size_t smem;
+  unsigned grid, block;
+  if (pair) {
+    switch (mask_mode) {
+      case 0: fn = chol_pair_kernel<0>; break;
+      case 1: fn = chol_pair_kernel<1>; break;
+      default: fn = chol_pair_kernel<2>; break;
+    }
+    smem = smem2;
+    grid = (unsigned)((p.nsys + 1) / 2);
+    block = kNT2;
+  } else {
+    switch (mask_mode) {
+      case 0: fn = chol_solve_kernel<0>; break;
+      case 1: fn = chol_solve_kernel<1>; break;
+      default: fn = chol_solve_kernel<2>; break;
+    }
+    smem = solver_smem_bytes(p.k);
+    grid = (unsigned)p.nsys;
+    block = kNT;
   }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  fn<<<(unsigned)p.nsys, kNT, smem, stream>>>(p);
+  fn<<<grid, block, smem, stream>>>(p);
   return cudaGetLastError();
 }
 

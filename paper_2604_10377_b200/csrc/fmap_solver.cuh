@@ -56,6 +56,7 @@ struct SolveParams {
   unsigned int* flags;           // validation flags (bit 5: empty spectrum)
   long long* trace;              // debug phase trace (nullptr = off)
   int trace_block;
+  int force_single;              // debug: force one system per CTA
 };
 
 __host__ __device__ __forceinline__ int col_off(int c, int Rp) {

@@ -8,12 +8,14 @@ import sys
 
 import numpy as np
 
-t = np.fromfile(sys.argv[1], dtype=np.int64).reshape(8, 1024)
-PW = 7
+t = np.fromfile(sys.argv[1], dtype=np.int64).reshape(-1, 1024)
+NW = int(sys.argv[2]) if len(sys.argv) > 2 else (16 if t[8:].any() else 8)
+t = t[:NW]
+PW = NW - 1
 t0 = t[:, 0].min()
 print("staging:", t[:, 0].max() - t0, " first diag:", t[PW, 1] - t[:, 0].max())
 prev = t[:, 1].max()
-print("panel    trsm   diag(w7)   bulk_end   panel_total")
+print("panel    trsm   [next-syrk end]  diag(PW)   bulk_end   panel_total")
 p = 0
 while True:
     b = 8 + 8 * p
@@ -22,10 +24,10 @@ while True:
     eA = t[:, b].max()
     row = [eA - prev]
     if t[:, b + 4].max():
-        row += [t[PW, b + 2] - eA, t[:, b + 4].max() - eA]
+        row += [t[:PW, b + 1].max() - eA if t[:, b + 1].any() else 0, t[PW, b + 2] - eA, t[:, b + 4].max() - eA]
         nxt = t[:, b + 4].max()
     else:
-        row += [0, 0]
+        row += [0, 0, 0]
         nxt = eA
     row.append(nxt - prev)
     print(f"{p:5d}", "  ".join(f"{x:9d}" for x in row))
