@@ -386,6 +386,87 @@ __device__ __forceinline__ void syrk_tile(float* A, int Rp, const Panel& P, int 
   }
 }
 
+// 8x4 register tile: rows r0a..r0a+3 and r0b..r0b+3 (two 4-row groups, 32 rows
+// apart so that the 8 row-lanes of a warp read one contiguous 128-byte segment
+// per group), columns c0..c0+3.  va / vb: the group lies on or below the
+// diagonal (otherwise its destination is not stored and is skipped).
+template <bool FULL>
+__device__ __forceinline__ void syrk_tile84(float* A, int Rp, const Panel& P, int nbe, int r0a,
+                                            int r0b, int c0, bool va, bool vb) {
+  float acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+  const float* pa = A + P.base0 + r0a;
+  const float* pb = A + P.base0 + r0b;
+  const float* pc = A + P.base0 + c0;
+  auto step = [&](const float4 xa, const float4 xb, const float4 y) {
+    const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+    const float yr[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xr[a], yr[b], acc[a][b]);
+  };
+  if (FULL) {
+#pragma unroll
+    for (int t = 0; t < kNB; ++t) {
+      const int o = t * P.stride - S4(t);
+      step(ld4(pa + o), ld4(pb + o), ld4(pc + o));
+    }
+  } else {
+    for (int t = 0; t < nbe; ++t) {
+      step(ld4(pa), ld4(pb), ld4(pc));
+      const int st = P.stride - ((t + 1) & ~3);
+      pa += st;
+      pb += st;
+      pc += st;
+    }
+  }
+  const int qs = Rp - c0;
+  float* qa = A + col_off(c0, Rp) - c0 + r0a;
+  float* qb = A + col_off(c0, Rp) - c0 + r0b;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (va) {
+      float4 v = ld4(qa + b * qs);
+      v.x -= acc[0][b];
+      v.y -= acc[1][b];
+      v.z -= acc[2][b];
+      v.w -= acc[3][b];
+      st4(qa + b * qs, v);
+    }
+    if (vb) {
+      float4 v = ld4(qb + b * qs);
+      v.x -= acc[4][b];
+      v.y -= acc[5][b];
+      v.z -= acc[6][b];
+      v.w -= acc[7][b];
+      st4(qb + b * qs, v);
+    }
+  }
+}
+
+// One 64x16 warp tile (column block cb, row block starting at rb) of SYRK(p):
+// lane (lr = lane&7, lc = lane>>3) owns rows rb+4lr.., rb+32+4lr.. and columns
+// cb+4lc..  Skips 4x4 groups above the diagonal, outside the matrix or inside
+// the excluded diagonal block [db, db+dbn)^2.
+template <bool FULL>
+__device__ __forceinline__ void syrk_warp_tile(float* A, int Rp, int K4, const Panel& P, int nbe,
+                                               int cb, int rb, int db, int dbn, int lane) {
+  const int lr = lane & 7, lc = lane >> 3;
+  const int c0 = cb + 4 * lc;
+  if (c0 >= K4) return;
+  const int ra = rb + 4 * lr, rbb = rb + 32 + 4 * lr;
+  const bool cin = c0 < db + dbn;
+  const bool va = ra < Rp && ra >= c0 && !(cin && ra < db + dbn);
+  const bool vb = rbb < Rp && rbb >= c0 && !(cin && rbb < db + dbn);
+  if (!va && !vb) return;
+  // operand rows must exist even for a skipped group: clamp to a valid row
+  syrk_tile84<FULL>(A, Rp, P, nbe, va ? ra : rbb, vb ? rbb : ra, c0, va, vb);
+}
+
 // Bulk SYRK(p) over columns [c_lo, K4), rows >= column, skipping the diagonal
 // block [db, db+dbn)^2 (handled by the panel warp).  Warp tiles of 32 rows x 16
 // columns (lanes 8 x 4, 4x4 each) are pulled from *counter.
@@ -393,23 +474,19 @@ template <bool FULL>
 __device__ __forceinline__ void syrk_bulk(float* A, int Rp, int K4, const Panel& P, int nbe,
                                           int c_lo, int db, int dbn, int* counter, int lane) {
   const int ncb = (K4 - c_lo + 15) >> 4;
-  const int lr = lane & 7, lc = lane >> 3;
   while (true) {
     int w = 0;
     if (lane == 0) w = atomicAdd(counter, 1);
     w = __shfl_sync(0xffffffffu, w, 0);
-    int u = 0, cb = c_lo, nrb = (Rp - cb + 31) >> 5;
+    int u = 0, cb = c_lo, nrb = (Rp - cb + 63) >> 6;
     while (u < ncb && w >= nrb) {
       w -= nrb;
       ++u;
       cb += 16;
-      nrb = (Rp - cb + 31) >> 5;
+      nrb = (Rp - cb + 63) >> 6;
     }
     if (u >= ncb) break;
-    const int r0 = cb + (w << 5) + (lr << 2);
-    const int c0 = cb + (lc << 2);
-    const bool in_diag = (r0 < db + dbn) && (c0 < db + dbn);
-    if (c0 < K4 && r0 < Rp && r0 >= c0 && !in_diag) syrk_tile<FULL>(A, Rp, P, nbe, r0, c0);
+    syrk_warp_tile<FULL>(A, Rp, K4, P, nbe, cb, cb + (w << 6), db, dbn, lane);
   }
 }
 
@@ -867,8 +944,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       if (cs < K4) {
         const int ncb = (K4 - cs + 15) >> 4;
         int W = 0;
-        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 31) >> 5;
-        const int lr = lane & 7, lc = lane >> 3;
+        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 63) >> 6;
         while (true) {
           int w = 0;
           if (lane == 0) w = atomicAdd(counter, 1);
@@ -876,18 +952,14 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
           if (w >= 2 * W) break;
           const int h = w >= W;
           w -= h * W;
-          int cb = cs, nrb = (Rp - cb + 31) >> 5;
+          int cb = cs, nrb = (Rp - cb + 63) >> 6;
           while (w >= nrb) {
             w -= nrb;
             cb += 16;
-            nrb = (Rp - cb + 31) >> 5;
+            nrb = (Rp - cb + 63) >> 6;
           }
-          const int r0 = cb + (w << 5) + (lr << 2);
-          const int c0 = cb + (lc << 2);
-          if (c0 < K4 && r0 < Rp && r0 >= c0) {
-            if (full) syrk_tile<true>(Ah(h), Rp, Pj, nbe, r0, c0);
-            else syrk_tile<false>(Ah(h), Rp, Pj, nbe, r0, c0);
-          }
+          if (full) syrk_warp_tile<true>(Ah(h), Rp, K4, Pj, nbe, cb, cb + (w << 6), 0, 0, lane);
+          else syrk_warp_tile<false>(Ah(h), Rp, K4, Pj, nbe, cb, cb + (w << 6), 0, 0, lane);
         }
       }
     }

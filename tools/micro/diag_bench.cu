@@ -4,7 +4,7 @@
 
 using namespace fmap;
 
-__global__ void bench(long long* out, int reps, int nwarps_busy, int variant, int diag_warp) {
+__global__ void bench(long long* out, int reps, int nwarps_busy, int variant, int diag_warp, int lds_busy) {
   extern __shared__ __align__(16) float smem[];
   const int Rp = 20, K4 = 16;
   float* A = smem;
@@ -42,12 +42,28 @@ __global__ void bench(long long* out, int reps, int nwarps_busy, int variant, in
         __syncwarp();
       }
     }
-  } else {
+  } else if (!lds_busy) {
     float a = lane, b = 1.0001f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
     for (int it = 0; it < reps * 400; ++it) {
       c0 = fmaf(a, b, c0); c1 = fmaf(a, b, c1); c2 = fmaf(a, b, c2); c3 = fmaf(a, b, c3);
     }
     if (c0 + c1 + c2 + c3 == 1.2345f) out[100] = 1;
+  } else {
+    // SYRK-like: 2 LDS.128 + 16 FFMA per step on a 4x4 register tile
+    float acc[16] = {};
+    const float* base = smem + 4096 + ((lane & 7) * 4);
+    for (int it = 0; it < reps * 100; ++it) {
+      const float4 x = *reinterpret_cast<const float4*>(base + (it & 63) * 36);
+      const float4 y = *reinterpret_cast<const float4*>(base + (it & 63) * 36 + 16 * (lane >> 3));
+      const float xr[4] = {x.x, x.y, x.z, x.w}, yr[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u * 4 + v] = fmaf(xr[u], yr[v], acc[u * 4 + v]);
+    }
+    float t = 0.f;
+    for (int e = 0; e < 16; ++e) t += acc[e];
+    if (t == 1.2345f) out[100] = 1;
   }
   long long t1 = clock64();
   if (warp == diag_warp && lane == 0) { out[0] = (t1 - t0) / reps; out[1] = bad; }
@@ -56,61 +72,16 @@ __global__ void bench(long long* out, int reps, int nwarps_busy, int variant, in
 int main() {
   long long* d; cudaMalloc(&d, 1024 * 8);
   long long h[2];
-  const char* names[] = {"diag16", "2x chol8 (regs)", "ld/st tri8 x2", "diag16_shfl"};
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+  const char* names[] = {"diag16(repl)", "2x chol8 (regs)", "ld/st", "diag16_shfl"};
   for (int v : {0, 3})
-    for (int nw : {1, 8, 16}) {
-      for (int dw : {0, nw - 1}) {
-        bench<<<1, 32 * nw, 16384>>>(d, 50, nw - 1, v, dw);
+    for (int nw : {1, 8, 16})
+      for (int lb : {0, 1}) {
+        if (nw == 1 && lb) continue;
+        bench<<<1, 32 * nw, 100000>>>(d, 50, nw - 1, v, nw - 1, lb);
         cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-        printf("%-16s warps=%2d diag on warp %2d: %lld cycles/call\n", names[v], nw, dw, h[0]);
+        printf("%-14s warps=%2d busy=%s: %lld cycles/call\n", names[v], nw, lb ? "LDS+FFMA" : "FFMA    ", h[0]);
       }
-    }
-  {
-    // correctness: run both variants once on the same block, compare L and sinv
-    bench<<<1, 32, 16384>>>(d, 1, 0, 0, 0);
-    cudaDeviceSynchronize();
-  }
-  // two CTAs per SM: launch 2*148 CTAs of 8 warps, diag on warp 7 of each
-  for (int dw : {0, 7}) {
-    bench<<<296, 256, 100000>>>(d, 50, 7, 0, dw);
-    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-    printf("2 CTAs/SM x 8 warps, diag on warp %d (block 0): %lld\n", dw, h[0]);
-  }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
-
-// ---- correctness check kernel: both diag variants on the same SPD block ----
-__global__ void check(float* out) {
-  __shared__ __align__(16) float A1[512], A2[512], s1[32], s2[32];
-  const int Rp = 20, K4 = 16, lane = threadIdx.x;
-  for (int c = 0; c < K4; ++c)
-    for (int r = (c & ~3) + lane; r < Rp; r += 32) {
-      float v = (r < K4) ? (r == c ? 17.f : 1.f / (1 + abs(r - c)) + 0.01f * ((r * 7 + c * 3) % 5)) : 0.f;
-      if (r < c) v = 0.f;
-      A1[col_off(c, Rp) - (c & ~3) + r] = v;
-      A2[col_off(c, Rp) - (c & ~3) + r] = v;
-    }
-  __syncwarp();
-  float pm = 1e30f;
-  unsigned bad = 0;
-  float scr[1];
-  (void)scr;
-  __shared__ __align__(16) float sc[128];
-  diag16<true>(A1, Rp, 0, 16, sc, s1, lane, pm, bad);
-  diag16_shfl<true>(A2, Rp, 0, 16, s2, lane, pm, bad);
-  float e = 0.f;
-  for (int c = 0; c < K4; ++c)
-    for (int r = c; r < K4; ++r) e = fmaxf(e, fabsf(A1[col_off(c, Rp) - (c & ~3) + r] - A2[col_off(c, Rp) - (c & ~3) + r]));
-  for (int c = 0; c < K4; ++c) e = fmaxf(e, fabsf(s1[c] - s2[c]));
-  if (lane == 0) out[0] = e;
-}
-
-struct CheckRunner {
-  CheckRunner() {
-    float* d; cudaMalloc(&d, 4);
-    check<<<1, 32>>>(d);
-    float h; cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost);
-    printf("diag16 vs diag16_shfl max abs diff: %g\n", h);
-  }
-} check_runner_instance;
