@@ -810,6 +810,14 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   const int64_t slast = p.sys_offset + p.nsys - 1;
   int64_t sys[2] = {s0, s0 + 1 <= slast ? s0 + 1 : s0};
   const bool valid1 = s0 + 1 <= slast;
+  // pair / row of each system (hoisted: 64-bit division is a software routine)
+  int64_t qq[2];
+  int ii[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    qq[h] = sys[h] / k;
+    ii[h] = (int)(sys[h] - qq[h] * k);
+  }
   auto Ah = [&](int h) { return smem + h * SYS; };
   auto xvh = [&](int h) { return smem + h * SYS + Pn; };
   auto sinvh = [&](int h) { return smem + h * SYS + Pn + K4; };
@@ -820,9 +828,8 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     const bool vec = (k & 3) == 0;
     for (int cc = warp; cc < 2 * K4; cc += kNW2) {
       const int h = cc >= K4, c = cc - h * K4;
-      const int64_t s = sys[h];
-      const int64_t q = s / k;
-      const int i = (int)(s - q * k);
+      const int64_t q = qq[h];
+      const int i = ii[h];
       const int c4 = c & ~3;
       float* col = Ah(h) + colbase(c, Rp);
       if (c < k) {
@@ -844,7 +851,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   if constexpr (MASK_MODE == 1) {
     __syncthreads();  // sc[] initialised
     for (int h = 0; h < 2; ++h) {
-      const int64_t q = sys[h] / k;
+      const int64_t q = qq[h];
       float m = 0.f;
       for (int c = tid; c < k; c += kNT2)
         m = fmaxf(m, fmaxf(p.ev1[(size_t)q * k + c], p.ev2[(size_t)q * k + c]));
@@ -867,8 +874,8 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     float dm[2] = {0.f, 0.f};
     for (int e = tid; e < 2 * k; e += kNT2) {
       const int h = e >= k, c = e - h * k;
-      const int64_t q = sys[h] / k;
-      const int i = (int)(sys[h] - q * k);
+      const int64_t q = qq[h];
+      const int i = ii[h];
       float* d = Ah(h) + colbase(c, Rp) + c;
       const float v = *d + (p.lambda * mask_entry<MASK_MODE>(p, q, i, c, evmax[h]) + p.ridge);
       *d = v;
@@ -1072,8 +1079,8 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   {
     const int h = hp, g = lane & 15;
     const int64_t s = sys[h];
-    const int64_t q = s / k;
-    const int i = (int)(s - q * k);
+    const int64_t q = qq[h];
+    const int i = ii[h];
     const bool write = h == 0 || valid1;
     bool nonfinite = false;
     float* Crow = p.C + ((size_t)q * k + i) * k;
