@@ -452,19 +452,9 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   if (!gram || !rhs || !mask || !C_out) return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
   if (!(lambda >= 0.f)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "lambda must be non-negative");
   const size_t kk = (size_t)k * k;
-  // solver.hpp:132-145, per problem in order, before any device work
-  for (int64_t q = 0; q < b; ++q) {
-    const float* m = mask + q * kk;
-    for (size_t e = 0; e < kk; ++e)
-      if (!(m[e] >= 0.f))
-        return set_err(ctx, FMAP_INVALID_ARGUMENT, "penalty mask entries must be non-negative");
-    if (!host_finite(gram + q * kk, kk))
-      return set_err(ctx, FMAP_INVALID_ARGUMENT, "gram contains non-finite entries");
-    if (!host_finite(rhs + q * kk, kk))
-      return set_err(ctx, FMAP_INVALID_ARGUMENT, "rhs contains non-finite entries");
-    if (!host_finite(m, kk))
-      return set_err(ctx, FMAP_INVALID_ARGUMENT, "mask contains non-finite entries");
-  }
+  // solver.hpp:132-145: validated on the device (validate_kernel) after the
+  // copies and before any result is exposed; the status precedence follows the
+  // reference's check order (mask >= 0, finite gram, rhs, mask).
   const size_t bytes = (size_t)b * kk * sizeof(float);
   const size_t staging = carve_size({bytes, bytes, bytes, bytes});
   fmap_solver_options o;
@@ -491,7 +481,7 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   FMAP_CK(ctx, cudaMemcpyAsync(dG, gram, bytes, cudaMemcpyHostToDevice, ctx->stream));
   FMAP_CK(ctx, cudaMemcpyAsync(dR, rhs, bytes, cudaMemcpyHostToDevice, ctx->stream));
   FMAP_CK(ctx, cudaMemcpyAsync(dM, mask, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  st = solve_core(ctx, b, k, dG, dR, dM, nullptr, nullptr, 0, 0.f, lambda, &o, dC, report, false,
+  st = solve_core(ctx, b, k, dG, dR, dM, nullptr, nullptr, 0, 0.f, lambda, &o, dC, report, true,
                   staging);
   if (st) return st;
   FMAP_CK(ctx, cudaMemcpyAsync(C_out, dC, bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -1,0 +1,159 @@
+"""GPU parity for the rest of the north_star path, through the C ABI:
+mask kernel (masks.hpp), normal equations (solver.hpp:95-103), projection
+Phi^T Mass F, fused-mask solver, residual kernel
+(check_stationarity), end-to-end pipeline on BASELINE-shaped inputs (cfg1,
+cfg5 partial shapes, cfg4 bidirectional at reduced batch), and the C++
+adapter binary.  Oracle = oracle/ (CPU restatement) and float64 numpy."""
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+TOL_REL = 1e-4
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def test_masks_match_oracle(fm, oracle):
+    rng = np.random.default_rng(1)
+    for kind, fmk in ((0, fm.MaskKind.Commutativity), (1, fm.MaskKind.Resolvent)):
+        for k in (1, 2, 7, 50, 200):
+            e1 = np.sort(rng.uniform(0, 200, k)).astype(np.float32)
+            e2 = np.sort(rng.uniform(0, 200, k)).astype(np.float32)
+            e1[0] = 0.0
+            got = fm.build_mask(fmk, e1, e2, 0.5)
+            ref = oracle.mask(kind, e1, e2, 0.5, dtype=np.float32)
+            np.testing.assert_allclose(got, ref, rtol=2e-6, atol=1e-7 * max(1.0, np.abs(ref).max()))
+    with pytest.raises(fm.InvalidArgument):
+        fm.build_mask(fm.MaskKind.Resolvent, np.zeros(3, np.float32), np.zeros(3, np.float32), 0.5)
+    with pytest.raises(fm.InvalidArgument):
+        fm.build_mask(fm.MaskKind.Resolvent, np.ones(3, np.float32), np.ones(3, np.float32), 0.0)
+    with pytest.raises(fm.InvalidArgument):
+        fm.build_mask(fm.MaskKind.Commutativity, -np.ones(3, np.float32), np.ones(3, np.float32))
+
+
+def test_normal_equations(fm, oracle):
+    for k, d in ((4, 8), (50, 128), (200, 256), (37, 19)):
+        a, b, _, _ = oracle.generate_instance(k, d, 5)
+        neq = fm.normal_equations(a, b)
+        g, r = oracle.normal_equations(a.astype(np.float32), b.astype(np.float32))
+        scale = np.abs(g).max()
+        assert np.abs(neq.gram - g).max() <= 1e-5 * scale
+        assert np.abs(neq.rhs - r).max() <= 1e-5 * max(np.abs(r).max(), scale)
+    with pytest.raises(fm.InvalidArgument):
+        fm.normal_equations(np.ones((3, 4)), np.ones((2, 4)))
+
+
+def test_projection_kernel(fm, oracle):
+    from paper_2604_10377_b200 import synth
+    import ctypes as C
+    cfg = synth.PairConfig("t", 2, 50, 128, 1500, 1500)
+    data = synth.make_batch(cfg)
+    t = {k: _dev(v) for k, v in data.items()}
+    out = torch.empty((2, 50, 128), device="cuda")
+    ctx = fm._lib.context(0)
+    st = ctx._lib.fmap_project_f32_dev(ctx.handle, 2, 1500, 50, 128, C.c_void_p(t["phi1"].data_ptr()),
+                                       C.c_void_p(t["mass1"].data_ptr()), C.c_void_p(t["F1"].data_ptr()),
+                                       C.c_void_p(out.data_ptr()))
+    assert st == 0
+    torch.cuda.synchronize()
+    for q in range(2):
+        ref = oracle.project_mass(data["phi1"][q], data["mass1"][q], data["F1"][q])
+        assert np.abs(out[q].cpu().numpy() - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("kind", ["resolvent", "commutativity"])
+def test_fused_mask_solver_matches_mask_solver(fm, oracle, kind):
+    from paper_2604_10377_b200 import synth
+    G, R, e1, e2 = synth.random_normal_equations(3, 60, 120, 11)
+    fmk = fm.MaskKind.Resolvent if kind == "resolvent" else fm.MaskKind.Commutativity
+    M = fm.build_mask(fmk, e1, e2, 0.5)
+    lam = 100.0 if kind == "resolvent" else 1e-3
+    c_mask, _ = fm.solve_device(_dev(G), _dev(R), _dev(M), lam=lam)
+    c_ev, rep = fm.solve_device(_dev(G), _dev(R), lam=lam, ev1=_dev(e1), ev2=_dev(e2), mask_kind=fmk, sigma=0.5)
+    a, b = c_mask.cpu().numpy(), c_ev.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-5 * np.abs(a).max()
+    ref = oracle.solve(G, R, M, lam, dtype=np.float32).maps
+    assert np.abs(b - ref).max() <= TOL_REL * np.abs(ref).max()
+
+
+def test_residual_kernel_matches_oracle(fm, oracle):
+    G, R, M, a, b = oracle.random_problem(40, 80, 3, kind=1)
+    lam = 100.0
+    C = oracle.solve(G, R, M, lam).maps
+    got = fm.check_stationarity(C, a, b, M, lam)
+    ref = oracle.residual(C, *oracle.normal_equations(a.astype(np.float32), b.astype(np.float32)), M, lam)
+    assert abs(got - ref) <= 1e-3 * max(ref, 1e-3)
+    pert = C + 0.1 * oracle.randn(40, 40, 4)
+    assert fm.check_stationarity(pert, a, b, M, lam) > got
+
+
+def _pipeline_case(fm, oracle, cfg, bidirectional=False):
+    from paper_2604_10377_b200 import synth
+    data = synth.make_batch(cfg)
+    t = {k: _dev(v) for k, v in data.items()}
+    cxy, cyx, rep = fm.pipeline_device(t["phi1"], t["mass1"], t["F1"], t["ev1"], t["phi2"], t["mass2"], t["F2"],
+                                       t["ev2"], lam=cfg.lam, sigma=cfg.sigma, bidirectional=bidirectional)
+    for q in range(cfg.batch):
+        pair = {k: v[q] for k, v in data.items()}
+        A, B = synth.descriptors_f64(pair)
+        M = oracle.mask(1, pair["ev1"].astype(np.float64), pair["ev2"].astype(np.float64), cfg.sigma)
+        ref = oracle.solve(A @ A.T, B @ A.T, M, cfg.lam).maps
+        err = np.abs(cxy[q].cpu().numpy() - ref).max()
+        assert err <= TOL_REL * np.abs(ref).max(), f"C_xy pair {q}: {err}"
+        rel_res = oracle.residual(cxy[q].cpu().numpy(), A @ A.T, B @ A.T, M, cfg.lam) / np.linalg.norm(B @ A.T)
+        assert rel_res <= 1e-5, rel_res
+        if bidirectional:
+            Myx = oracle.mask(1, pair["ev2"].astype(np.float64), pair["ev1"].astype(np.float64), cfg.sigma)
+            assert np.abs(Myx - M.T).max() <= 1e-12  # mask(ev2, ev1) = M^T
+            ref2 = oracle.solve(B @ B.T, A @ B.T, Myx, cfg.lam).maps
+            err2 = np.abs(cyx[q].cpu().numpy() - ref2).max()
+            assert err2 <= TOL_REL * np.abs(ref2).max(), f"C_yx pair {q}: {err2}"
+    return rep
+
+
+def test_pipeline_cfg1(fm, oracle):
+    from paper_2604_10377_b200 import synth
+    _pipeline_case(fm, oracle, synth.CONFIGS["cfg1"])
+
+
+def test_pipeline_cfg5_partial_shapes(fm, oracle):
+    from paper_2604_10377_b200 import synth
+    cfg = synth.CONFIGS["cfg5"]
+    small = synth.PairConfig("cfg5-4", 4, cfg.k, cfg.d, cfg.n_src, cfg.n_tgt, partial=True)
+    rep = _pipeline_case(fm, oracle, small)
+    assert rep.min_rcond > 1e-7
+
+
+def test_pipeline_cfg4_bidirectional_subset(fm, oracle):
+    from paper_2604_10377_b200 import synth
+    cfg = synth.CONFIGS["cfg4"]
+    small = synth.PairConfig("cfg4-2", 2, cfg.k, cfg.d, cfg.n_src, cfg.n_tgt, bidirectional=True)
+    _pipeline_case(fm, oracle, small, bidirectional=True)
+
+
+def test_cpp_adapter_runs(tmp_path):
+    exe = tmp_path / "test_adapter"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"), str(ROOT / "tests/cpp/test_adapter.cpp"),
+                    "-L", str(ROOT / "paper_2604_10377_b200"), "-lfmap_cuda",
+                    f"-Wl,-rpath,{ROOT / 'paper_2604_10377_b200'}", "-o", str(exe)], check=True)
+    rc = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert rc.returncode == 0, rc.stdout + rc.stderr
+    assert "PASS" in rc.stdout
+
+
+def test_golden_solutions_on_gpu(fm):
+    z = np.load(ROOT / "tests" / "golden" / "solutions.npz")
+    for name in sorted({n.split("__")[0] for n in z.files}):
+        G, R, M, lam, C = (z[f"{name}__{s}"] for s in ("G", "R", "M", "lam", "C"))
+        try:
+            got = fm.solve_host(G[None], R[None], M[None], float(lam)).maps[0]
+        except fm.SingularSystemError:
+            pytest.fail(f"{name}: unexpectedly singular")
+        assert np.abs(got - C).max() <= TOL_REL * np.abs(C).max(), name

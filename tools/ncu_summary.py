@@ -30,7 +30,7 @@ def main():
             out[d["Metric Name"]] = f'{d["Metric Value"]} {d["Metric Unit"]}'.strip()
     raw = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
     if len(raw) >= 3:
-        names, vals = raw[0], raw[2]
+        names, units, vals = raw[0], raw[1], raw[2]
         for want in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
                      "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
                      "smsp__inst_executed_op_shared_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
@@ -39,7 +39,7 @@ def main():
                      "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio"):
             for i, n in enumerate(names):
                 if n == want:
-                    out[want] = vals[i]
+                    out[want] = f"{vals[i]} {units[i]}".strip()
     for k, v in out.items():
         print(f"{k:70s} {v}")
     sass = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
@@ -66,6 +66,14 @@ def main():
     for o, n in sorted(ops.items(), key=lambda x: -x[1])[:14]:
         print(f"  {o:10s} {100*n/tot_n:5.1f}%")
     if "--json" in sys.argv:
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tb = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if key in out:
+                v, u = out[key].split()
+                tb += float(v.replace(",", "")) * mult.get(u, 1)
+        out["dram_bytes_per_launch"] = tb
+        out["report"] = rep
         json.dump(out, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
 
 
