@@ -307,6 +307,59 @@ __device__ __noinline__ void diag16_shfl(float* A, int Rp, int j, int nbe, float
   __syncwarp();
 }
 
+// Cholesky of the 16x16 diagonal block at (j, j), lane-per-row (lane & 15 = row
+// r; lanes 16..31 may factor a second system's block), ONE shared-memory
+// exchange per pivot: every lane publishes its raw column-t entry a[r][t] to
+// xbuf, then each lane reads the whole column (4 LDS.128 broadcasts) and derives
+// the pivot d = a[t][t], s = 1/sqrt(d), its own L[r][t] = a[r][t]*s and the
+// rank-1 update a[r][c] -= (a[r][t]/d) * a[c][t] locally.  ~25 instructions and
+// one exchange per pivot.  xbuf: 16 floats per half-warp, 16-byte aligned.
+template <bool FULL>
+__device__ __noinline__ void diag16_x1(float* A, int Rp, int j, int nbe, float* sinv, float* xbuf,
+                                       int lane, float& pivmin, unsigned& bad) {
+  const Panel P(j, Rp);
+  const int r = lane & 15;
+  float a[kNB], lr[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    float v = (r == c) ? 1.f : 0.f;
+    if (c <= r && (FULL || (r < nbe && c < nbe))) v = A[P.col(c) + j + r];
+    a[c] = v;
+  }
+  float sv = 0.f;
+#pragma unroll
+  for (int t = 0; t < kNB; ++t) {
+    xbuf[r] = a[t];
+    __syncwarp();
+    float col[kNB];
+#pragma unroll
+    for (int g = 0; g < kNB; g += 4) {
+      const float4 v = ld4(xbuf + g);
+      col[g] = v.x;
+      col[g + 1] = v.y;
+      col[g + 2] = v.z;
+      col[g + 3] = v.w;
+    }
+    __syncwarp();
+    const float d = col[t];
+    pivmin = fminf(pivmin, d);
+    bad |= (unsigned)(!(d > 0.f)) | (unsigned)(!(d <= FLT_MAX));
+    const float s = rsqrt_fast(d);
+    const float w = a[t] * (s * s);  // a[r][t] / d
+    lr[t] = a[t] * s;                // L[r][t]
+    if (r == t) sv = s;
+#pragma unroll
+    for (int c = t + 1; c < kNB; ++c) a[c] = fmaf(-w, col[c], a[c]);
+  }
+  if (FULL || r < nbe) {
+#pragma unroll
+    for (int c = 0; c < kNB; ++c)
+      if (c <= r && (FULL || c < nbe)) A[P.col(c) + j + r] = lr[c];
+    sinv[j + r] = sv;
+  }
+  __syncwarp();
+}
+
 // TRSM of one row r of panel [j, j+nbe): x = a L11^{-T} by forward substitution
 // (right-looking over the columns of L11, LDS.128 broadcasts).
 template <bool FULL>
@@ -893,15 +946,21 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   FMAP_TRACE(0);
 
   const int hp = lane >> 4;  // panel warp: system of this half-warp
+  float* xb = reinterpret_cast<float*>(sc + 8) + 16 * hp;  // diag exchange buffer (per system)
   float pivmin = FLT_MAX;
   unsigned bad = 0u;
   if (warp == kPW2) {
-    if (K4 >= kNB) diag16_shfl<true>(Ah(hp), Rp, 0, kNB, sinvh(hp), lane, pivmin, bad, 16);
-    else diag16_shfl<false>(Ah(hp), Rp, 0, K4, sinvh(hp), lane, pivmin, bad, 16);
+    if (K4 >= kNB) diag16_x1<true>(Ah(hp), Rp, 0, kNB, sinvh(hp), xb, lane, pivmin, bad);
+    else diag16_x1<false>(Ah(hp), Rp, 0, K4, sinvh(hp), xb, lane, pivmin, bad);
   }
   __syncthreads();
   FMAP_TRACE(1);
 
+  // Schedule per panel p (diag(p) already done):
+  //   A  bulk: TRSM(p) rows >= jn  ||  deferred SYRK(p-1) of columns >= jn   (disjoint)
+  //   B  bulk: SYRK(p) of the next panel's columns [jn, jn+nbn), rows >= jn
+  //   C  panel warp alone: diag(p+1) of both systems (uncontended)
+  int jprev = -1;  // panel whose trailing SYRK is still pending
   for (int j = 0; j < K4; j += kNB) {
     const int ts = 8 + (j / kNB) * 8;
     const int nbe = min(kNB, K4 - j);
@@ -909,7 +968,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     const int nbn = min(kNB, K4 - jn);
     const Panel Pj(j, Rp);
     const bool full = nbe == kNB;
-    // A: TRSM(p) of all rows >= jn, both systems
+    // A
     if (warp != kPW2) {
       const int nr = Rp - jn;
       for (int e = tid; e < 2 * nr; e += kBulk2) {
@@ -917,12 +976,34 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
         if (full) trsm_row<true>(Ah(h), Pj, sinvh(h), nbe, r);
         else trsm_row<false>(Ah(h), Pj, sinvh(h), nbe, r);
       }
+      if (jprev >= 0 && jn < K4) {
+        const Panel Pp(jprev, Rp);  // previous panel (always full width)
+        const int cs = jn;
+        const int ncb = (K4 - cs + 15) >> 4;
+        int W = 0;
+        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 63) >> 6;
+        while (true) {
+          int w = 0;
+          if (lane == 0) w = atomicAdd(counter, 1);
+          w = __shfl_sync(0xffffffffu, w, 0);
+          if (w >= 2 * W) break;
+          const int h = w >= W;
+          w -= h * W;
+          int cb = cs, nrb = (Rp - cb + 63) >> 6;
+          while (w >= nrb) {
+            w -= nrb;
+            cb += 16;
+            nrb = (Rp - cb + 63) >> 6;
+          }
+          syrk_warp_tile<true>(Ah(h), Rp, K4, Pp, kNB, cb, cb + (w << 6), 0, 0, lane);
+        }
+      }
     }
-    if (tid == 0) *counter = 0;
     FMAP_TRACE(ts + 0);
     __syncthreads();
+    if (tid == 0) *counter = 0;
     if (nbn <= 0) break;
-    // B: SYRK of the next panel's columns (incl. its diagonal block), both systems
+    // B
     if (warp != kPW2) {
       const int C0 = jn >> 2, nR = Rp >> 2, ncol = nbn >> 2;
       int ntile = 0;
@@ -941,35 +1022,13 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     }
     FMAP_TRACE(ts + 1);
     __syncthreads();
-    // C: panel warp -> both next diagonal blocks; bulk -> SYRK(p) of the rest
+    // C
     if (warp == kPW2) {
-      if (nbn == kNB) diag16_shfl<true>(Ah(hp), Rp, jn, nbn, sinvh(hp), lane, pivmin, bad, 16);
-      else diag16_shfl<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), lane, pivmin, bad, 16);
+      if (nbn == kNB) diag16_x1<true>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
+      else diag16_x1<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       FMAP_TRACE(ts + 2);
-    } else {
-      const int cs = jn + nbn;
-      if (cs < K4) {
-        const int ncb = (K4 - cs + 15) >> 4;
-        int W = 0;
-        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 63) >> 6;
-        while (true) {
-          int w = 0;
-          if (lane == 0) w = atomicAdd(counter, 1);
-          w = __shfl_sync(0xffffffffu, w, 0);
-          if (w >= 2 * W) break;
-          const int h = w >= W;
-          w -= h * W;
-          int cb = cs, nrb = (Rp - cb + 63) >> 6;
-          while (w >= nrb) {
-            w -= nrb;
-            cb += 16;
-            nrb = (Rp - cb + 63) >> 6;
-          }
-          if (full) syrk_warp_tile<true>(Ah(h), Rp, K4, Pj, nbe, cb, cb + (w << 6), 0, 0, lane);
-          else syrk_warp_tile<false>(Ah(h), Rp, K4, Pj, nbe, cb, cb + (w << 6), 0, 0, lane);
-        }
-      }
     }
+    jprev = j;
     FMAP_TRACE(ts + 4);
     __syncthreads();
   }
@@ -1103,7 +1162,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
 
 size_t pair_smem_bytes(int k) {
   const int K4 = (k + 3) & ~3;
-  return (size_t)(2 * pair_stride_floats(K4) + 8) * sizeof(float);
+  return (size_t)(2 * pair_stride_floats(K4) + 8 + 32) * sizeof(float);
 }
 
 // Host-side launcher: two systems per CTA when both fit in one SM's shared

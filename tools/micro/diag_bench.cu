@@ -25,6 +25,8 @@ __global__ void bench(long long* out, int reps, int nwarps_busy, int variant, in
         diag16<true>(A, Rp, 0, 16, scr, sinv, lane, pm, bad);
       } else if (variant == 3) {
         diag16_shfl<true>(A, Rp, 0, 16, sinv, lane, pm, bad);
+      } else if (variant == 4) {
+        diag16_x1<true>(A, Rp, 0, 16, sinv, scr + 64 + 16 * (lane >> 4), lane, pm, bad);
       } else if (variant == 1) {  // two register-only chol8
         float t[36], inv[8];
 #pragma unroll
@@ -73,8 +75,8 @@ int main() {
   long long* d; cudaMalloc(&d, 1024 * 8);
   long long h[2];
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
-  const char* names[] = {"diag16(repl)", "2x chol8 (regs)", "ld/st", "diag16_shfl"};
-  for (int v : {0, 3})
+  const char* names[] = {"diag16(repl)", "2x chol8 (regs)", "ld/st", "diag16_shfl", "diag16_x1"};
+  for (int v : {3, 4})
     for (int nw : {1, 8, 16})
       for (int lb : {0, 1}) {
         if (nw == 1 && lb) continue;
