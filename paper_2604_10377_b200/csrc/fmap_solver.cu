@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   //   A  bulk: TRSM(p) rows >= jn  ||  deferred SYRK(p-1) of columns >= jn   (disjoint)
   //   B  bulk: SYRK(p) of the next panel's columns [jn, jn+nbn), rows >= jn
   //   C  panel warp alone: diag(p+1) of both systems (uncontended)
-  int jprev = -1;  // panel whose trailing SYRK is still pending
+  int jpend = -1;  // panel whose trailing SYRK is still pending
   for (int j = 0; j < K4; j += kNB) {
     const int ts = 8 + (j / kNB) * 8;
     const int nbe = min(kNB, K4 - j);
@@ -976,8 +976,8 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
         if (full) trsm_row<true>(Ah(h), Pj, sinvh(h), nbe, r);
         else trsm_row<false>(Ah(h), Pj, sinvh(h), nbe, r);
       }
-      if (jprev >= 0 && jn < K4) {
-        const Panel Pp(jprev, Rp);  // previous panel (always full width)
+      if (jpend >= 0 && jn < K4) {
+        const Panel Pp(jpend, Rp);  // previous panel (always full width)
         const int cs = jn;
         const int ncb = (K4 - cs + 15) >> 4;
         int W = 0;
@@ -1028,7 +1028,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       else diag16_x1<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       FMAP_TRACE(ts + 2);
     }
-    jprev = j;
+    jpend = j;
     FMAP_TRACE(ts + 4);
     __syncthreads();
   }
