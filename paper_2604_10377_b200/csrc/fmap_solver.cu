@@ -360,6 +360,111 @@ __device__ __noinline__ void diag16_x1(float* A, int Rp, int j, int nbe, float* 
   __syncwarp();
 }
 
+// Cholesky of the 16x16 diagonal block, lane-per-row (lane & 15 = row r; the
+// upper half-warp may factor a second system), in 4-pivot blocks: per block b
+//   1. rows 4b..4b+3 publish their raw entries of columns 4b..4b+3 (STS.128);
+//      every lane factors that 4x4 pivot block locally (replicated, no comms);
+//   2. each lane solves its own row of L for these 4 columns (4-step chain)
+//      and publishes it (STS.128);
+//   3. each lane applies the rank-4 update to its remaining columns from the
+//      published L rows (LDS.128 broadcasts).
+// Two exchanges per 4 pivots instead of one per pivot.  xbuf: 64 floats per
+// half-warp (16 rows x 4), 16-byte aligned.
+template <bool FULL>
+__device__ __noinline__ void diag16_b4(float* A, int Rp, int j, int nbe, float* sinv, float* xbuf,
+                                       int lane, float& pivmin, unsigned& bad) {
+  const Panel P(j, Rp);
+  const int r = lane & 15;
+  float a[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    float v = (r == c) ? 1.f : 0.f;
+    if (c <= r && (FULL || (r < nbe && c < nbe))) v = A[P.col(c) + j + r];
+    a[c] = v;
+  }
+  float sv[4] = {0.f, 0.f, 0.f, 0.f};  // 1/L_tt of this lane's own pivot block
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int t0 = 4 * b;
+    // 1. publish raw pivot-block rows, factor the 4x4 block locally
+    if ((r >> 2) == b) st4(xbuf + 4 * r, make_float4(a[t0], a[t0 + 1], a[t0 + 2], a[t0 + 3]));
+    __syncwarp();
+    float p4[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 v = ld4(xbuf + 4 * (t0 + u));
+      p4[u][0] = v.x;
+      p4[u][1] = v.y;
+      p4[u][2] = v.z;
+      p4[u][3] = v.w;
+    }
+    __syncwarp();
+    float inv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float d = p4[q][q];
+      pivmin = fminf(pivmin, d);
+      bad |= (unsigned)(!(d > 0.f)) | (unsigned)(!(d <= FLT_MAX));
+      const float s = rsqrt_fast(d);
+      inv[q] = s;
+      p4[q][q] = d * s;
+#pragma unroll
+      for (int u = q + 1; u < 4; ++u) p4[u][q] *= s;
+#pragma unroll
+      for (int c = q + 1; c < 4; ++c)
+#pragma unroll
+        for (int u = c; u < 4; ++u) p4[u][c] = fmaf(-p4[u][q], p4[c][q], p4[u][c]);
+    }
+    // 2. own row of L for columns t0..t0+3: x = a[t0..] L4^{-T}
+    float x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float v = a[t0 + q];
+#pragma unroll
+      for (int u = 0; u < q; ++u) v = fmaf(-x[u], p4[q][u], v);
+      x[q] = v * inv[q];
+    }
+    if ((r >> 2) == b) {  // rows of the pivot block: L from the local factor
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v = 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u == (r & 3) && q <= u) v = p4[u][q];
+        x[q] = v;
+        if (q == (r & 3)) sv[b] = inv[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[t0 + q] = x[q];
+    st4(xbuf + 4 * r, make_float4(x[0], x[1], x[2], x[3]));
+    __syncwarp();
+    // 3. rank-4 update of the remaining columns c > t0+3 (this row only)
+#pragma unroll
+    for (int c = t0 + 4; c < kNB; ++c) {
+      const float4 l = ld4(xbuf + 4 * c);  // L[c][t0..t0+3]
+      float v = a[c];
+      v = fmaf(-x[0], l.x, v);
+      v = fmaf(-x[1], l.y, v);
+      v = fmaf(-x[2], l.z, v);
+      v = fmaf(-x[3], l.w, v);
+      a[c] = v;
+    }
+    __syncwarp();
+  }
+  if (FULL || r < nbe) {
+#pragma unroll
+    for (int c = 0; c < kNB; ++c)
+      if (c <= r && (FULL || c < nbe)) A[P.col(c) + j + r] = a[c];
+    float s = sv[0];
+#pragma unroll
+    for (int b = 1; b < 4; ++b)
+      if ((r >> 2) == b) s = sv[b];
+    sinv[j + r] = s;
+  }
+  __syncwarp();
+}
+
 // TRSM of one row r of panel [j, j+nbe): x = a L11^{-T} by forward substitution
 // (right-looking over the columns of L11, LDS.128 broadcasts).
 template <bool FULL>
@@ -499,6 +604,92 @@ __device__ __forceinline__ void syrk_tile84(float* A, int Rp, const Panel& P, in
       st4(qb + b * qs, v);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core SYRK (legacy mma.sync m16n8k8 TF32 with 3xTF32 splitting, ~fp32
+// accuracy): a warp updates a block of 32 columns x 64 rows,
+//   A[r][c] -= sum_{t<16} L[r][j+t] L[c][j+t]    (panel j always 16 wide).
+// MMA M = output columns, N = output rows, K = panel columns, so a lane's
+// accumulator pair (d0,d1) is rows (2*t4, 2*t4+1) of one column: contiguous in
+// the column-major layout (LDS.64 / STS.64).  Fragments (g = lane/4, t4 = lane%4):
+//   a0..a3 = L[c0+g(+8)][j+t4(+4)],  b0,b1 = L[r0+g][j+t4(+4)].
+// Positions above the stored triangle / outside the matrix are not written.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void split_tf32(float x, unsigned& hi, unsigned& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0,
+                                         unsigned b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NT_M, int NT_N>  // 16-column m-tiles, 8-row n-tiles
+__device__ __forceinline__ void syrk_mma_block(float* A, int Rp, int K4, const Panel& P, int r0,
+                                               int c0, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  float acc[NT_M][NT_N][4];
+#pragma unroll
+  for (int m = 0; m < NT_M; ++m)
+#pragma unroll
+    for (int n = 0; n < NT_N; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[m][n][e] = 0.f;
+  const int rmax = Rp - 1;
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    const int ta = 8 * ks + t4, tb = ta + 4;  // panel columns of this lane
+    const float* colA = A + P.col(ta);
+    const float* colB = A + P.col(tb);
+    unsigned ahi[NT_M][4], alo[NT_M][4];
+#pragma unroll
+    for (int m = 0; m < NT_M; ++m) {
+      const int ca = min(c0 + 16 * m + g, rmax), cb = min(c0 + 16 * m + g + 8, rmax);
+      split_tf32(colA[ca], ahi[m][0], alo[m][0]);
+      split_tf32(colA[cb], ahi[m][1], alo[m][1]);
+      split_tf32(colB[ca], ahi[m][2], alo[m][2]);
+      split_tf32(colB[cb], ahi[m][3], alo[m][3]);
+    }
+#pragma unroll
+    for (int n = 0; n < NT_N; ++n) {
+      const int rr = min(r0 + 8 * n + g, rmax);
+      unsigned bh0, bl0, bh1, bl1;
+      split_tf32(colA[rr], bh0, bl0);
+      split_tf32(colB[rr], bh1, bl1);
+#pragma unroll
+      for (int m = 0; m < NT_M; ++m) {
+        mma_tf32(acc[m][n], ahi[m], bh0, bh1);
+        mma_tf32(acc[m][n], ahi[m], bl0, bl1);
+        mma_tf32(acc[m][n], alo[m], bh0, bh1);
+      }
+    }
+  }
+  // d0,d1: (row r0+8n+2t4 (+1), col c0+16m+g); d2,d3: col + 8
+#pragma unroll
+  for (int m = 0; m < NT_M; ++m)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int c = c0 + 16 * m + g + 8 * half;
+      if (c >= K4) continue;
+      float* col = A + colbase(c, Rp);
+#pragma unroll
+      for (int n = 0; n < NT_N; ++n) {
+        const int r = r0 + 8 * n + 2 * t4;
+        if (r >= (c & ~3) && r < Rp) {  // r even, Rp multiple of 4: r+1 < Rp too
+          float2 v = *reinterpret_cast<float2*>(col + r);
+          v.x -= acc[m][n][2 * half];
+          v.y -= acc[m][n][2 * half + 1];
+          *reinterpret_cast<float2*>(col + r) = v;
+        }
+      }
+    }
 }
 
 // One 64x16 warp tile (column block cb, row block starting at rb) of SYRK(p):
@@ -979,9 +1170,9 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       if (jpend >= 0 && jn < K4) {
         const Panel Pp(jpend, Rp);  // previous panel (always full width)
         const int cs = jn;
-        const int ncb = (K4 - cs + 15) >> 4;
+        const int ncb = (K4 - cs + 31) >> 5;
         int W = 0;
-        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 63) >> 6;
+        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 32 * u) + 63) >> 6;
         while (true) {
           int w = 0;
           if (lane == 0) w = atomicAdd(counter, 1);
@@ -992,10 +1183,10 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
           int cb = cs, nrb = (Rp - cb + 63) >> 6;
           while (w >= nrb) {
             w -= nrb;
-            cb += 16;
+            cb += 32;
             nrb = (Rp - cb + 63) >> 6;
           }
-          syrk_warp_tile<true>(Ah(h), Rp, K4, Pp, kNB, cb, cb + (w << 6), 0, 0, lane);
+          syrk_mma_block<2, 8>(Ah(h), Rp, K4, Pp, cb + (w << 6), cb, lane);
         }
       }
     }

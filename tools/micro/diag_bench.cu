@@ -27,6 +27,8 @@ __global__ void bench(long long* out, int reps, int nwarps_busy, int variant, in
         diag16_shfl<true>(A, Rp, 0, 16, sinv, lane, pm, bad);
       } else if (variant == 4) {
         diag16_x1<true>(A, Rp, 0, 16, sinv, scr + 64 + 16 * (lane >> 4), lane, pm, bad);
+      } else if (variant == 5) {
+        diag16_b4<true>(A, Rp, 0, 16, sinv, scr + 256 + 64 * (lane >> 4), lane, pm, bad);
       } else if (variant == 1) {  // two register-only chol8
         float t[36], inv[8];
 #pragma unroll
@@ -71,12 +73,43 @@ __global__ void bench(long long* out, int reps, int nwarps_busy, int variant, in
   if (warp == diag_warp && lane == 0) { out[0] = (t1 - t0) / reps; out[1] = bad; }
 }
 
+
+// correctness: x1 vs b4 on the same SPD block (both systems' halves)
+__global__ void check(float* out) {
+  __shared__ __align__(16) float A1[512], A2[512], s1[32], s2[32], xb[256];
+  const int Rp = 20, K4 = 16, lane = threadIdx.x;
+  for (int c = 0; c < K4; ++c)
+    for (int r = (c & ~3) + lane; r < Rp; r += 32) {
+      float v = (r < K4) ? (r == c ? 17.f : 1.f / (1 + abs(r - c)) + 0.01f * ((r * 7 + c * 3) % 5)) : 0.f;
+      if (r < c) v = 0.f;
+      A1[col_off(c, Rp) - (c & ~3) + r] = v;
+      A2[col_off(c, Rp) - (c & ~3) + r] = v;
+    }
+  __syncwarp();
+  float pm = 1e30f;
+  unsigned bad = 0;
+  diag16_x1<true>(A1, Rp, 0, 16, s1, xb + 16 * (lane >> 4), lane, pm, bad);
+  diag16_b4<true>(A2, Rp, 0, 16, s2, xb + 64 + 64 * (lane >> 4), lane, pm, bad);
+  __syncwarp();
+  float e = 0.f;
+  for (int c = 0; c < K4; ++c)
+    for (int r = c; r < K4; ++r) e = fmaxf(e, fabsf(A1[col_off(c, Rp) - (c & ~3) + r] - A2[col_off(c, Rp) - (c & ~3) + r]));
+  for (int c = 0; c < K4; ++c) e = fmaxf(e, fabsf(s1[c] - s2[c]));
+  if (lane == 0) out[0] = e;
+}
+
 int main() {
+  {
+    float* d; cudaMalloc(&d, 4);
+    check<<<1, 32>>>(d);
+    float h; cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost);
+    printf("x1 vs b4 max abs diff: %g\n", h);
+  }
   long long* d; cudaMalloc(&d, 1024 * 8);
   long long h[2];
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
-  const char* names[] = {"diag16(repl)", "2x chol8 (regs)", "ld/st", "diag16_shfl", "diag16_x1"};
-  for (int v : {3, 4})
+  const char* names[] = {"diag16(repl)", "2x chol8 (regs)", "ld/st", "diag16_shfl", "diag16_x1", "diag16_b4"};
+  for (int v : {4, 5})
     for (int nw : {1, 8, 16})
       for (int lb : {0, 1}) {
         if (nw == 1 && lb) continue;
