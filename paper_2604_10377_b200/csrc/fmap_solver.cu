@@ -1148,10 +1148,9 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   FMAP_TRACE(1);
 
   // Schedule per panel p (diag(p) already done):
-  //   A  bulk: TRSM(p) rows >= jn  ||  deferred SYRK(p-1) of columns >= jn   (disjoint)
-  //   B  bulk: SYRK(p) of the next panel's columns [jn, jn+nbn), rows >= jn
-  //   C  panel warp alone: diag(p+1) of both systems (uncontended)
-  int jpend = -1;  // panel whose trailing SYRK is still pending
+  //   A  bulk: TRSM(p) rows >= jn (both systems)
+  //   B  bulk: SYRK(p) of the next panel's columns [jn, jn+nbn) (incl. its diag block)
+  //   C  panel warp: diag(p+1) of both systems || bulk: SYRK(p) of columns >= jn+nbn
   for (int j = 0; j < K4; j += kNB) {
     const int ts = 8 + (j / kNB) * 8;
     const int nbe = min(kNB, K4 - j);
@@ -1167,32 +1166,10 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
         if (full) trsm_row<true>(Ah(h), Pj, sinvh(h), nbe, r);
         else trsm_row<false>(Ah(h), Pj, sinvh(h), nbe, r);
       }
-      if (jpend >= 0 && jn < K4) {
-        const Panel Pp(jpend, Rp);  // previous panel (always full width)
-        const int cs = jn;
-        const int ncb = (K4 - cs + 31) >> 5;
-        int W = 0;
-        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 32 * u) + 63) >> 6;
-        while (true) {
-          int w = 0;
-          if (lane == 0) w = atomicAdd(counter, 1);
-          w = __shfl_sync(0xffffffffu, w, 0);
-          if (w >= 2 * W) break;
-          const int h = w >= W;
-          w -= h * W;
-          int cb = cs, nrb = (Rp - cb + 63) >> 6;
-          while (w >= nrb) {
-            w -= nrb;
-            cb += 32;
-            nrb = (Rp - cb + 63) >> 6;
-          }
-          syrk_mma_block<2, 8>(Ah(h), Rp, K4, Pp, cb + (w << 6), cb, lane);
-        }
-      }
     }
+    if (tid == 0) *counter = 0;
     FMAP_TRACE(ts + 0);
     __syncthreads();
-    if (tid == 0) *counter = 0;
     if (nbn <= 0) break;
     // B
     if (warp != kPW2) {
@@ -1218,8 +1195,29 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       if (nbn == kNB) diag16_x1<true>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       else diag16_x1<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       FMAP_TRACE(ts + 2);
+    } else {
+      const int cs = jn + nbn;
+      if (cs < K4) {  // SYRK(p) is always a full 16-wide panel here
+        const int ncb = (K4 - cs + 15) >> 4;
+        int W = 0;
+        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 63) >> 6;
+        while (true) {
+          int w = 0;
+          if (lane == 0) w = atomicAdd(counter, 1);
+          w = __shfl_sync(0xffffffffu, w, 0);
+          if (w >= 2 * W) break;
+          const int h = w >= W;
+          w -= h * W;
+          int cb = cs, nrb = (Rp - cb + 63) >> 6;
+          while (w >= nrb) {
+            w -= nrb;
+            cb += 16;
+            nrb = (Rp - cb + 63) >> 6;
+          }
+          syrk_warp_tile<true>(Ah(h), Rp, K4, Pj, nbe, cb, cb + (w << 6), 0, 0, lane);
+        }
+      }
     }
-    jpend = j;
     FMAP_TRACE(ts + 4);
     __syncthreads();
   }
