@@ -247,6 +247,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     p.trace_block = tb ? std::atoi(tb) : 0;
   }
   p.force_single = std::getenv("FMAP_FORCE_SINGLE") ? 1 : 0;
+  p.pair_shared_smsp = std::getenv("FMAP_PAIR_SHARED") ? 1 : 0;
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, launch_chol_solve(p, mask_mode, ctx->stream));
   if (d_trace) {

@@ -1036,12 +1036,27 @@ constexpr int kNW2 = kNT2 / 32;
 constexpr int kPW2 = kNW2 - 1;
 constexpr int kBulk2 = kNT2 - 32;
 
+// ISO: warps 3, 7, 11 stay idle so SMSP 3 (wid % 4 == 3) hosts only the panel
+// warp 15 — the per-SMSP issue arbiter is fair, so this is the only way to give
+// the latency-bound critical path a scheduler of its own.
+template <bool ISO>
+__device__ __forceinline__ bool pair_bulk(int warp) {
+  return ISO ? ((warp & 3) != 3) : (warp != kPW2);
+}
+template <bool ISO>
+__device__ __forceinline__ int pair_bt(int warp, int lane) {
+  return (ISO ? (warp - (warp >> 2)) : warp) * 32 + lane;
+}
+template <bool ISO>
+__host__ __device__ constexpr int pair_nbulk() { return ISO ? 12 * 32 : kBulk2; }
+
 __host__ __device__ __forceinline__ int pair_stride_floats(int K4) {
   return packed_size(K4) + 2 * K4 + 32;  // matrix, xv, sinv, 32 scratch floats
 }
 
-template <int MASK_MODE>
+template <int MASK_MODE, bool ISO>
 __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
+  constexpr int NB_T = pair_nbulk<ISO>();
   extern __shared__ __align__(16) float smem[];
   const int k = p.k, K4 = p.K4, Rp = p.Rp;
   const int Pn = packed_size(K4);
@@ -1159,9 +1174,9 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     const Panel Pj(j, Rp);
     const bool full = nbe == kNB;
     // A
-    if (warp != kPW2) {
+    if (pair_bulk<ISO>(warp)) {
       const int nr = Rp - jn;
-      for (int e = tid; e < 2 * nr; e += kBulk2) {
+      for (int e = pair_bt<ISO>(warp, lane); e < 2 * nr; e += NB_T) {
         const int h = e >= nr, r = jn + e - h * nr;
         if (full) trsm_row<true>(Ah(h), Pj, sinvh(h), nbe, r);
         else trsm_row<false>(Ah(h), Pj, sinvh(h), nbe, r);
@@ -1172,11 +1187,11 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     __syncthreads();
     if (nbn <= 0) break;
     // B
-    if (warp != kPW2) {
+    if (pair_bulk<ISO>(warp)) {
       const int C0 = jn >> 2, nR = Rp >> 2, ncol = nbn >> 2;
       int ntile = 0;
       for (int cc = 0; cc < ncol; ++cc) ntile += nR - (C0 + cc);
-      for (int L = tid; L < 2 * ntile; L += kBulk2) {
+      for (int L = pair_bt<ISO>(warp, lane); L < 2 * ntile; L += NB_T) {
         const int h = L >= ntile;
         int l = L - h * ntile, cc = 0;
         while (l >= nR - (C0 + cc)) {
@@ -1195,7 +1210,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       if (nbn == kNB) diag16_x1<true>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       else diag16_x1<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       FMAP_TRACE(ts + 2);
-    } else {
+    } else if (pair_bulk<ISO>(warp)) {
       const int cs = jn + nbn;
       if (cs < K4) {  // SYRK(p) is always a full 16-wide panel here
         const int ncb = (K4 - cs + 15) >> 4;
@@ -1293,8 +1308,8 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
         }
         xv[jnext + g] -= acc;
       }
-    } else if (jprev >= 0 && jnext > 0) {
-      for (int e = tid; e < 2 * jnext; e += kBulk2) {
+    } else if (jprev >= 0 && jnext > 0 && pair_bulk<ISO>(warp)) {
+      for (int e = pair_bt<ISO>(warp, lane); e < 2 * jnext; e += NB_T) {
         const int h = e >= jnext, c = e - h * jnext;
         const float* col = Ah(h) + colbase(c, Rp) + jprev;
         const float* xs = xvh(h) + 2 * K4;
@@ -1367,10 +1382,11 @@ cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t 
   size_t smem;
   unsigned grid, block;
   if (pair) {
+    const bool iso = !p.pair_shared_smsp;
     switch (mask_mode) {
-      case 0: fn = chol_pair_kernel<0>; break;
-      case 1: fn = chol_pair_kernel<1>; break;
-      default: fn = chol_pair_kernel<2>; break;
+      case 0: fn = iso ? chol_pair_kernel<0, true> : chol_pair_kernel<0, false>; break;
+      case 1: fn = iso ? chol_pair_kernel<1, true> : chol_pair_kernel<1, false>; break;
+      default: fn = iso ? chol_pair_kernel<2, true> : chol_pair_kernel<2, false>; break;
     }
     smem = smem2;
     grid = (unsigned)((p.nsys + 1) / 2);

@@ -57,6 +57,7 @@ struct SolveParams {
   long long* trace;              // debug phase trace (nullptr = off)
   int trace_block;
   int force_single;              // debug: force one system per CTA
+  int pair_shared_smsp;          // debug: pair kernel without the isolated panel-warp SMSP
 };
 
 __host__ __device__ __forceinline__ int col_off(int c, int Rp) {
