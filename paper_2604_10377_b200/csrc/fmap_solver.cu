@@ -465,6 +465,37 @@ __device__ __noinline__ void diag16_b4(float* A, int Rp, int j, int nbe, float* 
   __syncwarp();
 }
 
+// In-place inverse of the lower-triangular 16x16 diagonal block at (j, j) (L with
+// 1/L_tt in sinv): lane c (< nbe) solves L x = e_c by forward substitution over
+// rows c..15 (reading L rows as broadcasts), then writes column c of L^{-1}.
+// Used after the factorization so the back substitution is a mat-vec per block.
+__device__ __forceinline__ void invert_diag16(float* A, int Rp, int j, int nbe, const float* sinv,
+                                              int c) {
+  const Panel P(j, Rp);
+  float x[kNB];
+#pragma unroll
+  for (int r = 0; r < kNB; ++r) x[r] = 0.f;
+  if (c < nbe) {
+#pragma unroll
+    for (int r = 0; r < kNB; ++r) {
+      if (r < nbe && r >= c) {
+        float v = (r == c) ? 1.f : 0.f;
+#pragma unroll
+        for (int u = 0; u < r; ++u)
+          if (u >= c) v = fmaf(-A[P.col(u) + j + r], x[u], v);  // L[r][u] x_u
+        x[r] = v * sinv[j + r];
+      }
+    }
+  }
+  __syncwarp();
+  if (c < nbe) {
+#pragma unroll
+    for (int r = 0; r < kNB; ++r)
+      if (r < nbe && r >= c) A[P.col(c) + j + r] = x[r];
+  }
+  __syncwarp();
+}
+
 // TRSM of one row r of panel [j, j+nbe): x = a L11^{-T} by forward substitution
 // (right-looking over the columns of L11, LDS.128 broadcasts).
 template <bool FULL>
@@ -1238,12 +1269,26 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   }
   FMAP_TRACE(1000);
 
-  // ---- back substitution, both systems (see chol_solve_kernel) ----
+  // ---- back substitution, both systems ----
+  // 1. invert every 16x16 diagonal block of L in place (one half-warp per block,
+  //    all blocks of both systems in parallel).
+  {
+    const int nblk = (K4 + kNB - 1) / kNB;
+    const int half = lane >> 4, c = lane & 15;
+    for (int bi = 2 * warp + half; bi < 2 * 2 * nblk; bi += 2 * kNW2) {
+      const int h = bi >= nblk, jb = (bi - h * nblk) * kNB;
+      invert_diag16(Ah(h), Rp, jb, min(kNB, K4 - jb), sinvh(h), c);
+    }
+  }
   for (int e = tid; e < 2 * K4; e += kNT2) {
     const int h = e >= K4, c = e - h * K4;
     xvh(h)[c] = Ah(h)[colbase(c, Rp) + K4];
   }
   __syncthreads();
+  // 2. blocks last to first: the panel warp forms x_B = L_BB^{-T} y_B (lane c:
+  //    column c of L_BB^{-1} . y_B, no dependency chain) and applies x_B and the
+  //    previous block's x to the next block; the bulk applies the previous
+  //    block's x to all rows above the next block (one-block lag).
   int jprev = -1, nprev = 0;
   for (int jb = ((K4 - 1) / kNB) * kNB; jb >= 0; jb -= kNB) {
     const int nbe = min(kNB, K4 - jb);
@@ -1253,27 +1298,22 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       float* A = Ah(hp);
       float* xv = xvh(hp);
       float* xs = xv + K4 + K4;  // this system's 32 scratch floats
-      float lcol[kNB];
-      const float* colg = A + colbase(jb + min(g, nbe - 1), Rp) + jb;
+      float y = 0.f;
+      if (g < nbe) {
+        const float* colg = A + colbase(jb + g, Rp) + jb;  // L_BB^{-1}[r][g], r >= g
 #pragma unroll
-      for (int r4 = 0; r4 < kNB; r4 += 4) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (g < nbe && r4 + 3 >= (g & ~3) && r4 < nbe) v = ld4(colg + r4);
-        lcol[r4] = v.x;
-        lcol[r4 + 1] = v.y;
-        lcol[r4 + 2] = v.z;
-        lcol[r4 + 3] = v.w;
-      }
-      float y = (g < nbe) ? xv[jb + g] : 0.f;
-      const float sg = (g < nbe) ? sinvh(hp)[jb + g] : 0.f;
-#pragma unroll
-      for (int c = kNB - 1; c >= 0; --c) {
-        if (c < nbe) {
-          const float xc = __shfl_sync(0xffffffffu, y * sg, c, 16);
-          if (g == c) y = xc;
-          if (g < c) y = fmaf(-lcol[c], xc, y);
+        for (int r4 = 0; r4 < kNB; r4 += 4) {
+          if (r4 < nbe && r4 + 3 >= g) {
+            const float4 l = ld4(colg + r4);
+            const float4 yy = ld4(xv + jb + r4);
+            if (r4 >= g) y = fmaf(l.x, yy.x, y);
+            if (r4 + 1 >= g) y = fmaf(l.y, yy.y, y);
+            if (r4 + 2 >= g) y = fmaf(l.z, yy.z, y);
+            if (r4 + 3 >= g) y = fmaf(l.w, yy.w, y);
+          }
         }
       }
+      __syncwarp();
       if (g < nbe) {
         xv[jb + g] = y;
         xs[16 + g] = y;
