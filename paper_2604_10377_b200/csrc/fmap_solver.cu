@@ -466,24 +466,29 @@ __device__ __noinline__ void diag16_b4(float* A, int Rp, int j, int nbe, float* 
 }
 
 // In-place inverse of the lower-triangular 16x16 diagonal block at (j, j) (L with
-// 1/L_tt in sinv): lane c (< nbe) solves L x = e_c by forward substitution over
-// rows c..15 (reading L rows as broadcasts), then writes column c of L^{-1}.
-// Used after the factorization so the back substitution is a mat-vec per block.
+// 1/L_tt in sinv).  Lane c computes column c of L^{-1} right-looking: x_u =
+// acc_u / L_uu, then acc_r -= L[r][u] x_u for r > u — an FMUL->FFMA chain per
+// column with the L column loads (LDS.128 broadcasts) off the chain.  Lanes need
+// no predicates: for u < c the accumulators stay 0.
 __device__ __forceinline__ void invert_diag16(float* A, int Rp, int j, int nbe, const float* sinv,
                                               int c) {
   const Panel P(j, Rp);
-  float x[kNB];
+  float acc[kNB];
 #pragma unroll
-  for (int r = 0; r < kNB; ++r) x[r] = 0.f;
-  if (c < nbe) {
+  for (int r = 0; r < kNB; ++r) acc[r] = (r == c) ? 1.f : 0.f;
 #pragma unroll
-    for (int r = 0; r < kNB; ++r) {
-      if (r < nbe && r >= c) {
-        float v = (r == c) ? 1.f : 0.f;
+  for (int u = 0; u < kNB; ++u) {
+    if (u < nbe) {
+      const float xu = acc[u] * sinv[j + u];
+      acc[u] = xu;
 #pragma unroll
-        for (int u = 0; u < r; ++u)
-          if (u >= c) v = fmaf(-A[P.col(u) + j + r], x[u], v);  // L[r][u] x_u
-        x[r] = v * sinv[j + r];
+      for (int g = ((u + 1) & ~3); g < kNB; g += 4) {
+        if (g < nbe) {
+          const float4 l = ld4(A + P.col(u) + j + g);  // L[g..g+3][u]
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+            if (g + w > u) acc[g + w] = fmaf(-f4get(l, w), xu, acc[g + w]);
+        }
       }
     }
   }
@@ -491,7 +496,7 @@ __device__ __forceinline__ void invert_diag16(float* A, int Rp, int j, int nbe, 
   if (c < nbe) {
 #pragma unroll
     for (int r = 0; r < kNB; ++r)
-      if (r < nbe && r >= c) A[P.col(c) + j + r] = x[r];
+      if (r < nbe && r >= c) A[P.col(c) + j + r] = acc[r];
   }
   __syncwarp();
 }
@@ -1280,6 +1285,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       invert_diag16(Ah(h), Rp, jb, min(kNB, K4 - jb), sinvh(h), c);
     }
   }
+  FMAP_TRACE(1002);
   for (int e = tid; e < 2 * K4; e += kNT2) {
     const int h = e >= K4, c = e - h * K4;
     xvh(h)[c] = Ah(h)[colbase(c, Rp) + K4];
@@ -1375,6 +1381,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     }
     jprev = jb;
     nprev = nbe;
+    FMAP_TRACE(1010 + jb / kNB);
     __syncthreads();
   }
   if (warp != kPW2) return;

@@ -34,3 +34,11 @@ while True:
     prev = nxt
     p += 1
 print("backsub:", t[PW, 1001] - t[:, 1000].max(), " total:", t[PW, 1001] - t0)
+if t[:, 1002].any():
+    print("  invert diag blocks:", t[:, 1002].max() - t[:, 1000].max())
+    prevb = t[:, 1002].max()
+    for jbi in range(13, -1, -1):
+        if 1010 + jbi < t.shape[1] and t[:, 1010 + jbi].any():
+            e = t[:, 1010 + jbi].max()
+            print(f"  block {jbi:2d}: {e - prevb}")
+            prevb = e
