@@ -1280,7 +1280,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   {
     const int nblk = (K4 + kNB - 1) / kNB;
     const int half = lane >> 4, c = lane & 15;
-    for (int bi = 2 * warp + half; bi < 2 * 2 * nblk; bi += 2 * kNW2) {
+    for (int bi = 2 * warp + half; bi < 2 * nblk; bi += 2 * kNW2) {
       const int h = bi >= nblk, jb = (bi - h * nblk) * kNB;
       invert_diag16(Ah(h), Rp, jb, min(kNB, K4 - jb), sinvh(h), c);
     }
