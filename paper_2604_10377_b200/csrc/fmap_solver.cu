@@ -315,7 +315,7 @@ __device__ __noinline__ void diag16_shfl(float* A, int Rp, int j, int nbe, float
 // rank-1 update a[r][c] -= (a[r][t]/d) * a[c][t] locally.  ~25 instructions and
 // one exchange per pivot.  xbuf: 16 floats per half-warp, 16-byte aligned.
 template <bool FULL>
-__device__ __noinline__ void diag16_x1(float* A, int Rp, int j, int nbe, float* sinv, float* xbuf,
+__device__ __forceinline__ void diag16_x1(float* A, int Rp, int j, int nbe, float* sinv, float* xbuf,
                                        int lane, float& pivmin, unsigned& bad) {
   const Panel P(j, Rp);
   const int r = lane & 15;
@@ -470,6 +470,7 @@ __device__ __noinline__ void diag16_b4(float* A, int Rp, int j, int nbe, float* 
 // acc_u / L_uu, then acc_r -= L[r][u] x_u for r > u — an FMUL->FFMA chain per
 // column with the L column loads (LDS.128 broadcasts) off the chain.  Lanes need
 // no predicates: for u < c the accumulators stay 0.
+template <bool FULL>
 __device__ __forceinline__ void invert_diag16(float* A, int Rp, int j, int nbe, const float* sinv,
                                               int c) {
   const Panel P(j, Rp);
@@ -478,12 +479,12 @@ __device__ __forceinline__ void invert_diag16(float* A, int Rp, int j, int nbe, 
   for (int r = 0; r < kNB; ++r) acc[r] = (r == c) ? 1.f : 0.f;
 #pragma unroll
   for (int u = 0; u < kNB; ++u) {
-    if (u < nbe) {
+    if (FULL || u < nbe) {
       const float xu = acc[u] * sinv[j + u];
       acc[u] = xu;
 #pragma unroll
       for (int g = ((u + 1) & ~3); g < kNB; g += 4) {
-        if (g < nbe) {
+        if (FULL || g < nbe) {
           const float4 l = ld4(A + P.col(u) + j + g);  // L[g..g+3][u]
 #pragma unroll
           for (int w = 0; w < 4; ++w)
@@ -493,12 +494,73 @@ __device__ __forceinline__ void invert_diag16(float* A, int Rp, int j, int nbe, 
     }
   }
   __syncwarp();
-  if (c < nbe) {
+  if (FULL || c < nbe) {
+    float* col = A + P.col(c) + j;
 #pragma unroll
     for (int r = 0; r < kNB; ++r)
-      if (r < nbe && r >= c) A[P.col(c) + j + r] = acc[r];
+      if ((FULL || r < nbe) && r >= c) col[r] = acc[r];
   }
   __syncwarp();
+}
+
+// Back-substitution step of the panel warp for one 16-row block B at jb (the
+// diagonal block already holds L_BB^{-1}): lane g (< 16) forms x_g =
+// (L_BB^{-T} y_B)_g, publishes x_B to xs[16..32), then (if a block above
+// exists) applies x_B and the previous block's x (xs[0..16), rows jprev..)
+// to entry jnext+g.  FULL: nbe == 16 (every block but possibly the last).
+template <bool FULL, bool LAG_FULL>
+__device__ __forceinline__ void backsub_block(float* A, int Rp, float* xv, float* xs, int jb,
+                                              int nbe, int jnext, int jprev, int nprev, int g) {
+  float y = 0.f;
+  if (FULL || g < nbe) {
+    const float* colg = A + colbase(jb + g, Rp) + jb;  // L_BB^{-1}[r][g], r >= g
+#pragma unroll
+    for (int r4 = 0; r4 < kNB; r4 += 4) {
+      if ((FULL || r4 < nbe) && r4 + 3 >= (g & ~3)) {
+        const float4 l = ld4(colg + r4);
+        const float4 yy = ld4(xv + jb + r4);
+        y = fmaf(r4 >= g ? l.x : 0.f, yy.x, y);
+        y = fmaf(r4 + 1 >= g ? l.y : 0.f, yy.y, y);
+        y = fmaf(r4 + 2 >= g ? l.z : 0.f, yy.z, y);
+        y = fmaf(r4 + 3 >= g ? l.w : 0.f, yy.w, y);
+      }
+    }
+  }
+  __syncwarp();
+  if (FULL || g < nbe) {
+    xv[jb + g] = y;
+    xs[16 + g] = y;
+  }
+  __syncwarp();
+  if (jnext >= 0) {
+    const float* col = A + colbase(jnext + g, Rp);
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < kNB; r += 4) {
+      if (FULL || r < nbe) {
+        const float4 l = ld4(col + jb + r);
+        const float4 xx = ld4(xs + 16 + r);
+        acc = fmaf(l.x, xx.x, acc);
+        acc = fmaf(l.y, xx.y, acc);
+        acc = fmaf(l.z, xx.z, acc);
+        acc = fmaf(l.w, xx.w, acc);
+      }
+    }
+    if (jprev >= 0) {
+#pragma unroll
+      for (int r = 0; r < kNB; r += 4) {
+        if (LAG_FULL || r < nprev) {
+          const float4 l = ld4(col + jprev + r);
+          const float4 xx = ld4(xs + r);
+          acc = fmaf(l.x, xx.x, acc);
+          acc = fmaf(l.y, xx.y, acc);
+          acc = fmaf(l.z, xx.z, acc);
+          acc = fmaf(l.w, xx.w, acc);
+        }
+      }
+    }
+    xv[jnext + g] -= acc;
+  }
 }
 
 // TRSM of one row r of panel [j, j+nbe): x = a L11^{-T} by forward substitution
@@ -1282,7 +1344,9 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     const int half = lane >> 4, c = lane & 15;
     for (int bi = 2 * warp + half; bi < 2 * nblk; bi += 2 * kNW2) {
       const int h = bi >= nblk, jb = (bi - h * nblk) * kNB;
-      invert_diag16(Ah(h), Rp, jb, min(kNB, K4 - jb), sinvh(h), c);
+      const int nb = min(kNB, K4 - jb);
+      if (nb == kNB) invert_diag16<true>(Ah(h), Rp, jb, nb, sinvh(h), c);
+      else invert_diag16<false>(Ah(h), Rp, jb, nb, sinvh(h), c);
     }
   }
   FMAP_TRACE(1002);
@@ -1301,58 +1365,15 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     const int jnext = jb - kNB;
     if (warp == kPW2) {
       const int g = lane & 15;
-      float* A = Ah(hp);
       float* xv = xvh(hp);
       float* xs = xv + K4 + K4;  // this system's 32 scratch floats
-      float y = 0.f;
-      if (g < nbe) {
-        const float* colg = A + colbase(jb + g, Rp) + jb;  // L_BB^{-1}[r][g], r >= g
-#pragma unroll
-        for (int r4 = 0; r4 < kNB; r4 += 4) {
-          if (r4 < nbe && r4 + 3 >= g) {
-            const float4 l = ld4(colg + r4);
-            const float4 yy = ld4(xv + jb + r4);
-            if (r4 >= g) y = fmaf(l.x, yy.x, y);
-            if (r4 + 1 >= g) y = fmaf(l.y, yy.y, y);
-            if (r4 + 2 >= g) y = fmaf(l.z, yy.z, y);
-            if (r4 + 3 >= g) y = fmaf(l.w, yy.w, y);
-          }
-        }
-      }
-      __syncwarp();
-      if (g < nbe) {
-        xv[jb + g] = y;
-        xs[16 + g] = y;
-      }
-      __syncwarp();
-      if (jnext >= 0) {
-        const float* col = A + colbase(jnext + g, Rp);
-        float acc = 0.f;
-#pragma unroll
-        for (int r = 0; r < kNB; r += 4) {
-          if (r < nbe) {
-            const float4 l = ld4(col + jb + r);
-            const float4 xx = ld4(xs + 16 + r);
-            acc = fmaf(l.x, xx.x, acc);
-            acc = fmaf(l.y, xx.y, acc);
-            acc = fmaf(l.z, xx.z, acc);
-            acc = fmaf(l.w, xx.w, acc);
-          }
-        }
-        if (jprev >= 0) {
-#pragma unroll
-          for (int r = 0; r < kNB; r += 4) {
-            if (r < nprev) {
-              const float4 l = ld4(col + jprev + r);
-              const float4 xx = ld4(xs + r);
-              acc = fmaf(l.x, xx.x, acc);
-              acc = fmaf(l.y, xx.y, acc);
-              acc = fmaf(l.z, xx.z, acc);
-              acc = fmaf(l.w, xx.w, acc);
-            }
-          }
-        }
-        xv[jnext + g] -= acc;
+      if (nbe == kNB) {
+        if (nprev == kNB || jprev < 0)
+          backsub_block<true, true>(Ah(hp), Rp, xv, xs, jb, nbe, jnext, jprev, nprev, g);
+        else
+          backsub_block<true, false>(Ah(hp), Rp, xv, xs, jb, nbe, jnext, jprev, nprev, g);
+      } else {
+        backsub_block<false, false>(Ah(hp), Rp, xv, xs, jb, nbe, jnext, jprev, nprev, g);
       }
     } else if (jprev >= 0 && jnext > 0 && pair_bulk<ISO>(warp)) {
       for (int e = pair_bt<ISO>(warp, lane); e < 2 * jnext; e += NB_T) {
