@@ -509,8 +509,9 @@ __device__ __forceinline__ void invert_diag16(float* A, int Rp, int j, int nbe, 
 // exists) applies x_B and the previous block's x (xs[0..16), rows jprev..)
 // to entry jnext+g.  FULL: nbe == 16 (every block but possibly the last).
 template <bool FULL, bool LAG_FULL>
-__device__ __forceinline__ void backsub_block(float* A, int Rp, float* xv, float* xs, int jb,
-                                              int nbe, int jnext, int jprev, int nprev, int g) {
+__device__ __forceinline__ void backsub_block(float* A, int Rp, float* xv, float* xcur,
+                                              const float* xprev, int jb, int nbe, int jnext,
+                                              int jprev, int nprev, int g) {
   float y = 0.f;
   if (FULL || g < nbe) {
     const float* colg = A + colbase(jb + g, Rp) + jb;  // L_BB^{-1}[r][g], r >= g
@@ -529,7 +530,7 @@ __device__ __forceinline__ void backsub_block(float* A, int Rp, float* xv, float
   __syncwarp();
   if (FULL || g < nbe) {
     xv[jb + g] = y;
-    xs[16 + g] = y;
+    xcur[g] = y;
   }
   __syncwarp();
   if (jnext >= 0) {
@@ -539,7 +540,7 @@ __device__ __forceinline__ void backsub_block(float* A, int Rp, float* xv, float
     for (int r = 0; r < kNB; r += 4) {
       if (FULL || r < nbe) {
         const float4 l = ld4(col + jb + r);
-        const float4 xx = ld4(xs + 16 + r);
+        const float4 xx = ld4(xcur + r);
         acc = fmaf(l.x, xx.x, acc);
         acc = fmaf(l.y, xx.y, acc);
         acc = fmaf(l.z, xx.z, acc);
@@ -551,7 +552,7 @@ __device__ __forceinline__ void backsub_block(float* A, int Rp, float* xv, float
       for (int r = 0; r < kNB; r += 4) {
         if (LAG_FULL || r < nprev) {
           const float4 l = ld4(col + jprev + r);
-          const float4 xx = ld4(xs + r);
+          const float4 xx = ld4(xprev + r);
           acc = fmaf(l.x, xx.x, acc);
           acc = fmaf(l.y, xx.y, acc);
           acc = fmaf(l.z, xx.z, acc);
@@ -1309,6 +1310,11 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       else diag16_x1<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       FMAP_TRACE(ts + 2);
     } else if (pair_bulk<ISO>(warp)) {
+      if (warp == 0) {
+        // L11(p) is final and TRSM(p) is done: invert it in place for the back
+        // substitution (half-warp per system); the warp then joins the SYRK.
+        invert_diag16<true>(Ah(lane >> 4), Rp, j, kNB, sinvh(lane >> 4), lane & 15);
+      }
       const int cs = jn + nbn;
       if (cs < K4) {  // SYRK(p) is always a full 16-wide panel here
         const int ncb = (K4 - cs + 15) >> 4;
@@ -1337,17 +1343,12 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   FMAP_TRACE(1000);
 
   // ---- back substitution, both systems ----
-  // 1. invert every 16x16 diagonal block of L in place (one half-warp per block,
-  //    all blocks of both systems in parallel).
-  {
-    const int nblk = (K4 + kNB - 1) / kNB;
-    const int half = lane >> 4, c = lane & 15;
-    for (int bi = 2 * warp + half; bi < 2 * nblk; bi += 2 * kNW2) {
-      const int h = bi >= nblk, jb = (bi - h * nblk) * kNB;
-      const int nb = min(kNB, K4 - jb);
-      if (nb == kNB) invert_diag16<true>(Ah(h), Rp, jb, nb, sinvh(h), c);
-      else invert_diag16<false>(Ah(h), Rp, jb, nb, sinvh(h), c);
-    }
+  // 1. diagonal blocks 0 .. last-1 were inverted during the factorization
+  //    (phase C); invert the last one here (half-warp per system).
+  if (warp == 0) {
+    const int jl = ((K4 - 1) / kNB) * kNB, nb = K4 - jl;
+    if (nb == kNB) invert_diag16<true>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
+    else invert_diag16<false>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
   }
   FMAP_TRACE(1002);
   for (int e = tid; e < 2 * K4; e += kNT2) {
@@ -1359,33 +1360,34 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   //    column c of L_BB^{-1} . y_B, no dependency chain) and applies x_B and the
   //    previous block's x to the next block; the bulk applies the previous
   //    block's x to all rows above the next block (one-block lag).
-  int jprev = -1, nprev = 0;
-  for (int jb = ((K4 - 1) / kNB) * kNB; jb >= 0; jb -= kNB) {
+  int jprev = -1, nprev = 0, par = 0;
+  for (int jb = ((K4 - 1) / kNB) * kNB; jb >= 0; jb -= kNB, par ^= 1) {
     const int nbe = min(kNB, K4 - jb);
     const int jnext = jb - kNB;
     if (warp == kPW2) {
       const int g = lane & 15;
       float* xv = xvh(hp);
-      float* xs = xv + K4 + K4;  // this system's 32 scratch floats
+      float* xcur = xv + 2 * K4 + 16 * par;        // x of this block
+      const float* xprev = xv + 2 * K4 + 16 * (par ^ 1);  // x of the previous block
       if (nbe == kNB) {
         if (nprev == kNB || jprev < 0)
-          backsub_block<true, true>(Ah(hp), Rp, xv, xs, jb, nbe, jnext, jprev, nprev, g);
+          backsub_block<true, true>(Ah(hp), Rp, xv, xcur, xprev, jb, nbe, jnext, jprev, nprev, g);
         else
-          backsub_block<true, false>(Ah(hp), Rp, xv, xs, jb, nbe, jnext, jprev, nprev, g);
+          backsub_block<true, false>(Ah(hp), Rp, xv, xcur, xprev, jb, nbe, jnext, jprev, nprev, g);
       } else {
-        backsub_block<false, false>(Ah(hp), Rp, xv, xs, jb, nbe, jnext, jprev, nprev, g);
+        backsub_block<false, false>(Ah(hp), Rp, xv, xcur, xprev, jb, nbe, jnext, jprev, nprev, g);
       }
     } else if (jprev >= 0 && jnext > 0 && pair_bulk<ISO>(warp)) {
       for (int e = pair_bt<ISO>(warp, lane); e < 2 * jnext; e += NB_T) {
         const int h = e >= jnext, c = e - h * jnext;
         const float* col = Ah(h) + colbase(c, Rp) + jprev;
-        const float* xs = xvh(h) + 2 * K4;
+        const float* xprev = xvh(h) + 2 * K4 + 16 * (par ^ 1);
         float acc = 0.f;
 #pragma unroll
         for (int r = 0; r < kNB; r += 4) {
           if (r < nprev) {
             const float4 l = ld4(col + r);
-            const float4 xx = ld4(xs + r);
+            const float4 xx = ld4(xprev + r);
             acc = fmaf(l.x, xx.x, acc);
             acc = fmaf(l.y, xx.y, acc);
             acc = fmaf(l.z, xx.z, acc);
@@ -1394,11 +1396,6 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
         }
         xvh(h)[c] -= acc;
       }
-    }
-    __syncthreads();
-    if (warp == kPW2 && (lane & 15) < 4) {
-      float* xs = xvh(hp) + 2 * K4;
-      st4(xs + 4 * (lane & 15), ld4(xs + 16 + 4 * (lane & 15)));
     }
     jprev = jb;
     nprev = nbe;
