@@ -1272,7 +1272,10 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     const int nbn = min(kNB, K4 - jn);
     const Panel Pj(j, Rp);
     const bool full = nbe == kNB;
-    // A
+    // A  (the panel warp, idle here, inverts the previous panel's diagonal block
+    //     in place for the back substitution: L11(p-1) is final, TRSM(p-1) done)
+    if (warp == kPW2 && j >= kNB)
+      invert_diag16<true>(Ah(hp), Rp, j - kNB, kNB, sinvh(hp), lane & 15);
     if (pair_bulk<ISO>(warp)) {
       const int nr = Rp - jn;
       for (int e = pair_bt<ISO>(warp, lane); e < 2 * nr; e += NB_T) {
@@ -1310,11 +1313,6 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       else diag16_x1<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       FMAP_TRACE(ts + 2);
     } else if (pair_bulk<ISO>(warp)) {
-      if (warp == 0) {
-        // L11(p) is final and TRSM(p) is done: invert it in place for the back
-        // substitution (half-warp per system); the warp then joins the SYRK.
-        invert_diag16<true>(Ah(lane >> 4), Rp, j, kNB, sinvh(lane >> 4), lane & 15);
-      }
       const int cs = jn + nbn;
       if (cs < K4) {  // SYRK(p) is always a full 16-wide panel here
         const int ncb = (K4 - cs + 15) >> 4;
@@ -1343,12 +1341,16 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   FMAP_TRACE(1000);
 
   // ---- back substitution, both systems ----
-  // 1. diagonal blocks 0 .. last-1 were inverted during the factorization
-  //    (phase C); invert the last one here (half-warp per system).
-  if (warp == 0) {
-    const int jl = ((K4 - 1) / kNB) * kNB, nb = K4 - jl;
-    if (nb == kNB) invert_diag16<true>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
-    else invert_diag16<false>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
+  // 1. diagonal blocks 0 .. last-2 were inverted during the factorization (by
+  //    the panel warp in phase A); invert the last two here (half-warp each).
+  if (warp == 0 || warp == 1) {
+    const int jl = ((K4 - 1) / kNB) * kNB;
+    const int jb = jl - kNB * warp;
+    if (jb >= 0) {
+      const int nb = min(kNB, K4 - jb);
+      if (nb == kNB) invert_diag16<true>(Ah(lane >> 4), Rp, jb, nb, sinvh(lane >> 4), lane & 15);
+      else invert_diag16<false>(Ah(lane >> 4), Rp, jb, nb, sinvh(lane >> 4), lane & 15);
+    }
   }
   FMAP_TRACE(1002);
   for (int e = tid; e < 2 * K4; e += kNT2) {
