@@ -1341,16 +1341,12 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   FMAP_TRACE(1000);
 
   // ---- back substitution, both systems ----
-  // 1. diagonal blocks 0 .. last-2 were inverted during the factorization (by
-  //    the panel warp in phase A); invert the last two here (half-warp each).
-  if (warp == 0 || warp == 1) {
-    const int jl = ((K4 - 1) / kNB) * kNB;
-    const int jb = jl - kNB * warp;
-    if (jb >= 0) {
-      const int nb = min(kNB, K4 - jb);
-      if (nb == kNB) invert_diag16<true>(Ah(lane >> 4), Rp, jb, nb, sinvh(lane >> 4), lane & 15);
-      else invert_diag16<false>(Ah(lane >> 4), Rp, jb, nb, sinvh(lane >> 4), lane & 15);
-    }
+  // 1. diagonal blocks 0 .. last-1 were inverted during the factorization (by
+  //    the panel warp in phase A of the following panel); invert the last here.
+  if (warp == 0) {
+    const int jl = ((K4 - 1) / kNB) * kNB, nb = K4 - jl;
+    if (nb == kNB) invert_diag16<true>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
+    else invert_diag16<false>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
   }
   FMAP_TRACE(1002);
   for (int e = tid; e < 2 * K4; e += kNT2) {
