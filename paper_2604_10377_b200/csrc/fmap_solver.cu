@@ -1153,21 +1153,22 @@ __host__ __device__ __forceinline__ int pair_stride_floats(int K4) {
   return packed_size(K4) + 2 * K4 + 32;  // matrix, xv, sinv, 32 scratch floats
 }
 
-template <int MASK_MODE, bool ISO>
+template <int MASK_MODE, bool ISO, int NS>
 __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
+  static_assert(NS == 1 || NS == 2, "one or two systems per CTA");
   constexpr int NB_T = pair_nbulk<ISO>();
   extern __shared__ __align__(16) float smem[];
   const int k = p.k, K4 = p.K4, Rp = p.Rp;
   const int Pn = packed_size(K4);
   const int SYS = pair_stride_floats(K4);
-  unsigned* sc = reinterpret_cast<unsigned*>(smem + 2 * SYS);  // shared scalars
+  unsigned* sc = reinterpret_cast<unsigned*>(smem + NS * SYS);  // shared scalars
   // sc[0..1] dmax per system, sc[2..3] ev_max per system, sc[4] tile counter
   int* counter = reinterpret_cast<int*>(sc + 4);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t s0 = p.sys_offset + 2 * (int64_t)blockIdx.x;
+  const int64_t s0 = p.sys_offset + NS * (int64_t)blockIdx.x;
   const int64_t slast = p.sys_offset + p.nsys - 1;
   int64_t sys[2] = {s0, s0 + 1 <= slast ? s0 + 1 : s0};
-  const bool valid1 = s0 + 1 <= slast;
+  const bool valid1 = NS == 2 && s0 + 1 <= slast;
   // pair / row of each system (hoisted: 64-bit division is a software routine)
   int64_t qq[2];
   int ii[2];
@@ -1184,7 +1185,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   // ---- staging (both systems) ----
   {
     const bool vec = (k & 3) == 0;
-    for (int cc = warp; cc < 2 * K4; cc += kNW2) {
+    for (int cc = warp; cc < NS * K4; cc += kNW2) {
       const int h = cc >= K4, c = cc - h * K4;
       const int64_t q = qq[h];
       const int i = ii[h];
@@ -1208,7 +1209,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   float evmax[2] = {0.f, 0.f};
   if constexpr (MASK_MODE == 1) {
     __syncthreads();  // sc[] initialised
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NS; ++h) {
       const int64_t q = qq[h];
       float m = 0.f;
       for (int c = tid; c < k; c += kNT2)
@@ -1222,7 +1223,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   __syncthreads();
   if constexpr (MASK_MODE == 1) {
     evmax[0] = __uint_as_float(sc[2]);
-    evmax[1] = __uint_as_float(sc[3]);
+    evmax[1] = NS == 2 ? __uint_as_float(sc[3]) : evmax[0];
     if (!(evmax[0] > 0.f) || !(evmax[1] > 0.f)) {
       if (tid == 0) atomicOr(p.flags, 32u);
       return;
@@ -1230,7 +1231,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   }
   {  // diagonal: + lambda * m_i(c) + ridge
     float dm[2] = {0.f, 0.f};
-    for (int e = tid; e < 2 * k; e += kNT2) {
+    for (int e = tid; e < NS * k; e += kNT2) {
       const int h = e >= k, c = e - h * k;
       const int64_t q = qq[h];
       const int i = ii[h];
@@ -1240,7 +1241,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       dm[h] = fmaxf(dm[h], fabsf(v));
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NS; ++h) {
       float m = dm[h];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -1250,7 +1251,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   __syncthreads();
   FMAP_TRACE(0);
 
-  const int hp = lane >> 4;  // panel warp: system of this half-warp
+  const int hp = NS == 2 ? (lane >> 4) : 0;  // panel warp: system of this half-warp
   float* xb = reinterpret_cast<float*>(sc + 8) + 16 * hp;  // diag exchange buffer (per system)
   float pivmin = FLT_MAX;
   unsigned bad = 0u;
@@ -1278,7 +1279,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       invert_diag16<true>(Ah(hp), Rp, j - kNB, kNB, sinvh(hp), lane & 15);
     if (pair_bulk<ISO>(warp)) {
       const int nr = Rp - jn;
-      for (int e = pair_bt<ISO>(warp, lane); e < 2 * nr; e += NB_T) {
+      for (int e = pair_bt<ISO>(warp, lane); e < NS * nr; e += NB_T) {
         const int h = e >= nr, r = jn + e - h * nr;
         if (full) trsm_row<true>(Ah(h), Pj, sinvh(h), nbe, r);
         else trsm_row<false>(Ah(h), Pj, sinvh(h), nbe, r);
@@ -1293,7 +1294,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
       const int C0 = jn >> 2, nR = Rp >> 2, ncol = nbn >> 2;
       int ntile = 0;
       for (int cc = 0; cc < ncol; ++cc) ntile += nR - (C0 + cc);
-      for (int L = pair_bt<ISO>(warp, lane); L < 2 * ntile; L += NB_T) {
+      for (int L = pair_bt<ISO>(warp, lane); L < NS * ntile; L += NB_T) {
         const int h = L >= ntile;
         int l = L - h * ntile, cc = 0;
         while (l >= nR - (C0 + cc)) {
@@ -1322,7 +1323,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
           int w = 0;
           if (lane == 0) w = atomicAdd(counter, 1);
           w = __shfl_sync(0xffffffffu, w, 0);
-          if (w >= 2 * W) break;
+          if (w >= NS * W) break;
           const int h = w >= W;
           w -= h * W;
           int cb = cs, nrb = (Rp - cb + 63) >> 6;
@@ -1345,11 +1346,11 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   //    the panel warp in phase A of the following panel); invert the last here.
   if (warp == 0) {
     const int jl = ((K4 - 1) / kNB) * kNB, nb = K4 - jl;
-    if (nb == kNB) invert_diag16<true>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
-    else invert_diag16<false>(Ah(lane >> 4), Rp, jl, nb, sinvh(lane >> 4), lane & 15);
+    if (nb == kNB) invert_diag16<true>(Ah(hp), Rp, jl, nb, sinvh(hp), lane & 15);
+    else invert_diag16<false>(Ah(hp), Rp, jl, nb, sinvh(hp), lane & 15);
   }
   FMAP_TRACE(1002);
-  for (int e = tid; e < 2 * K4; e += kNT2) {
+  for (int e = tid; e < NS * K4; e += kNT2) {
     const int h = e >= K4, c = e - h * K4;
     xvh(h)[c] = Ah(h)[colbase(c, Rp) + K4];
   }
@@ -1376,7 +1377,7 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
         backsub_block<false, false>(Ah(hp), Rp, xv, xcur, xprev, jb, nbe, jnext, jprev, nprev, g);
       }
     } else if (jprev >= 0 && jnext > 0 && pair_bulk<ISO>(warp)) {
-      for (int e = pair_bt<ISO>(warp, lane); e < 2 * jnext; e += NB_T) {
+      for (int e = pair_bt<ISO>(warp, lane); e < NS * jnext; e += NB_T) {
         const int h = e >= jnext, c = e - h * jnext;
         const float* col = Ah(h) + colbase(c, Rp) + jprev;
         const float* xprev = xvh(h) + 2 * K4 + 16 * (par ^ 1);
@@ -1427,9 +1428,9 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   }
 }
 
-size_t pair_smem_bytes(int k) {
+size_t pair_smem_bytes(int k, int ns) {
   const int K4 = (k + 3) & ~3;
-  return (size_t)(2 * pair_stride_floats(K4) + 8 + 32) * sizeof(float);
+  return (size_t)(ns * pair_stride_floats(K4) + 8 + 32) * sizeof(float);
 }
 
 // Host-side launcher: two systems per CTA when both fit in one SM's shared
@@ -1439,20 +1440,30 @@ cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t 
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t smem2 = pair_smem_bytes(p.k);
+  const size_t smem2 = pair_smem_bytes(p.k, 2), smem1 = pair_smem_bytes(p.k, 1);
   const bool pair = smem2 <= (size_t)optin && !p.force_single;
+  const bool wide = !pair && smem1 <= (size_t)optin && !p.force_single;  // one system, 16 warps
   void (*fn)(SolveParams) = nullptr;
   size_t smem;
   unsigned grid, block;
-  if (pair) {
-    const bool iso = !p.pair_shared_smsp;
-    switch (mask_mode) {
-      case 0: fn = iso ? chol_pair_kernel<0, true> : chol_pair_kernel<0, false>; break;
-      case 1: fn = iso ? chol_pair_kernel<1, true> : chol_pair_kernel<1, false>; break;
-      default: fn = iso ? chol_pair_kernel<2, true> : chol_pair_kernel<2, false>; break;
+  const bool iso = !p.pair_shared_smsp;
+  if (pair || wide) {
+#define FMAP_PICK(NSV)                                                                       \
+  switch (mask_mode) {                                                                       \
+    case 0: fn = iso ? chol_pair_kernel<0, true, NSV> : chol_pair_kernel<0, false, NSV>; break; \
+    case 1: fn = iso ? chol_pair_kernel<1, true, NSV> : chol_pair_kernel<1, false, NSV>; break; \
+    default: fn = iso ? chol_pair_kernel<2, true, NSV> : chol_pair_kernel<2, false, NSV>; break; \
+  }
+    if (pair) {
+      FMAP_PICK(2)
+      smem = smem2;
+      grid = (unsigned)((p.nsys + 1) / 2);
+    } else {
+      FMAP_PICK(1)
+      smem = smem1;
+      grid = (unsigned)p.nsys;
     }
-    smem = smem2;
-    grid = (unsigned)((p.nsys + 1) / 2);
+#undef FMAP_PICK
     block = kNT2;
   } else {
     switch (mask_mode) {
