@@ -1263,36 +1263,9 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
   FMAP_TRACE(1);
 
   // Schedule per panel p (diag(p) already done):
-  //   A  bulk: TRSM(p) rows >= jn, then drain the remaining SYRK(p-1) tiles of
-  //            columns >= jn (disjoint from TRSM(p)); panel warp: invert the
-  //            previous diagonal block for the back substitution
-  //   B  bulk: SYRK(p) of the next panel's columns [jn, jn+nbn)
-  //   C  panel warp: diag(p+1);  bulk: pull SYRK(p) tiles of columns >= jn+nbn
-  //      only until the panel warp raises `diag_done` (elastic: the rest is
-  //      drained in the next phase A), so this barrier waits for the diag only.
-  volatile int* diag_done = reinterpret_cast<volatile int*>(sc + 5);
-  int jpend = -1;  // panel whose trailing SYRK tiles may still be pending
-  auto syrk_rest_tiles = [&](const Panel& Pp, int cs, bool elastic) {
-    if (cs >= K4) return;
-    const int ncb = (K4 - cs + 15) >> 4;
-    int W = 0;
-    for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 63) >> 6;
-    while (true) {
-      int w = 0;
-      if (lane == 0) w = (elastic && *diag_done) ? (1 << 30) : atomicAdd(counter, 1);
-      w = __shfl_sync(0xffffffffu, w, 0);
-      if (w >= NS * W) break;
-      const int h = w >= W;
-      w -= h * W;
-      int cb = cs, nrb = (Rp - cb + 63) >> 6;
-      while (w >= nrb) {
-        w -= nrb;
-        cb += 16;
-        nrb = (Rp - cb + 63) >> 6;
-      }
-      syrk_warp_tile<true>(Ah(h), Rp, K4, Pp, kNB, cb, cb + (w << 6), 0, 0, lane);
-    }
-  };
+  //   A  bulk: TRSM(p) rows >= jn (both systems)
+  //   B  bulk: SYRK(p) of the next panel's columns [jn, jn+nbn) (incl. its diag block)
+  //   C  panel warp: diag(p+1) of both systems || bulk: SYRK(p) of columns >= jn+nbn
   for (int j = 0; j < K4; j += kNB) {
     const int ts = 8 + (j / kNB) * 8;
     const int nbe = min(kNB, K4 - j);
@@ -1300,7 +1273,8 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     const int nbn = min(kNB, K4 - jn);
     const Panel Pj(j, Rp);
     const bool full = nbe == kNB;
-    // A
+    // A  (the panel warp, idle here, inverts the previous panel's diagonal block
+    //     in place for the back substitution: L11(p-1) is final, TRSM(p-1) done)
     if (warp == kPW2 && j >= kNB)
       invert_diag16<true>(Ah(hp), Rp, j - kNB, kNB, sinvh(hp), lane & 15);
     if (pair_bulk<ISO>(warp)) {
@@ -1310,14 +1284,10 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
         if (full) trsm_row<true>(Ah(h), Pj, sinvh(h), nbe, r);
         else trsm_row<false>(Ah(h), Pj, sinvh(h), nbe, r);
       }
-      if (jpend >= 0) syrk_rest_tiles(Panel(jpend, Rp), jn, false);
     }
+    if (tid == 0) *counter = 0;
     FMAP_TRACE(ts + 0);
     __syncthreads();
-    if (tid == 0) {
-      *counter = 0;
-      *diag_done = 0;
-    }
     if (nbn <= 0) break;
     // B
     if (pair_bulk<ISO>(warp)) {
@@ -1342,13 +1312,30 @@ __global__ void __launch_bounds__(kNT2, 1) chol_pair_kernel(SolveParams p) {
     if (warp == kPW2) {
       if (nbn == kNB) diag16_x1<true>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
       else diag16_x1<false>(Ah(hp), Rp, jn, nbn, sinvh(hp), xb, lane, pivmin, bad);
-      __syncwarp();
-      if (lane == 0) *diag_done = 1;
       FMAP_TRACE(ts + 2);
     } else if (pair_bulk<ISO>(warp)) {
-      syrk_rest_tiles(Pj, jn + nbn, true);
+      const int cs = jn + nbn;
+      if (cs < K4) {  // SYRK(p) is always a full 16-wide panel here
+        const int ncb = (K4 - cs + 15) >> 4;
+        int W = 0;
+        for (int u = 0; u < ncb; ++u) W += (Rp - (cs + 16 * u) + 63) >> 6;
+        while (true) {
+          int w = 0;
+          if (lane == 0) w = atomicAdd(counter, 1);
+          w = __shfl_sync(0xffffffffu, w, 0);
+          if (w >= NS * W) break;
+          const int h = w >= W;
+          w -= h * W;
+          int cb = cs, nrb = (Rp - cb + 63) >> 6;
+          while (w >= nrb) {
+            w -= nrb;
+            cb += 16;
+            nrb = (Rp - cb + 63) >> 6;
+          }
+          syrk_warp_tile<true>(Ah(h), Rp, K4, Pj, nbe, cb, cb + (w << 6), 0, 0, lane);
+        }
+      }
     }
-    jpend = j;
     FMAP_TRACE(ts + 4);
     __syncthreads();
   }
