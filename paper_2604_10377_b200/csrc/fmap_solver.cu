@@ -25,6 +25,7 @@
 
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 namespace fmap {
 
@@ -1440,6 +1441,12 @@ cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t 
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // tensor-core solver (tcgen05 + TMEM) unless FMAP_SOLVER=simt
+  {
+    const char* sel = std::getenv("FMAP_SOLVER");
+    const bool simt = sel && sel[0] == 's';
+    if (!simt && !p.force_single && tc_supported(p.k, optin)) return launch_chol_tc(p, mask_mode, stream);
+  }
   const size_t smem2 = pair_smem_bytes(p.k, 2), smem1 = pair_smem_bytes(p.k, 1);
   const bool pair = smem2 <= (size_t)optin && !p.force_single;
   const bool wide = !pair && smem1 <= (size_t)optin && !p.force_single;  // one system, 16 warps

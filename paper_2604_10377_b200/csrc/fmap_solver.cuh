@@ -73,4 +73,8 @@ __host__ __device__ __forceinline__ size_t solver_smem_bytes(int k) {
   return (size_t)(packed_size(K4) + 2 * K4 + 104 + 32) * sizeof(float);
 }
 
+// Tensor-core (tcgen05 / TMEM) solver, fmap_tc.cu.
+bool tc_supported(int k, int optin_smem);
+cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream);
+
 }  // namespace fmap
