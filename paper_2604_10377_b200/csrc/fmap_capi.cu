@@ -179,9 +179,11 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   const size_t nsys = (size_t)b * k;
   const bool need_mask_scratch = opts.compute_residual && mask_mode != 0;
   const size_t res_partial = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
+  const bool use_tc = tc_supported((int)k, ctx->max_smem_optin) && !std::getenv("FMAP_FORCE_SINGLE");
+  const size_t tc_bytes = use_tc ? tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms) : 0;
   const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
                                      need_mask_scratch ? (size_t)b * kk * sizeof(float) : 0,
-                                     (size_t)k * sizeof(float)});
+                                     (size_t)k * sizeof(float), tc_bytes});
   const uint64_t required = (uint64_t)scratch + host_staging_bytes;
   if (rep) rep->peak_extra_bytes = required;
   if (opts.has_memory_cap && required > opts.memory_cap_bytes) {
@@ -201,6 +203,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   double* res_out = cv.take<double>((size_t)b);
   float* mask_scratch = cv.take<float>(need_mask_scratch ? (size_t)b * kk : 0);
   float* zrow = cv.take<float>((size_t)k);
+  float* tc_scr = cv.take<float>(tc_bytes / sizeof(float));
 
   if ((st = reset_ctrl(ctx))) return st;
   ctx->launches = 0;
@@ -235,6 +238,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   p.fail_min = d_fail(ctx);
   p.rcond_min_bits = d_rcond(ctx);
   p.flags = d_flags(ctx);
+  p.tc_scratch = use_tc ? tc_scr : nullptr;
 
   // debug: FMAP_TRACE_FILE=<path> dumps per-warp clock64 phase stamps of one block
   const char* trace_file = std::getenv("FMAP_TRACE_FILE");

@@ -1445,7 +1445,8 @@ cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t 
   {
     const char* sel = std::getenv("FMAP_SOLVER");
     const bool simt = sel && sel[0] == 's';
-    if (!simt && !p.force_single && tc_supported(p.k, optin)) return launch_chol_tc(p, mask_mode, stream);
+    if (!simt && !p.force_single && p.tc_scratch && tc_supported(p.k, optin))
+      return launch_chol_tc(p, mask_mode, stream);
   }
   const size_t smem2 = pair_smem_bytes(p.k, 2), smem1 = pair_smem_bytes(p.k, 1);
   const bool pair = smem2 <= (size_t)optin && !p.force_single;

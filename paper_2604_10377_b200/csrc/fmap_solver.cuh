@@ -54,6 +54,7 @@ struct SolveParams {
   unsigned long long* fail_min;  // lowest failing global system index
   unsigned int* rcond_min_bits;  // float bits of the smallest rcond estimate
   unsigned int* flags;           // validation flags (bit 5: empty spectrum)
+  float* tc_scratch;             // tensor-core solver: per-CTA L scratch (tc_scratch_bytes)
   long long* trace;              // debug phase trace (nullptr = off)
   int trace_block;
   int force_single;              // debug: force one system per CTA
@@ -75,6 +76,7 @@ __host__ __device__ __forceinline__ size_t solver_smem_bytes(int k) {
 
 // Tensor-core (tcgen05 / TMEM) solver, fmap_tc.cu.
 bool tc_supported(int k, int optin_smem);
+size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms);
 cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream);
 
 }  // namespace fmap

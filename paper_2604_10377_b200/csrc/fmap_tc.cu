@@ -53,16 +53,23 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTL = 128;  // TMEM lanes / tile-A rows
 
 struct TcLayout {
-  int K16, s, P, tl_warps, threads;
+  int K16, s, P, tl_warps, nmain, bwarp, threads;
   int tmem_cols;
   int Rop;  // operand buffer rows
+  int cps;  // CTAs per SM
   // offsets in floats from the dynamic smem base
-  int off_hi, off_lo, off_tri, off_lp, off_l11, off_inv, off_yv, off_xv, off_zb, off_red;
-  int off_misc;  // 64 floats: mbarriers + scalars
+  int off_hi, off_lo, off_tri, off_lp, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_misc;
   int floats;
+  long long lb;  // floats of one L scratch slot (global memory)
 };
 
 __host__ __device__ inline int tri_size(int s) { return ((s * (s + 1) / 2) + 3) & ~3; }
+
+// First float of block p's L21 rows in an L scratch slot: block p holds rows
+// 16p+16 .. K16-1, 16 floats each.
+__host__ __device__ inline long long lb_off(int p, int K16) {
+  return 16ll * p * (K16 - 16) - 128ll * p * (p - 1);
+}
 
 __host__ inline TcLayout make_layout(int k) {
   TcLayout L{};
@@ -70,7 +77,9 @@ __host__ inline TcLayout make_layout(int k) {
   L.s = L.K16 > kTL ? L.K16 - kTL : 0;
   L.P = L.K16 / 16;
   L.tl_warps = (L.s + 1 + 31) / 32;  // top-left rows + the augmented rhs "row"
-  L.threads = 128 + 32 * L.tl_warps;
+  L.nmain = 128 + 32 * L.tl_warps;
+  L.bwarp = L.nmain / 32;            // back-substitution warp
+  L.threads = L.nmain + 32;
   int c = 32;
   while (c < L.K16) c <<= 1;
   L.tmem_cols = c;
@@ -80,14 +89,20 @@ __host__ inline TcLayout make_layout(int k) {
   L.off_lo = o;  o += L.Rop * 16;
   L.off_tri = o; o += tri_size(L.s);
   L.off_lp = o;  o += (L.s > 0 ? L.s : 1) * 16;
-  L.off_l11 = o; o += L.P * 256;
-  L.off_inv = o; o += L.P * 16;
-  L.off_yv = o;  o += L.K16;
-  L.off_xv = o;  o += L.K16;
+  L.off_lt = o;  o += 256 + 16;               // current diagonal block (transposed) + 1/L_tt
+  L.off_l11 = o; o += 2 * L.P * 136;          // per slot: packed lower L_bb of every block
+  L.off_yv = o;  o += 2 * L.K16;              // per slot: y = L^{-1} r
+  L.off_xv = o;  o += L.K16;                  // back substitution: x
+  L.off_lb = o;  o += 2 * (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;  // back substitution: L block buffers
   L.off_zb = o;  o += 32;
-  L.off_red = o; o += (L.threads / 32) * 16;
   L.off_misc = o; o += 64;
   L.floats = o;
+  L.lb = (lb_off(L.P, L.K16) + 31) & ~31ll;
+  const int cps_tmem = 512 / L.tmem_cols;
+  const size_t bytes = (size_t)L.floats * 4 + 1024;
+  const int cps_smem = (int)(233472 / bytes);
+  L.cps = cps_tmem < cps_smem ? cps_tmem : cps_smem;
+  if (L.cps < 1) L.cps = 1;
   return L;
 }
 
@@ -200,6 +215,24 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+// Named barrier over the main (factorization) warps only.
+__device__ __forceinline__ void main_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+
 __device__ __forceinline__ float rsqrt_fast(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -270,8 +303,10 @@ __device__ __forceinline__ void diag_factor(float (&a)[16], float& inv, int g, b
   }
 }
 
-// l = L11^{-1}-solve of one row:  l[t] = (a[t] - sum_{u<t} l[u] L11[t][u]) * inv[t]
-__device__ __forceinline__ void trsm_row(const float* __restrict__ L11, const float* __restrict__ inv,
+// l = L11^{-1}-solve of one row:  l[t] = (a[t] - sum_{u<t} l[u] L11[t][u]) * inv[t],
+// right-looking over the TRANSPOSED block LT[t][c] = L11[c][t] (column t is one
+// broadcast LDS.128 run); chain 16 x (FMUL + FFMA).
+__device__ __forceinline__ void trsm_row(const float* __restrict__ LT, const float* __restrict__ inv,
                                          const float (&a)[16], float (&l)[16]) {
   float v[16];
 #pragma unroll
@@ -279,41 +314,84 @@ __device__ __forceinline__ void trsm_row(const float* __restrict__ L11, const fl
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
     l[t] = v[t] * inv[t];
-    // right-looking: v[c] -= l[t] * L11[c][t] for c > t
 #pragma unroll
-    for (int c = t + 1; c < 16; ++c) v[c] = fmaf(-l[t], L11[c * 16 + t], v[c]);
+    for (int c4 = (t + 1) >> 2; c4 < 4; ++c4) {
+      const float4 col = *reinterpret_cast<const float4*>(LT + t * 16 + 4 * c4);
+      if (4 * c4 > t) v[4 * c4] = fmaf(-l[t], col.x, v[4 * c4]);
+      if (4 * c4 + 1 > t) v[4 * c4 + 1] = fmaf(-l[t], col.y, v[4 * c4 + 1]);
+      if (4 * c4 + 2 > t) v[4 * c4 + 2] = fmaf(-l[t], col.z, v[4 * c4 + 2]);
+      if (4 * c4 + 3 > t) v[4 * c4 + 3] = fmaf(-l[t], col.w, v[4 * c4 + 3]);
+    }
   }
 }
 
-}  // namespace
+// Debug phase trace (FMAP_TRACE_FILE): clock64 stamps of one CTA's second system.
+#define TC_TRACE(cond, slot)                                                              \
+  do {                                                                                    \
+    if (p.trace && tr_on && (cond)) p.trace[(slot)] = clock64();                          \
+  } while (0)
 
+// Launch-local system number sl -> (pair q, row i).  A full batch is walked pair-
+// interleaved (consecutive sl hit different pairs), so the CTAs running at the
+// same time read different Gram matrices instead of all hammering one.
+__device__ __forceinline__ void sys_of(const SolveParams& p, int64_t sl, int64_t& q, int& i) {
+  const int k = p.k;
+  if (p.sys_offset == 0 && p.nsys % k == 0) {
+    const int64_t b = p.nsys / k;
+    q = sl % b;
+    i = (int)(sl / b);
+  } else {
+    const int64_t sys = p.sys_offset + sl;
+    q = sys / k;
+    i = (int)(sys - q * k);
+  }
+}
+
+// Load the 16 entries of row `row` in columns 16cb..16cb+15 (G[c][row], lower part
+// c <= row only; coalesced across the warp's consecutive rows).
+__device__ __forceinline__ void load_cols(const float* __restrict__ Gq, int k, int row, bool ok, int cb,
+                                          float (&v)[16]) {
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int c = 16 * cb + t;
+    v[t] = (ok && c <= row && c < k) ? __ldg(Gq + (size_t)c * k + row) : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Main warps (0..nmain/32-1): staging + blocked factorization of system n of this
+// CTA into slot n&1; the back-substitution warp solves L^T x = y for system n-1
+// meanwhile and writes the row of C.
 // ---------------------------------------------------------------------------
 template <int MASK_MODE, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLayout Ly) {
   extern __shared__ __align__(1024) float smem[];
   const int k = p.k, K16 = Ly.K16, s = Ly.s, P = Ly.P;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nthreads = Ly.threads;
+  const int NM = Ly.nmain;
   float* opnd_hi = smem + Ly.off_hi;
   float* opnd_lo = smem + Ly.off_lo;
   float* tri = smem + Ly.off_tri;
   float* Lp = smem + Ly.off_lp;
-  float* L11all = smem + Ly.off_l11;
-  float* invall = smem + Ly.off_inv;
-  float* yv = smem + Ly.off_yv;
-  float* xv = smem + Ly.off_xv;
+  float* LT = smem + Ly.off_lt;  // current diagonal block, transposed: LT[t][c] = L[c][t]
+  float* inv = LT + 256;         // 1/L_tt of the current block
   float* zb = smem + Ly.off_zb;
-  float* red = smem + Ly.off_red;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + Ly.off_misc);  // [0] LA, [1] REST
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 4);
-  unsigned* sc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 8);
-  // sc[0] dmax bits, sc[1] pivmin bits, sc[2] bad, sc[3] ev_max bits, sc[4] nonfinite
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + Ly.off_misc);
+  // mbar[0] LA, [1] REST, [2..3] lfull (back-sub L blocks), [4..5] fact (slot), [6..7] bsub (slot)
+  uint64_t* lfull = mbar + 2;
+  uint64_t* fact = mbar + 4;
+  uint64_t* bsub = mbar + 6;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 16);
+  unsigned* sc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 20);
+  // sc[0] dmax bits, sc[1] pivmin bits, sc[2] bad, sc[3] ev_max bits (current system)
+  unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 32);  // [slot][4]
+  float* Lscr = p.tc_scratch + (size_t)blockIdx.x * 2 * Ly.lb;
 
   // ---- one-time setup ----
-  for (int e = tid; e < 2 * Ly.Rop * 16; e += nthreads) smem[Ly.off_hi + e] = 0.f;
+  for (int e = tid; e < 2 * Ly.Rop * 16; e += Ly.threads) smem[Ly.off_hi + e] = 0.f;
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) mbar_init(&mbar[e], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, (uint32_t)Ly.tmem_cols);
@@ -322,7 +400,113 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
-  // row ownership
+  // ======================= back-substitution warp =======================
+  if (warp == Ly.bwarp) {
+    float* xv = smem + Ly.off_xv;
+    float* lbuf = smem + Ly.off_lb;
+    const int lbs = (K16 - 16 > 0 ? K16 - 16 : 1) * 16;  // floats per L block buffer
+    uint32_t lb_use = 0;  // global L-block counter (lfull phases: block use u -> buffer u&1)
+    int n = 0;
+    for (int64_t sl = blockIdx.x; sl < p.nsys; sl += gridDim.x, ++n) {
+      const int slot = n & 1;
+      int64_t q;
+      int i;
+      sys_of(p, sl, q, i);
+      const int64_t sys = q * k + i;  // global system index (error convention)
+      mbar_wait(&fact[slot], (n >> 1) & 1);
+      unsigned* ssc = slotsc + 4 * slot;
+      if (ssc[3] == 0u) {
+        const float* L11 = smem + Ly.off_l11 + slot * P * 136;
+        const float* yv = smem + Ly.off_yv + slot * K16;
+        const float* Lsl = Lscr + (size_t)slot * Ly.lb;
+        // blocks b = P-2 .. 0 carry L rows below them; prefetch the first one
+        auto issue_blk = [&](int b, uint32_t use) {
+          const uint32_t bytes = (uint32_t)(K16 - 16 * b - 16) * 64u;
+          if (lane == 0) {
+            mbar_expect_tx(&lfull[use & 1], bytes);
+            bulk_g2s(lbuf + (use & 1) * lbs, Lsl + lb_off(b, K16), bytes, &lfull[use & 1]);
+          }
+        };
+        if (P >= 2) issue_blk(P - 2, lb_use);
+        for (int b = P - 1; b >= 0; --b) {
+          // lanes 0..15: column u = lane of W_b = L_bb^{-1} (independent of x)
+          const float* Lbb = L11 + b * 136;
+          float w[16];
+          {
+            const int u = lane & 15;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              float acc = (t == u) ? 1.f : 0.f;
+#pragma unroll
+              for (int v = 0; v < t; ++v) acc = fmaf(-Lbb[t * (t + 1) / 2 + v], w[v], acc);
+              w[t] = (t >= u) ? acc / Lbb[t * (t + 1) / 2 + t] : 0.f;
+            }
+          }
+          // s_t = sum_{c >= 16b+16} L[c][16b+t] x_c   (lane: rows rho = lane>>2 + 8m, cols 4(lane&3)..)
+          float v4[4] = {0.f, 0.f, 0.f, 0.f};
+          const int R = K16 - 16 * b - 16;
+          if (R > 0) {
+            const uint32_t use = lb_use++;
+            mbar_wait(&lfull[use & 1], (use >> 1) & 1);
+            if (b >= 1) issue_blk(b - 1, lb_use);  // prefetch the next block (other buffer)
+            const float* blk = lbuf + (use & 1) * lbs;
+            for (int rho = lane >> 2; rho < R; rho += 8) {
+              const float xc = xv[16 * b + 16 + rho];
+              const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
+              v4[0] = fmaf(l4.x, xc, v4[0]);
+              v4[1] = fmaf(l4.y, xc, v4[1]);
+              v4[2] = fmaf(l4.z, xc, v4[2]);
+              v4[3] = fmaf(l4.w, xc, v4[3]);
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) v4[e] += __shfl_xor_sync(kFull, v4[e], o);
+            __syncwarp();  // everyone done with this buffer before it is refilled
+          }
+          // lane t (< 16): z_t = y_t - s_t ; x_t = sum_{u >= t} W[u][t] z_u
+          const int t = lane & 15;
+          float st = 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float other = __shfl_sync(kFull, v4[e], (t >> 2));  // lane (t>>2) holds cols 4(t>>2)..
+            if ((t & 3) == e) st = other;
+          }
+          const float z = yv[16 * b + t] - st;
+          float x = 0.f;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const float zu = __shfl_sync(kFull, z, u);
+            x = fmaf(w[u], zu, x);  // w[u] = W[u][t] (lane t holds column t); zero for u < t
+          }
+          if (lane < 16) xv[16 * b + t] = x;
+          __syncwarp();
+        }
+        // row of C, singularity verdict
+        float* Crow = p.C + ((size_t)q * k + i) * k;
+        bool nf = false;
+        for (int c = lane; c < k; c += 32) {
+          const float x = xv[c];
+          nf |= !(fabsf(x) <= FLT_MAX);
+          Crow[c] = x;
+        }
+        nf = __any_sync(kFull, nf);
+        if (lane == 0) {
+          const float dm = __uint_as_float(ssc[0]);
+          const float pm = __uint_as_float(ssc[1]);
+          float rc = dm > 0.f ? pm / dm : 0.f;
+          if (!(rc >= 0.f)) rc = 0.f;
+          if (ssc[2] || nf || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)sys);
+          atomicMin(p.rcond_min_bits, __float_as_uint(rc));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bsub[slot]);
+    }
+    return;
+  }
+
+  // ======================= main warps =======================
   const bool tileA = warp < 4;
   const int row = tileA ? s + 32 * warp + lane : 32 * (warp - 4) + lane;
   const bool row_valid = tileA ? row < K16 : row < s;
@@ -330,82 +514,88 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
   const uint32_t trow = tbase + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quarter
   const int tri_row = row * (row + 1) / 2;
 
-  uint32_t g = 0;  // global panel counter (mbarrier phases)
+  uint32_t g = 0;  // global panel counter (LA / REST mbarrier phases)
   bool any_mma = false;
 
-  for (int64_t sl = blockIdx.x; sl < p.nsys; sl += gridDim.x) {
-    const int64_t sys = p.sys_offset + sl;
-    const int64_t q = sys / k;
-    const int i = (int)(sys - q * k);
+  int n = 0;
+  for (int64_t sl = blockIdx.x; sl < p.nsys; sl += gridDim.x, ++n) {
+    const int slot = n & 1;
+    int64_t q;
+    int i;
+    sys_of(p, sl, q, i);
+    const bool tr_on = blockIdx.x == (unsigned)p.trace_block && n == 1;
+    TC_TRACE(tid == 0, 0);
+    float* L11all = smem + Ly.off_l11 + slot * P * 136;
+    float* yv = smem + Ly.off_yv + slot * K16;
+    float* Lslot = Lscr + (size_t)slot * Ly.lb;
 
-    // previous system's MMAs must be complete before TMEM / operands are reused
-    if (any_mma) {
-      mbar_wait(&mbar[1], (g - 1) & 1);
-      tc_fence_after();
-    }
-    if (tid == 0) {  // tid 0 is also the last reader of the previous system's scalars
+    // slot reuse: the back-substitution of system n-2 must be done with it
+    if (n >= 2) mbar_wait(&bsub[slot], ((n - 2) >> 1) & 1);
+    if (tid == 0) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) sc[e] = 0u;
+      for (int e = 0; e < 4; ++e) sc[e] = 0u;
       sc[1] = __float_as_uint(FLT_MAX);
     }
-    __syncthreads();
-
     float ev_max = 0.f;
+    bool skip = false;
     if constexpr (MASK_MODE == 1) {
+      main_sync(NM);
       float m = 0.f;
-      for (int c = tid; c < k; c += nthreads)
+      for (int c = tid; c < k; c += NM)
         m = fmaxf(m, fmaxf(p.ev1[(size_t)q * k + c], p.ev2[(size_t)q * k + c]));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
       if (lane == 0) atomicMax(&sc[3], __float_as_uint(m));
-      __syncthreads();
+      main_sync(NM);
       ev_max = __uint_as_float(sc[3]);
-      if (!(ev_max > 0.f)) {
-        if (tid == 0) atomicOr(p.flags, 32u);
-        continue;  // uniform across the CTA
-      }
+      skip = !(ev_max > 0.f);
     }
 
     // ---- staging: row r of (G + lambda*diag(m_i) + ridge*I), identity padding ----
-    // G is read as columns (G[c][r], coalesced across the warp's rows); the lower
-    // triangle used here is G's upper triangle, as the packed-column solver does.
+    // G is read as columns (G[c][r]); the lower triangle used here is G's upper
+    // triangle, as in the packed-column SIMT solver.  Two 16-column groups of
+    // loads in flight per thread.
+    TC_TRACE(tid == 0, 398);
+    float rhs = 0.f, dmax = 0.f, dadd = 0.f;
+    const bool ld_ok = row_valid && row < k && !skip;
+    if (ld_ok) {
+      rhs = p.rhs_unit < 0 ? p.rhs[((size_t)q * k + i) * k + row] : (row == p.rhs_unit ? 1.f : 0.f);
+      dadd = p.lambda * mask_entry<MASK_MODE>(p, q, i, row, ev_max) + p.ridge;
+    }
     const float* Gq = p.gram + (size_t)q * k * k;
-    float rhs = 0.f;
-    float dmax = 0.f;
-    if (row_valid) {
-      if (row < k) {
-        rhs = p.rhs_unit < 0 ? p.rhs[((size_t)q * k + i) * k + row] : (row == p.rhs_unit ? 1.f : 0.f);
-      }
+    // previous system's MMAs must be complete before TMEM is rewritten
+    if (any_mma) {
+      mbar_wait(&mbar[1], (g - 1) & 1);
+      tc_fence_after();
     }
-    float dval = 1.f;
-    if (row_valid && row < k) {
-      dval = Gq[(size_t)row * k + row] + (p.lambda * mask_entry<MASK_MODE>(p, q, i, row, ev_max) + p.ridge);
-      dmax = fabsf(dval);
-    }
-    if (tileA) {
-      for (int cb = 0; cb < K16; cb += 16) {
-        float v[16];
+    TC_TRACE(tid == 0, 399);
+    {
+      const int ncb = tileA ? P : ((row_valid ? row : 0) >> 4) + 1;  // top-left: only c <= row
+      float cur[16], nxt[16];
+      load_cols(Gq, k, row, ld_ok, 0, cur);
+      for (int cb = 0; cb < P; ++cb) {
+        if (cb + 1 < P) load_cols(Gq, k, row, ld_ok && cb + 1 < ncb, cb + 1, nxt);
+        if (row_valid && (row >> 4) == cb) {  // diagonal entry
+          const int t = row & 15;
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          const int c = cb + t;
-          float x = 0.f;
-          if (row_valid) {
-            if (c == row) x = dval;
-            else if (row < k && c < k) x = __ldg(Gq + (size_t)c * k + row);
-          }
-          v[t] = x;
+          for (int u = 0; u < 16; ++u)
+            if (u == t) {
+              cur[u] = row < k ? cur[u] + dadd : 1.f;
+              dmax = row < k ? fabsf(cur[u]) : 0.f;
+            }
         }
-        tmem_st16(trow + (uint32_t)cb, v);
-      }
-      tmem_st_wait();
-    } else if (row_valid) {
-      for (int c = 0; c <= row; ++c) {
-        float x = 0.f;
-        if (c == row) x = dval;
-        else if (row < k && c < k) x = __ldg(Gq + (size_t)c * k + row);
-        tri[tri_row + c] = x;
+        if (tileA) {
+          tmem_st16(trow + (uint32_t)(16 * cb), cur);
+        } else if (row_valid && cb < ncb) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (16 * cb + t <= row) tri[tri_row + 16 * cb + t] = cur[t];
+        }
+#pragma unroll
+        for (int t = 0; t < 16; ++t) cur[t] = nxt[t];
       }
     }
+    if (tileA) tmem_st_wait();
     {
       float m = dmax;
 #pragma unroll
@@ -413,8 +603,9 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
       if (lane == 0) atomicMax(&sc[0], __float_as_uint(m));
     }
     tc_fence_before();
-    __syncthreads();
+    main_sync(NM);
     tc_fence_after();
+    TC_TRACE(tid == 0, 1);
 
     float pivmin = FLT_MAX;
     unsigned bad = 0u;
@@ -438,6 +629,7 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
           tc_fence_after();
         }
         tmem_ld16(trow + (uint32_t)j, a);
+        TC_TRACE(tid == 0, 2 + 4 * pp);
       } else {
 #pragma unroll
         for (int t = 0; t < 16; ++t) a[t] = (active && j + t <= row) ? tri[tri_row + j + t] : 0.f;
@@ -445,8 +637,6 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
       // b. diagonal block
       const bool in_diag = active && row < j + 16;
       const int dwarp = j >= s ? (j - s) >> 5 : 4 + (j >> 5);
-      float* L11 = L11all + pp * 256;
-      float* inv = invall + pp * 16;
       if (warp == dwarp) {
         float d[16];
 #pragma unroll
@@ -455,41 +645,48 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
         diag_factor(d, iv, lane & 15, in_diag && row < k, pivmin, bad);
         if (in_diag) {
           const int gr = row - j;
+          float* Lpk = L11all + pp * 136 + gr * (gr + 1) / 2;  // packed copy for the back-sub warp
 #pragma unroll
-          for (int t = 0; t < 16; ++t) L11[gr * 16 + t] = (t <= gr) ? d[t] : 0.f;
+          for (int t = 0; t < 16; ++t) {
+            LT[t * 16 + gr] = (t <= gr) ? d[t] : 0.f;  // transposed, for the TRSM
+            if (t <= gr) Lpk[t] = d[t];
+          }
           inv[gr] = iv;
           zb[gr] = rhs;
 #pragma unroll
           for (int t = 0; t < 16; ++t) a[t] = d[t];
         }
+        TC_TRACE(row == j, 3 + 4 * pp);
       }
-      __syncthreads();
+      main_sync(NM);
       // c. TRSM rows >= j+16 ; augmented row -> y for this panel
       float l[16];
       const bool trsm = active && row >= j + 16;
       if (trsm) {
-        trsm_row(L11, inv, a, l);
+        trsm_row(LT, inv, a, l);
       } else if (is_aug) {
         float z[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) z[t] = zb[t];
-        trsm_row(L11, inv, z, l);
+        trsm_row(LT, inv, z, l);
 #pragma unroll
         for (int t = 0; t < 16; ++t) yv[j + t] = l[t];
       } else {
 #pragma unroll
         for (int t = 0; t < 16; ++t) l[t] = in_diag ? a[t] : 0.f;
       }
-      // d. store L: TMEM (tile A, kept for back substitution), smem tri (top-left),
+      // d. store L: scratch (back substitution), smem tri (top-left rows),
       //    operand hi/lo (rows >= j+16)
-      if (tileA) {
-        tmem_st16(trow + (uint32_t)j, l);
-      } else if (active && !is_aug) {
+      if (!tileA && active && !is_aug) {
 #pragma unroll
         for (int t = 0; t < 16; ++t)
           if (j + t <= row) tri[tri_row + j + t] = l[t];
       }
       if (trsm) {
+        float4* dst = reinterpret_cast<float4*>(Lslot + lb_off(pp, K16) + (size_t)(row - j - 16) * 16);
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4)
+          __stcg(dst + c4, make_float4(l[4 * c4], l[4 * c4 + 1], l[4 * c4 + 2], l[4 * c4 + 3]));
         if (pp > 0) mbar_wait(&mbar[1], (g - 1) & 1);  // previous REST MMA done reading
         float* h = opnd_hi + opnd_idx(row, 0);
         float* lo = opnd_lo + opnd_idx(row, 0);
@@ -508,10 +705,10 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
                 make_float4(l[4 * c4], l[4 * c4 + 1], l[4 * c4 + 2], l[4 * c4 + 3]);
         }
       }
-      if (tileA) tmem_st_wait();
+      TC_TRACE(tid == 0, 4 + 4 * pp);
       fence_async_smem();
       tc_fence_before();
-      __syncthreads();
+      main_sync(NM);
       tc_fence_after();
       // e. tensor-core trailing update: lookahead (next panel) then the rest
       if (tid == 0) {
@@ -520,24 +717,9 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
         const uint32_t arow = (uint32_t)(s >> 3) * 512u;
         if (r0 < K16) {
           int c0 = r0;
-          // lookahead: 16 columns
-          {
-            const uint32_t id = idesc_tf32(16);
-            const uint32_t brow = (uint32_t)(c0 >> 3) * 512u;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              const uint32_t ko = (uint32_t)ks * 256u;
-              const uint64_t ah = sdesc(hib + arow + ko), al = sdesc(lob + arow + ko);
-              const uint64_t bh = sdesc(hib + brow + ko), bl = sdesc(lob + brow + ko);
-              mma_tf32(tbase + (uint32_t)c0, ah, bh, id);
-              mma_tf32(tbase + (uint32_t)c0, ah, bl, id);
-              mma_tf32(tbase + (uint32_t)c0, al, bh, id);
-            }
-          }
-          mma_commit(&mbar[0]);
-          c0 += 16;
+          int N = 16;
+          bool first = true;
           while (c0 < K16) {
-            const int N = min(256, K16 - c0);
             const uint32_t id = idesc_tf32(N);
             const uint32_t brow = (uint32_t)(c0 >> 3) * 512u;
 #pragma unroll
@@ -549,13 +731,17 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
               mma_tf32(tbase + (uint32_t)c0, ah, bl, id);
               mma_tf32(tbase + (uint32_t)c0, al, bh, id);
             }
+            if (first) mma_commit(&mbar[0]);
+            first = false;
             c0 += N;
+            N = min(256, K16 - c0);
           }
           mma_commit(&mbar[1]);
         } else {
           mma_commit(&mbar[0]);
           mma_commit(&mbar[1]);
         }
+        TC_TRACE(true, 5 + 4 * pp);
       }
       any_mma = true;
       // top-left SIMT trailing update (rows j+16..s-1, columns j+16..row)
@@ -573,12 +759,15 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
           }
           tri[tri_row + c] -= acc;
         }
+        TC_TRACE(row == s - 1, 300 + pp);
       }
 #pragma unroll
       for (int t = 0; t < 16; ++t) lprev[t] = trsm ? l[t] : 0.f;
     }
+    TC_TRACE(tid == 0, 200);
 
-    // ---- singularity bookkeeping ----
+    // ---- hand the system to the back-substitution warp ----
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // L scratch -> bulk-copy reads
     {
       unsigned b = bad;
       float pm = pivmin;
@@ -592,133 +781,45 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
         atomicMin(&sc[1], __float_as_uint(fmaxf(pm, 0.f)));
       }
     }
-
-    // ---- back substitution  L^T x = y ----
-    // B0: invert the diagonal blocks, W_b = L_bb^{-1} (column u of block b per
-    //     thread) into the operand buffer, idle once the last MMA has landed
-    mbar_wait(&mbar[1], (g - 1) & 1);
-    float* Wall = opnd_hi;
-    for (int e = tid; e < P * 16; e += nthreads) {
-      const int b = e >> 4, u = e & 15;
-      const float* Lb = L11all + b * 256;
-      const float* ib = invall + b * 16;
-      float w[16];
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        float acc = (t == u) ? 1.f : 0.f;
-#pragma unroll
-        for (int v = 0; v < t; ++v) acc = fmaf(-Lb[t * 16 + v], w[v], acc);
-        w[t] = (t >= u) ? acc * ib[t] : 0.f;
-      }
-#pragma unroll
-      for (int t = 0; t < 16; ++t) Wall[b * 256 + t * 16 + u] = w[t];
-    }
-    __syncthreads();
-    // B1: blocks from the bottom
-    float xr = 0.f;  // x of this thread's row (once known)
-    for (int b = P - 1; b >= 0; --b) {
-      const int c0 = 16 * b;
-      float v[16];
-      if (tileA) {
-        float lv[16];
-        tmem_ld16(trow + (uint32_t)c0, lv);
-        const bool use = row_valid && row >= c0 + 16;
-#pragma unroll
-        for (int t = 0; t < 16; ++t) v[t] = use ? lv[t] * xr : 0.f;
-      } else {
-        const bool use = row_valid && row >= c0 + 16;
-#pragma unroll
-        for (int t = 0; t < 16; ++t) v[t] = use ? tri[tri_row + c0 + t] * xr : 0.f;
-      }
-      // warp reduction of the 16-vector: lane (2t, 2t+1) ends with component t
-      {
-        const bool h16 = lane & 16;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float send = h16 ? v[e] : v[e + 8];
-          const float keep = h16 ? v[e + 8] : v[e];
-          v[e] = keep + __shfl_xor_sync(kFull, send, 16);
-        }
-        const bool h8 = lane & 8;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float send = h8 ? v[e] : v[e + 4];
-          const float keep = h8 ? v[e + 4] : v[e];
-          v[e] = keep + __shfl_xor_sync(kFull, send, 8);
-        }
-        const bool h4 = lane & 4;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const float send = h4 ? v[e] : v[e + 2];
-          const float keep = h4 ? v[e + 2] : v[e];
-          v[e] = keep + __shfl_xor_sync(kFull, send, 4);
-        }
-        const bool h2 = lane & 2;
-        {
-          const float send = h2 ? v[0] : v[1];
-          const float keep = h2 ? v[1] : v[0];
-          v[0] = keep + __shfl_xor_sync(kFull, send, 2);
-        }
-        v[0] += __shfl_xor_sync(kFull, v[0], 1);
-        if ((lane & 1) == 0) red[warp * 16 + ((lane >> 1) & 15)] = v[0];
-      }
-      __syncthreads();
-      if (warp == 0 && lane < 16) {
-        float z = yv[c0 + lane];
-        for (int w = 0; w < nthreads / 32; ++w) z -= red[w * 16 + lane];
-        zb[lane] = z;
-        __syncwarp(0xffffu);
-        const float* W = Wall + b * 256;
-        float x = 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (u >= lane) x = fmaf(W[u * 16 + lane], zb[u], x);  // x_t = sum_{u>=t} W[u][t] z_u
-        xv[c0 + lane] = x;
-      }
-      __syncthreads();
-      if (row_valid && row >= c0 && row < c0 + 16) xr = xv[row];
-    }
-    // ---- output row of C ----
-    {
-      float* Crow = p.C + ((size_t)q * k + i) * k;
-      bool nf = false;
-      for (int c = tid; c < k; c += nthreads) {
-        const float x = xv[c];
-        nf |= !(fabsf(x) <= FLT_MAX);
-        Crow[c] = x;
-      }
-      if (__any_sync(kFull, nf) && lane == 0) atomicOr(&sc[4], 1u);
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+    main_sync(NM);
     if (tid == 0) {
-      const float dm = __uint_as_float(sc[0]);
-      const float pm = __uint_as_float(sc[1]);
-      float rc = dm > 0.f ? pm / dm : 0.f;
-      if (!(rc >= 0.f)) rc = 0.f;
-      if (sc[2] || sc[4] || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)sys);
-      atomicMin(p.rcond_min_bits, __float_as_uint(rc));
+      unsigned* ssc = slotsc + 4 * slot;
+      ssc[0] = sc[0];
+      ssc[1] = sc[1];
+      ssc[2] = sc[2];
+      ssc[3] = skip ? 1u : 0u;
+      if (skip) atomicOr(p.flags, 32u);
+      mbar_arrive(&fact[slot]);
     }
+    TC_TRACE(tid == 0, 203);
   }
   // ---- teardown ----
   if (any_mma) {
     mbar_wait(&mbar[1], (g - 1) & 1);
     tc_fence_after();
   }
-  __syncthreads();
+  main_sync(NM);
   if (warp == 0) tmem_dealloc(tbase, (uint32_t)Ly.tmem_cols);
 }
 
-// Host-side launcher for the tensor-core solver.  Returns cudaErrorNotSupported
-// when k is outside its range (the caller then uses the SIMT solver).
+}  // namespace
+
+size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms) {
+  const TcLayout L = make_layout(k);
+  const int64_t maxgrid = (int64_t)num_sms * L.cps;
+  const int64_t grid = nsys < maxgrid ? nsys : maxgrid;
+  return (size_t)grid * 2 * (size_t)L.lb * sizeof(float);
+}
+
 bool tc_supported(int k, int optin_smem) {
   if (k < 1) return false;
   const TcLayout L = make_layout(k);
-  if (L.tmem_cols > 512 || L.threads > 320) return false;
+  if (L.tmem_cols > 512 || L.threads > 352) return false;
   return (size_t)L.floats * 4 <= (size_t)optin_smem;
 }
 
+// Host-side launcher for the tensor-core solver (p.tc_scratch must hold
+// tc_scratch_bytes(k, nsys, SMs)).
 cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream) {
   if (p.nsys <= 0) return cudaSuccess;
   int dev = 0, optin = 0, sms = 0;
@@ -726,35 +827,34 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const TcLayout L = make_layout(p.k);
-  if (L.tmem_cols > 512 || L.threads > 320) return cudaErrorNotSupported;
-  const int cps = 512 / L.tmem_cols;  // CTAs per SM the TMEM allows
-  // cap residency at `cps` CTAs per SM through the shared-memory request, so no
+  if (L.tmem_cols > 512 || L.threads > 352 || !p.tc_scratch) return cudaErrorNotSupported;
+  // cap residency at L.cps CTAs per SM through the shared-memory request, so no
   // CTA ever waits on a TMEM allocation
-  const size_t sm_total = 233472;
   size_t smem = (size_t)L.floats * 4;
-  const size_t floor_req = sm_total / (size_t)(cps + 1) + 1;
+  const size_t floor_req = 233472 / (size_t)(L.cps + 1) + 1;
   if (smem < floor_req) smem = floor_req;
   if (smem > (size_t)optin) {
     if ((size_t)L.floats * 4 > (size_t)optin) return cudaErrorNotSupported;
     smem = (size_t)optin;
   }
   void (*fn)(SolveParams, TcLayout) = nullptr;
-  if (cps >= 2) {  // <= 288 threads, two CTAs per SM
+  if (L.cps >= 2) {  // <= 320 threads, two CTAs per SM
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 288, 2>; break;
-      case 1: fn = chol_tc_kernel<1, 288, 2>; break;
-      default: fn = chol_tc_kernel<2, 288, 2>; break;
+      case 0: fn = chol_tc_kernel<0, 320, 2>; break;
+      case 1: fn = chol_tc_kernel<1, 320, 2>; break;
+      default: fn = chol_tc_kernel<2, 320, 2>; break;
     }
   } else {
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 320, 1>; break;
-      case 1: fn = chol_tc_kernel<1, 320, 1>; break;
-      default: fn = chol_tc_kernel<2, 320, 1>; break;
+      case 0: fn = chol_tc_kernel<0, 352, 1>; break;
+      case 1: fn = chol_tc_kernel<1, 352, 1>; break;
+      default: fn = chol_tc_kernel<2, 352, 1>; break;
     }
   }
+  if (L.cps >= 2 && L.threads > 320) return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t maxgrid = (int64_t)sms * cps;
+  const int64_t maxgrid = (int64_t)sms * L.cps;
   const unsigned grid = (unsigned)(p.nsys < maxgrid ? p.nsys : maxgrid);
   fn<<<grid, L.threads, smem, stream>>>(p, L);
   return cudaGetLastError();
