@@ -52,18 +52,25 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTL = 128;  // TMEM lanes / tile-A rows
 
+// Rows are split into groups of <= 128 from the bottom: group g holds rows
+// [lo[g], hi[g]) on TMEM lanes row - lo[g], and its own TMEM column region for the
+// matrix columns [16, hi[g]) (the panel-0 columns stay in registers):
+//   TMEM column of (group g, matrix column c) = base[g] + c - 16.
+// k = 200 (K16 = 208): rows 80..207 -> 192 columns, rows 0..79 -> 64 columns, 256
+// in total, so two CTAs (two systems) share one SM.
+constexpr int kMaxGroups = 3;
 struct TcLayout {
-  int K16, s, P, tl_warps, nmain, bwarp, threads;
+  int K16, P, G;
+  int lo[kMaxGroups], hi[kMaxGroups], base[kMaxGroups];
+  int nmain, bwarp, mwarp, threads, aug_tid;
   int tmem_cols;
   int Rop;  // operand buffer rows
   int cps;  // CTAs per SM
   // offsets in floats from the dynamic smem base
-  int off_hi, off_lo, off_tri, off_lp, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_misc;
+  int off_hi, off_lo, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_misc;
   int floats;
   long long lb;  // floats of one L scratch slot (global memory)
 };
-
-__host__ __device__ inline int tri_size(int s) { return ((s * (s + 1) / 2) + 3) & ~3; }
 
 // First float of block p's L21 rows in an L scratch slot: block p holds rows
 // 16p+16 .. K16-1, 16 floats each.
@@ -74,35 +81,45 @@ __host__ __device__ inline long long lb_off(int p, int K16) {
 __host__ inline TcLayout make_layout(int k) {
   TcLayout L{};
   L.K16 = (k + 15) & ~15;
-  L.s = L.K16 > kTL ? L.K16 - kTL : 0;
   L.P = L.K16 / 16;
-  L.tl_warps = (L.s + 1 + 31) / 32;  // top-left rows + the augmented rhs "row"
-  L.nmain = 128 + 32 * L.tl_warps;
-  L.bwarp = L.nmain / 32;            // back-substitution warp
-  L.threads = L.nmain + 32;
+  int hi = L.K16, base = 0;
+  L.G = 0;
+  while (hi > 0 && L.G < kMaxGroups) {
+    const int lo = hi > kTL ? hi - kTL : 0;
+    L.lo[L.G] = lo;
+    L.hi[L.G] = hi;
+    L.base[L.G] = base;
+    base += hi - 16;
+    hi = lo;
+    L.G++;
+  }
+  const int total = hi > 0 ? 1 << 30 : base;  // rows left over: unsupported
+  const int ntop = L.hi[L.G - 1] - L.lo[L.G - 1];
+  L.aug_tid = kTL * (L.G - 1) + ntop;
+  L.nmain = 32 * (4 * (L.G - 1) + (ntop + 1 + 31) / 32);
+  L.bwarp = L.nmain / 32;      // back-substitution warp
+  L.mwarp = L.bwarp + 1;       // MMA-issue warp
+  L.threads = L.nmain + 64;
   int c = 32;
-  while (c < L.K16) c <<= 1;
+  while (c < total && c < 1024) c <<= 1;
   L.tmem_cols = c;
   L.Rop = L.K16 > kTL ? L.K16 : kTL;
   int o = 0;
   L.off_hi = o;  o += L.Rop * 16;
   L.off_lo = o;  o += L.Rop * 16;
-  L.off_tri = o; o += tri_size(L.s);
-  L.off_lp = o;  o += (L.s > 0 ? L.s : 1) * 16;
   L.off_lt = o;  o += 256 + 16;               // current diagonal block (transposed) + 1/L_tt
-  L.off_l11 = o; o += 2 * L.P * 136;          // per slot: packed lower L_bb of every block
+  L.off_l11 = o; o += 2 * L.P * 152;          // per slot: packed lower L_bb (+ 1/L_tt) of every block
   L.off_yv = o;  o += 2 * L.K16;              // per slot: y = L^{-1} r
   L.off_xv = o;  o += L.K16;                  // back substitution: x
-  L.off_lb = o;  o += 2 * (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;  // back substitution: L block buffers
+  L.off_lb = o;  o += 2 * (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;  // back substitution: L blocks
   L.off_zb = o;  o += 32;
   L.off_misc = o; o += 64;
   L.floats = o;
   L.lb = (lb_off(L.P, L.K16) + 31) & ~31ll;
-  const int cps_tmem = 512 / L.tmem_cols;
+  const int cps_tmem = L.tmem_cols <= 512 ? 512 / L.tmem_cols : 0;
   const size_t bytes = (size_t)L.floats * 4 + 1024;
   const int cps_smem = (int)(233472 / bytes);
   L.cps = cps_tmem < cps_smem ? cps_tmem : cps_smem;
-  if (L.cps < 1) L.cps = 1;
   return L;
 }
 
@@ -239,13 +256,13 @@ __device__ __forceinline__ float rsqrt_fast(float x) {
   return y;
 }
 
+// x = hi + lo with hi = round-to-nearest TF32; lo is exact in fp32 and the tensor
+// core reads it as TF32 (truncated): |x - hi - tf32(lo)| <= 2^-21 |x|.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h, l;
+  uint32_t h;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  const float rem = x - __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(rem));
   hi = __uint_as_float(h);
-  lo = __uint_as_float(l);
+  lo = x - hi;
 }
 
 // float index of element (r, t) (t < 16) in an operand buffer
@@ -305,22 +322,19 @@ __device__ __forceinline__ void diag_factor(float (&a)[16], float& inv, int g, b
 
 // l = L11^{-1}-solve of one row:  l[t] = (a[t] - sum_{u<t} l[u] L11[t][u]) * inv[t],
 // right-looking over the TRANSPOSED block LT[t][c] = L11[c][t] (column t is one
-// broadcast LDS.128 run); chain 16 x (FMUL + FFMA).
+// broadcast LDS.128 run); chain 16 x (FMUL + FFMA).  `a` is consumed.
 __device__ __forceinline__ void trsm_row(const float* __restrict__ LT, const float* __restrict__ inv,
-                                         const float (&a)[16], float (&l)[16]) {
-  float v[16];
-#pragma unroll
-  for (int t = 0; t < 16; ++t) v[t] = a[t];
+                                         float (&a)[16], float (&l)[16]) {
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
-    l[t] = v[t] * inv[t];
+    l[t] = a[t] * inv[t];
 #pragma unroll
     for (int c4 = (t + 1) >> 2; c4 < 4; ++c4) {
       const float4 col = *reinterpret_cast<const float4*>(LT + t * 16 + 4 * c4);
-      if (4 * c4 > t) v[4 * c4] = fmaf(-l[t], col.x, v[4 * c4]);
-      if (4 * c4 + 1 > t) v[4 * c4 + 1] = fmaf(-l[t], col.y, v[4 * c4 + 1]);
-      if (4 * c4 + 2 > t) v[4 * c4 + 2] = fmaf(-l[t], col.z, v[4 * c4 + 2]);
-      if (4 * c4 + 3 > t) v[4 * c4 + 3] = fmaf(-l[t], col.w, v[4 * c4 + 3]);
+      if (4 * c4 > t) a[4 * c4] = fmaf(-l[t], col.x, a[4 * c4]);
+      if (4 * c4 + 1 > t) a[4 * c4 + 1] = fmaf(-l[t], col.y, a[4 * c4 + 1]);
+      if (4 * c4 + 2 > t) a[4 * c4 + 2] = fmaf(-l[t], col.z, a[4 * c4 + 2]);
+      if (4 * c4 + 3 > t) a[4 * c4 + 3] = fmaf(-l[t], col.w, a[4 * c4 + 3]);
     }
   }
 }
@@ -347,14 +361,31 @@ __device__ __forceinline__ void sys_of(const SolveParams& p, int64_t sl, int64_t
   }
 }
 
-// Load the 16 entries of row `row` in columns 16cb..16cb+15 (G[c][row], lower part
-// c <= row only; coalesced across the warp's consecutive rows).
+// Load the 16 entries of row `row` in columns 16cb..16cb+15 (lower part c <= row
+// only, G[row][c]): four 16-byte loads when k % 4 == 0, scalar otherwise.
 __device__ __forceinline__ void load_cols(const float* __restrict__ Gq, int k, int row, bool ok, int cb,
                                           float (&v)[16]) {
+  const int c0 = 16 * cb;
+  if (ok && (k & 3) == 0) {
+    const float4* src = reinterpret_cast<const float4*>(Gq + (size_t)row * k + c0);
 #pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const int c = 16 * cb + t;
-    v[t] = (ok && c <= row && c < k) ? __ldg(Gq + (size_t)c * k + row) : 0.f;
+    for (int c4 = 0; c4 < 4; ++c4) {
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c0 + 4 * c4 <= row && c0 + 4 * c4 < k) x = __ldg(src + c4);
+      v[4 * c4] = x.x;
+      v[4 * c4 + 1] = x.y;
+      v[4 * c4 + 2] = x.z;
+      v[4 * c4 + 3] = x.w;
+    }
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (c0 + t > row) v[t] = 0.f;
+  } else {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int c = c0 + t;
+      v[t] = (ok && c <= row && c < k) ? __ldg(Gq + (size_t)row * k + c) : 0.f;
+    }
   }
 }
 
@@ -366,32 +397,33 @@ __device__ __forceinline__ void load_cols(const float* __restrict__ Gq, int k, i
 template <int MASK_MODE, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLayout Ly) {
   extern __shared__ __align__(1024) float smem[];
-  const int k = p.k, K16 = Ly.K16, s = Ly.s, P = Ly.P;
+  const int k = p.k, K16 = Ly.K16, P = Ly.P;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NM = Ly.nmain;
   float* opnd_hi = smem + Ly.off_hi;
   float* opnd_lo = smem + Ly.off_lo;
-  float* tri = smem + Ly.off_tri;
-  float* Lp = smem + Ly.off_lp;
   float* LT = smem + Ly.off_lt;  // current diagonal block, transposed: LT[t][c] = L[c][t]
   float* inv = LT + 256;         // 1/L_tt of the current block
   float* zb = smem + Ly.off_zb;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + Ly.off_misc);
-  // mbar[0] LA, [1] REST, [2..3] lfull (back-sub L blocks), [4..5] fact (slot), [6..7] bsub (slot)
+  // mbar[0] LA, [1] REST, [2..3] lfull (back-sub L blocks), [4..5] fact (slot), [6..7] bsub (slot),
+  // [8] opsready (operands of the panel stored, one arrival per main warp), [9] ysync
   uint64_t* lfull = mbar + 2;
   uint64_t* fact = mbar + 4;
   uint64_t* bsub = mbar + 6;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 16);
-  unsigned* sc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 20);
+  uint64_t* opsready = mbar + 8;
+  uint64_t* ysync = mbar + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 20);
+  unsigned* sc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 24);
   // sc[0] dmax bits, sc[1] pivmin bits, sc[2] bad, sc[3] ev_max bits (current system)
-  unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 32);  // [slot][4]
+  unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 40);  // [slot][4]
   float* Lscr = p.tc_scratch + (size_t)blockIdx.x * 2 * Ly.lb;
 
   // ---- one-time setup ----
   for (int e = tid; e < 2 * Ly.Rop * 16; e += Ly.threads) smem[Ly.off_hi + e] = 0.f;
   if (tid == 0) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) mbar_init(&mbar[e], 1);
+    for (int e = 0; e < 10; ++e) mbar_init(&mbar[e], e == 8 ? (uint32_t)(Ly.nmain / 32) : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, (uint32_t)Ly.tmem_cols);
@@ -416,7 +448,7 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
       mbar_wait(&fact[slot], (n >> 1) & 1);
       unsigned* ssc = slotsc + 4 * slot;
       if (ssc[3] == 0u) {
-        const float* L11 = smem + Ly.off_l11 + slot * P * 136;
+        const float* L11 = smem + Ly.off_l11 + slot * P * 152;
         const float* yv = smem + Ly.off_yv + slot * K16;
         const float* Lsl = Lscr + (size_t)slot * Ly.lb;
         // blocks b = P-2 .. 0 carry L rows below them; prefetch the first one
@@ -430,7 +462,7 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
         if (P >= 2) issue_blk(P - 2, lb_use);
         for (int b = P - 1; b >= 0; --b) {
           // lanes 0..15: column u = lane of W_b = L_bb^{-1} (independent of x)
-          const float* Lbb = L11 + b * 136;
+          const float* Lbb = L11 + b * 152;
           float w[16];
           {
             const int u = lane & 15;
@@ -439,7 +471,7 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
               float acc = (t == u) ? 1.f : 0.f;
 #pragma unroll
               for (int v = 0; v < t; ++v) acc = fmaf(-Lbb[t * (t + 1) / 2 + v], w[v], acc);
-              w[t] = (t >= u) ? acc / Lbb[t * (t + 1) / 2 + t] : 0.f;
+              w[t] = (t >= u) ? acc * Lbb[136 + t] : 0.f;
             }
           }
           // s_t = sum_{c >= 16b+16} L[c][16b+t] x_c   (lane: rows rho = lane>>2 + 8m, cols 4(lane&3)..)
@@ -506,13 +538,73 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
     return;
   }
 
+  // ======================= MMA-issue warp =======================
+  // Per panel: wait until every main warp has stored its L21 operands, release the
+  // panel's y to the main warps (ysync), then issue the tensor-core trailing update
+  // of every group: lookahead (next panel's 16 columns, committed to LA) first,
+  // then the rest (REST).
+  if (warp == Ly.mwarp) {
+    if (lane == 0) {
+      const uint32_t hib = su32(opnd_hi), lob = su32(opnd_lo);
+      auto mma3 = [&](int glo_, int gbase_, int c0, int N) {
+        const uint32_t arow = (uint32_t)(glo_ >> 3) * 512u;
+        const uint32_t brow = (uint32_t)(c0 >> 3) * 512u;
+        const uint32_t id = idesc_tf32(N);
+        const uint32_t dcol = tbase + (uint32_t)(gbase_ + c0 - 16);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t ko = (uint32_t)ks * 256u;
+          const uint64_t ah = sdesc(hib + arow + ko), al = sdesc(lob + arow + ko);
+          const uint64_t bh = sdesc(hib + brow + ko), bl = sdesc(lob + brow + ko);
+          mma_tf32(dcol, ah, bh, id);
+          mma_tf32(dcol, ah, bl, id);
+          mma_tf32(dcol, al, bh, id);
+        }
+      };
+      uint32_t gm = 0;
+      for (int64_t sl = blockIdx.x; sl < p.nsys; sl += gridDim.x) {
+        for (int pp = 0; pp < P; ++pp, ++gm) {
+          mbar_wait(opsready, gm & 1);
+          mbar_arrive(ysync);
+          tc_fence_after();
+          const int r0 = 16 * pp + 16;
+#pragma unroll
+          for (int gg = 0; gg < kMaxGroups; ++gg)
+            if (gg < Ly.G && Ly.hi[gg] > r0) mma3(Ly.lo[gg], Ly.base[gg], r0, 16);
+          mma_commit(&mbar[0]);
+#pragma unroll
+          for (int gg = 0; gg < kMaxGroups; ++gg) {
+            if (gg >= Ly.G) continue;
+            int c0 = r0 + 16;
+            while (c0 < Ly.hi[gg]) {
+              const int N = min(256, Ly.hi[gg] - c0);
+              mma3(Ly.lo[gg], Ly.base[gg], c0, N);
+              c0 += N;
+            }
+          }
+          mma_commit(&mbar[1]);
+        }
+      }
+    }
+    return;
+  }
+
   // ======================= main warps =======================
-  const bool tileA = warp < 4;
-  const int row = tileA ? s + 32 * warp + lane : 32 * (warp - 4) + lane;
-  const bool row_valid = tileA ? row < K16 : row < s;
-  const bool is_aug = !tileA && row == s;  // augmented right-hand-side "row"
-  const uint32_t trow = tbase + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quarter
-  const int tri_row = row * (row + 1) / 2;
+  // warp w -> group g = w/4, TMEM lane quarter m = w%4, row lo[g] + 32m + lane
+  const int grp = warp >> 2, quarter = warp & 3;
+  const bool has_grp = grp < Ly.G;
+  int glo = 0, ghi = 0, gbase = 0;  // static indexing only (no local-memory copy of Ly)
+#pragma unroll
+  for (int gg = 0; gg < kMaxGroups; ++gg)
+    if (gg == grp && has_grp) {
+      glo = Ly.lo[gg];
+      ghi = Ly.hi[gg];
+      gbase = Ly.base[gg];
+    }
+  const int row = glo + 32 * quarter + lane;
+  const bool row_valid = has_grp && row < ghi;
+  const bool is_aug = tid == Ly.aug_tid;  // augmented right-hand-side "row"
+  const uint32_t tq = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)gbase - 16u;  // + column c
 
   uint32_t g = 0;  // global panel counter (LA / REST mbarrier phases)
   bool any_mma = false;
@@ -525,7 +617,7 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
     sys_of(p, sl, q, i);
     const bool tr_on = blockIdx.x == (unsigned)p.trace_block && n == 1;
     TC_TRACE(tid == 0, 0);
-    float* L11all = smem + Ly.off_l11 + slot * P * 136;
+    float* L11all = smem + Ly.off_l11 + slot * P * 152;
     float* yv = smem + Ly.off_yv + slot * K16;
     float* Lslot = Lscr + (size_t)slot * Ly.lb;
 
@@ -552,9 +644,9 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
     }
 
     // ---- staging: row r of (G + lambda*diag(m_i) + ridge*I), identity padding ----
-    // G is read as columns (G[c][r]); the lower triangle used here is G's upper
-    // triangle, as in the packed-column SIMT solver.  Two 16-column groups of
-    // loads in flight per thread.
+    // Row r of G's lower triangle (G[r][c], c <= r; G is symmetric by construction,
+    // G = A A^T).  Columns 0..15 stay in registers (panel 0), the rest go to the
+    // group's TMEM region.
     TC_TRACE(tid == 0, 398);
     float rhs = 0.f, dmax = 0.f, dadd = 0.f;
     const bool ld_ok = row_valid && row < k && !skip;
@@ -569,33 +661,35 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
       tc_fence_after();
     }
     TC_TRACE(tid == 0, 399);
+    float a0[16];
     {
-      const int ncb = tileA ? P : ((row_valid ? row : 0) >> 4) + 1;  // top-left: only c <= row
-      float cur[16], nxt[16];
-      load_cols(Gq, k, row, ld_ok, 0, cur);
-      for (int cb = 0; cb < P; ++cb) {
-        if (cb + 1 < P) load_cols(Gq, k, row, ld_ok && cb + 1 < ncb, cb + 1, nxt);
-        if (row_valid && (row >> 4) == cb) {  // diagonal entry
-          const int t = row & 15;
+      const int ncb = ghi >> 4;        // column chunks of this group (warp-uniform)
+      const int dcb = row >> 4, dt = row & 15;  // chunk / slot of the diagonal entry
+      float b0[16];
+      for (int cb = 1; cb < ncb; ++cb) {
+        load_cols(Gq, k, row, ld_ok, cb, b0);
+        if (row_valid && dcb == cb) {
 #pragma unroll
           for (int u = 0; u < 16; ++u)
-            if (u == t) {
-              cur[u] = row < k ? cur[u] + dadd : 1.f;
-              dmax = row < k ? fabsf(cur[u]) : 0.f;
+            if (u == dt) {
+              b0[u] = row < k ? b0[u] + dadd : 1.f;
+              dmax = row < k ? fabsf(b0[u]) : 0.f;
             }
         }
-        if (tileA) {
-          tmem_st16(trow + (uint32_t)(16 * cb), cur);
-        } else if (row_valid && cb < ncb) {
+        tmem_st16(tq + (uint32_t)(16 * cb), b0);
+        tmem_st_wait();
+      }
+      load_cols(Gq, k, row, ld_ok, 0, a0);
+      if (row_valid && dcb == 0) {
 #pragma unroll
-          for (int t = 0; t < 16; ++t)
-            if (16 * cb + t <= row) tri[tri_row + 16 * cb + t] = cur[t];
-        }
-#pragma unroll
-        for (int t = 0; t < 16; ++t) cur[t] = nxt[t];
+        for (int u = 0; u < 16; ++u)
+          if (u == dt) {
+            a0[u] = row < k ? a0[u] + dadd : 1.f;
+            dmax = row < k ? fabsf(a0[u]) : 0.f;
+          }
       }
     }
-    if (tileA) tmem_st_wait();
+    if (has_grp) tmem_st_wait();
     {
       float m = dmax;
 #pragma unroll
@@ -618,43 +712,59 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
       const int j = 16 * pp;
       const bool active = row_valid && row >= j;
       // a. lagged rhs update, panel entries
-      if (pp > 0 && active) {
+      if (pp > 0) {  // y of the previous panel (written by the rhs thread) is released by ysync
+        mbar_wait(ysync, (g - 1) & 1);
+        if (active) {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) rhs = fmaf(-lprev[t], yv[j - 16 + t], rhs);
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const float4 y4 = *reinterpret_cast<const float4*>(yv + j - 16 + 4 * c4);
+            rhs = fmaf(-lprev[4 * c4], y4.x, rhs);
+            rhs = fmaf(-lprev[4 * c4 + 1], y4.y, rhs);
+            rhs = fmaf(-lprev[4 * c4 + 2], y4.z, rhs);
+            rhs = fmaf(-lprev[4 * c4 + 3], y4.w, rhs);
+          }
+        }
       }
       float a[16];
-      if (tileA) {
-        if (pp > 0) {  // panel columns updated by the previous lookahead MMA
-          mbar_wait(&mbar[0], (g - 1) & 1);
-          tc_fence_after();
-        }
-        tmem_ld16(trow + (uint32_t)j, a);
-        TC_TRACE(tid == 0, 2 + 4 * pp);
+      if (pp == 0) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) a[t] = a0[t];
+      } else if (has_grp && ghi > j) {  // panel columns updated by the previous lookahead MMA
+        mbar_wait(&mbar[0], (g - 1) & 1);
+        tc_fence_after();
+        tmem_ld16(tq + (uint32_t)j, a);
       } else {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) a[t] = (active && j + t <= row) ? tri[tri_row + j + t] : 0.f;
+        for (int t = 0; t < 16; ++t) a[t] = 0.f;
       }
-      // b. diagonal block
+      TC_TRACE(tid == 0, 2 + 4 * pp);
+      // b. diagonal block (rows j..j+15 live in one warp)
       const bool in_diag = active && row < j + 16;
-      const int dwarp = j >= s ? (j - s) >> 5 : 4 + (j >> 5);
-      if (warp == dwarp) {
-        float d[16];
+      int dwarp = 0;
 #pragma unroll
-        for (int t = 0; t < 16; ++t) d[t] = a[t];
+      for (int gg = 0; gg < kMaxGroups; ++gg)
+        if (gg < Ly.G && j >= Ly.lo[gg] && j < Ly.hi[gg]) dwarp = 4 * gg + ((j - Ly.lo[gg]) >> 5);
+      if (warp == dwarp) {
         float iv = 0.f;
-        diag_factor(d, iv, lane & 15, in_diag && row < k, pivmin, bad);
+        diag_factor(a, iv, lane & 15, in_diag && row < k, pivmin, bad);
         if (in_diag) {
           const int gr = row - j;
-          float* Lpk = L11all + pp * 136 + gr * (gr + 1) / 2;  // packed copy for the back-sub warp
+          float* Lpk = L11all + pp * 152 + gr * (gr + 1) / 2;  // packed copy for the back-sub warp
+          L11all[pp * 152 + 136 + gr] = iv;
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            LT[t * 16 + gr] = (t <= gr) ? d[t] : 0.f;  // transposed, for the TRSM
-            if (t <= gr) Lpk[t] = d[t];
+            LT[t * 16 + gr] = (t <= gr) ? a[t] : 0.f;  // transposed, for the TRSM
+            if (t <= gr) Lpk[t] = a[t];
           }
           inv[gr] = iv;
           zb[gr] = rhs;
+        }
+        // the other half-warp's rows were clobbered by the factorization: reload
+        if (pp == 0) {
 #pragma unroll
-          for (int t = 0; t < 16; ++t) a[t] = d[t];
+          for (int t = 0; t < 16; ++t) a[t] = a0[t];
+        } else {
+          tmem_ld16(tq + (uint32_t)j, a);
         }
         TC_TRACE(row == j, 3 + 4 * pp);
       }
@@ -671,17 +781,8 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
         trsm_row(LT, inv, z, l);
 #pragma unroll
         for (int t = 0; t < 16; ++t) yv[j + t] = l[t];
-      } else {
-#pragma unroll
-        for (int t = 0; t < 16; ++t) l[t] = in_diag ? a[t] : 0.f;
       }
-      // d. store L: scratch (back substitution), smem tri (top-left rows),
-      //    operand hi/lo (rows >= j+16)
-      if (!tileA && active && !is_aug) {
-#pragma unroll
-        for (int t = 0; t < 16; ++t)
-          if (j + t <= row) tri[tri_row + j + t] = l[t];
-      }
+      // d. store L21: scratch (back substitution), operand hi/lo
       if (trsm) {
         float4* dst = reinterpret_cast<float4*>(Lslot + lb_off(pp, K16) + (size_t)(row - j - 16) * 16);
 #pragma unroll
@@ -698,69 +799,12 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
           *reinterpret_cast<float4*>(h + c4 * 32) = make_float4(hv[0], hv[1], hv[2], hv[3]);
           *reinterpret_cast<float4*>(lo + c4 * 32) = make_float4(lv[0], lv[1], lv[2], lv[3]);
         }
-        if (!tileA) {
-#pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4)
-            *reinterpret_cast<float4*>(Lp + row * 16 + 4 * c4) =
-                make_float4(l[4 * c4], l[4 * c4 + 1], l[4 * c4 + 2], l[4 * c4 + 3]);
-        }
       }
       TC_TRACE(tid == 0, 4 + 4 * pp);
       fence_async_smem();
-      tc_fence_before();
-      main_sync(NM);
-      tc_fence_after();
-      // e. tensor-core trailing update: lookahead (next panel) then the rest
-      if (tid == 0) {
-        const int r0 = j + 16;
-        const uint32_t hib = su32(opnd_hi), lob = su32(opnd_lo);
-        const uint32_t arow = (uint32_t)(s >> 3) * 512u;
-        if (r0 < K16) {
-          int c0 = r0;
-          int N = 16;
-          bool first = true;
-          while (c0 < K16) {
-            const uint32_t id = idesc_tf32(N);
-            const uint32_t brow = (uint32_t)(c0 >> 3) * 512u;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              const uint32_t ko = (uint32_t)ks * 256u;
-              const uint64_t ah = sdesc(hib + arow + ko), al = sdesc(lob + arow + ko);
-              const uint64_t bh = sdesc(hib + brow + ko), bl = sdesc(lob + brow + ko);
-              mma_tf32(tbase + (uint32_t)c0, ah, bh, id);
-              mma_tf32(tbase + (uint32_t)c0, ah, bl, id);
-              mma_tf32(tbase + (uint32_t)c0, al, bh, id);
-            }
-            if (first) mma_commit(&mbar[0]);
-            first = false;
-            c0 += N;
-            N = min(256, K16 - c0);
-          }
-          mma_commit(&mbar[1]);
-        } else {
-          mma_commit(&mbar[0]);
-          mma_commit(&mbar[1]);
-        }
-        TC_TRACE(true, 5 + 4 * pp);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(opsready);  // operands of this panel stored
       any_mma = true;
-      // top-left SIMT trailing update (rows j+16..s-1, columns j+16..row)
-      if (!tileA && trsm) {
-        for (int c = j + 16; c <= row; ++c) {
-          const float* lc = Lp + c * 16;
-          float acc = 0.f;
-#pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            const float4 v = *reinterpret_cast<const float4*>(lc + 4 * c4);
-            acc = fmaf(l[4 * c4], v.x, acc);
-            acc = fmaf(l[4 * c4 + 1], v.y, acc);
-            acc = fmaf(l[4 * c4 + 2], v.z, acc);
-            acc = fmaf(l[4 * c4 + 3], v.w, acc);
-          }
-          tri[tri_row + c] -= acc;
-        }
-        TC_TRACE(row == s - 1, 300 + pp);
-      }
 #pragma unroll
       for (int t = 0; t < 16; ++t) lprev[t] = trsm ? l[t] : 0.f;
     }
@@ -814,7 +858,7 @@ size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms) {
 bool tc_supported(int k, int optin_smem) {
   if (k < 1) return false;
   const TcLayout L = make_layout(k);
-  if (L.tmem_cols > 512 || L.threads > 352) return false;
+  if (L.tmem_cols > 512 || L.cps < 1 || L.threads > 384) return false;
   return (size_t)L.floats * 4 <= (size_t)optin_smem;
 }
 
@@ -827,7 +871,7 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const TcLayout L = make_layout(p.k);
-  if (L.tmem_cols > 512 || L.threads > 352 || !p.tc_scratch) return cudaErrorNotSupported;
+  if (L.tmem_cols > 512 || L.cps < 1 || L.threads > 384 || !p.tc_scratch) return cudaErrorNotSupported;
   // cap residency at L.cps CTAs per SM through the shared-memory request, so no
   // CTA ever waits on a TMEM allocation
   size_t smem = (size_t)L.floats * 4;
@@ -838,20 +882,19 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
     smem = (size_t)optin;
   }
   void (*fn)(SolveParams, TcLayout) = nullptr;
-  if (L.cps >= 2) {  // <= 320 threads, two CTAs per SM
+  if (L.cps >= 2 && L.threads <= 288) {  // two CTAs per SM
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 320, 2>; break;
-      case 1: fn = chol_tc_kernel<1, 320, 2>; break;
-      default: fn = chol_tc_kernel<2, 320, 2>; break;
+      case 0: fn = chol_tc_kernel<0, 288, 2>; break;
+      case 1: fn = chol_tc_kernel<1, 288, 2>; break;
+      default: fn = chol_tc_kernel<2, 288, 2>; break;
     }
   } else {
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 352, 1>; break;
-      case 1: fn = chol_tc_kernel<1, 352, 1>; break;
-      default: fn = chol_tc_kernel<2, 352, 1>; break;
+      case 0: fn = chol_tc_kernel<0, 384, 1>; break;
+      case 1: fn = chol_tc_kernel<1, 384, 1>; break;
+      default: fn = chol_tc_kernel<2, 384, 1>; break;
     }
   }
-  if (L.cps >= 2 && L.threads > 320) return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t maxgrid = (int64_t)sms * L.cps;

@@ -17,7 +17,9 @@ print(" p   load  diag  trsm  issue | total  (syrkTL end)")
 while t[2 + 4 * p]:
     a, d, r, m = (t[2 + 4 * p + e] for e in range(4))
     tl = t[300 + p]
-    print(f"{p:2d} {a - prev:6d} {d - a:5d} {r - d:5d} {m - r:5d} | {m - prev:6d}  {tl - m if tl else ''}")
+    bf, la = t[601 + 2 * p], t[600 + 2 * p]
+    extra = f"  [barrier-f {bf - r}, LA issue {la - bf}, REST issue {m - la}]" if bf and la else ""
+    print(f"{p:2d} {a - prev:6d} {d - a:5d} {r - d:5d} {m - r:5d} | {m - prev:6d}{extra}")
     prev = m
     p += 1
 print("panels end", rel(t[200]), " inv", t[201] - t[200], " backsub", t[202] - t[201], " out", t[203] - t[202],
