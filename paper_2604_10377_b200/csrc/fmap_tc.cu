@@ -361,31 +361,16 @@ __device__ __forceinline__ void sys_of(const SolveParams& p, int64_t sl, int64_t
   }
 }
 
-// Load the 16 entries of row `row` in columns 16cb..16cb+15 (lower part c <= row
-// only, G[row][c]): four 16-byte loads when k % 4 == 0, scalar otherwise.
+// Load the 16 entries of row `row` in columns 16cb..16cb+15 as G[c][row] (G is
+// symmetric; coalesced across the warp's consecutive rows: one 128-byte line per
+// load instruction).  Lower part c <= row only.
 __device__ __forceinline__ void load_cols(const float* __restrict__ Gq, int k, int row, bool ok, int cb,
                                           float (&v)[16]) {
   const int c0 = 16 * cb;
-  if (ok && (k & 3) == 0) {
-    const float4* src = reinterpret_cast<const float4*>(Gq + (size_t)row * k + c0);
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (c0 + 4 * c4 <= row && c0 + 4 * c4 < k) x = __ldg(src + c4);
-      v[4 * c4] = x.x;
-      v[4 * c4 + 1] = x.y;
-      v[4 * c4 + 2] = x.z;
-      v[4 * c4 + 3] = x.w;
-    }
-#pragma unroll
-    for (int t = 0; t < 16; ++t)
-      if (c0 + t > row) v[t] = 0.f;
-  } else {
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int c = c0 + t;
-      v[t] = (ok && c <= row && c < k) ? __ldg(Gq + (size_t)row * k + c) : 0.f;
-    }
+  for (int t = 0; t < 16; ++t) {
+    const int c = c0 + t;
+    v[t] = (ok && c <= row && c < k) ? __ldg(Gq + (size_t)c * k + row) : 0.f;
   }
 }
 
@@ -644,9 +629,10 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
     }
 
     // ---- staging: row r of (G + lambda*diag(m_i) + ridge*I), identity padding ----
-    // Row r of G's lower triangle (G[r][c], c <= r; G is symmetric by construction,
-    // G = A A^T).  Columns 0..15 stay in registers (panel 0), the rest go to the
-    // group's TMEM region.
+    // Row r of G (read as column r, G[c][r]: coalesced; the lower triangle used is
+    // G's upper triangle, as the SIMT solver; G = A A^T is symmetric by
+    // construction).  Columns 0..15 stay in registers (panel 0), the rest go to the
+    // group's TMEM region, two chunks of loads in flight.
     TC_TRACE(tid == 0, 398);
     float rhs = 0.f, dmax = 0.f, dadd = 0.f;
     const bool ld_ok = row_valid && row < k && !skip;
@@ -665,19 +651,26 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
     {
       const int ncb = ghi >> 4;        // column chunks of this group (warp-uniform)
       const int dcb = row >> 4, dt = row & 15;  // chunk / slot of the diagonal entry
-      float b0[16];
-      for (int cb = 1; cb < ncb; ++cb) {
-        load_cols(Gq, k, row, ld_ok, cb, b0);
+      auto fix_diag = [&](float (&v)[16], int cb) {
         if (row_valid && dcb == cb) {
 #pragma unroll
           for (int u = 0; u < 16; ++u)
             if (u == dt) {
-              b0[u] = row < k ? b0[u] + dadd : 1.f;
-              dmax = row < k ? fabsf(b0[u]) : 0.f;
+              v[u] = row < k ? v[u] + dadd : 1.f;
+              dmax = row < k ? fabsf(v[u]) : 0.f;
             }
         }
+      };
+      for (int cb = 1; cb < ncb; cb += 2) {  // two chunks of loads in flight
+        float b0[16], b1[16];
+        load_cols(Gq, k, row, ld_ok, cb, b0);
+        if (cb + 1 < ncb) load_cols(Gq, k, row, ld_ok, cb + 1, b1);
+        fix_diag(b0, cb);
         tmem_st16(tq + (uint32_t)(16 * cb), b0);
-        tmem_st_wait();
+        if (cb + 1 < ncb) {
+          fix_diag(b1, cb + 1);
+          tmem_st16(tq + (uint32_t)(16 * (cb + 1)), b1);
+        }
       }
       load_cols(Gq, k, row, ld_ok, 0, a0);
       if (row_valid && dcb == 0) {
