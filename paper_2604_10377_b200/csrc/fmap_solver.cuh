@@ -77,6 +77,8 @@ __host__ __device__ __forceinline__ size_t solver_smem_bytes(int k) {
 // Tensor-core (tcgen05 / TMEM) solver, fmap_tc.cu.
 bool tc_supported(int k, int optin_smem);
 size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms);
+cudaError_t launch_project_tc(const float* phi, const float* mass, const float* F, int64_t b,
+                              int64_t n, int k, int d, float* out, cudaStream_t st);
 cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream);
 
 }  // namespace fmap

@@ -217,8 +217,8 @@ __device__ __forceinline__ uint32_t idesc_tf32(int N) {
          ((uint32_t)(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t idesc) {
-  const uint32_t acc = 1u;
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc = 1u) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(dtmem),
@@ -893,6 +893,178 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   const int64_t maxgrid = (int64_t)sms * L.cps;
   const unsigned grid = (unsigned)(p.nsys < maxgrid ? p.nsys : maxgrid);
   fn<<<grid, L.threads, smem, stream>>>(p, L);
+  return cudaGetLastError();
+}
+
+// ===========================================================================
+// Spectral projection on the tensor core (north_star stage 1):
+//   Out[q] (k x d) = Phi_q^T (k x n) * diag(Mass_q) * F_q (n x d)
+// as a 3xTF32 tcgen05 GEMM, M = 128 basis functions per CTA, N = d (<= 256),
+// K = vertices in 16-vertex stages.  Eight producer warps load Phi and F with
+// coalesced column loads (lane = basis function / feature channel), apply the
+// Mass scaling, split hi/lo and store the tiles K-major (core matrices, the same
+// layout as the solver's operands); one MMA-issue warp runs 6 MMAs per stage
+// (2 k-steps x {hi*hi, hi*lo, lo*hi}); two stages in flight (mbarriers).  The
+// accumulator lives in TMEM; the epilogue writes Out rows coalesced per lane.
+// Bound: HBM (4(nk + n + nd) bytes per shape) and the tensor pipe.
+// ===========================================================================
+namespace {
+constexpr int kPjK = 16;      // vertices per stage
+constexpr int kPjThreads = 288;  // 8 producer warps + 1 MMA warp
+
+__device__ __forceinline__ float tf32_hi(float x) {  // round-to-nearest TF32
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  return __uint_as_float(h);
+}
+
+__global__ void __launch_bounds__(kPjThreads, 2) proj_tc_kernel(const float* __restrict__ phi,
+                                                                  const float* __restrict__ mass,
+                                                                  const float* __restrict__ F,
+                                                                  int64_t n, int k, int d, int N,
+                                                                  float* __restrict__ out) {
+  extern __shared__ __align__(1024) float smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = blockIdx.y, i0 = blockIdx.x * 128;
+  const float* Pq = phi + (size_t)q * n * k;
+  const float* Fq = F + (size_t)q * n * d;
+  const float* Mq = mass + (size_t)q * n;
+  // per stage buffer: A_hi | A_lo (128 x 16) | B_hi | B_lo (N x 16)
+  const int abytes = 128 * kPjK, bbytes = N * kPjK;  // floats
+  const int sstride = 2 * abytes + 2 * bbytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sstride);  // full[2], empty[2], done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
+  if (tid == 0) {
+    mbar_init(&bar[0], 8);
+    mbar_init(&bar[1], 8);
+    mbar_init(&bar[2], 1);
+    mbar_init(&bar[3], 1);
+    mbar_init(&bar[4], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const int nst = (int)((n + kPjK - 1) / kPjK);
+
+  if (warp == 8) {  // ---- MMA issue ----
+    if (lane == 0) {
+      const uint32_t id = idesc_tf32(N) & ~(1u << 13);  // D += A*B (no negation)
+      for (int st = 0; st < nst; ++st) {
+        const int buf = st & 1;
+        mbar_wait(&bar[buf], (st >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ah = su32(smem + buf * sstride), al = ah + abytes * 4;
+        const uint32_t bh = al + abytes * 4, bl = bh + bbytes * 4;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t ko = (uint32_t)ks * 256u;
+          mma_tf32(tbase, sdesc(ah + ko), sdesc(bh + ko), id, (st > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32(tbase, sdesc(ah + ko), sdesc(bl + ko), id, 1u);
+          mma_tf32(tbase, sdesc(al + ko), sdesc(bh + ko), id, 1u);
+        }
+        mma_commit(&bar[2 + buf]);
+      }
+      mma_commit(&bar[4]);
+    }
+  } else {  // ---- producers (256 threads) ----
+    for (int st = 0; st < nst; ++st) {
+      const int buf = st & 1;
+      const int64_t v0 = (int64_t)st * kPjK;
+      // loads first (latency overlaps the wait for the buffer)
+      float av[2][4], bv[4][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tid + 256 * h, i = c & 127, kc = c >> 7;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t v = v0 + 4 * kc + u;
+          av[h][u] = (v < n && i0 + i < k) ? __ldg(Pq + v * k + i0 + i) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int c = tid + 256 * h;
+        const int t = c % N, kc = c / N;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t v = v0 + 4 * kc + u;
+          bv[h][u] = (kc < 4 && v < n && t < d) ? __ldg(Mq + v) * __ldg(Fq + v * d + t) : 0.f;
+        }
+      }
+      if (st >= 2) mbar_wait(&bar[2 + buf], ((st - 2) >> 1) & 1);  // MMAs of stage st-2 done
+      float* S = smem + buf * sstride;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tid + 256 * h, i = c & 127, kc = c >> 7;
+        const int o = (i >> 3) * 128 + kc * 32 + (i & 7) * 4;
+        float hv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) hv[u] = tf32_hi(av[h][u]);
+        *reinterpret_cast<float4*>(S + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<float4*>(S + abytes + o) =
+            make_float4(av[h][0] - hv[0], av[h][1] - hv[1], av[h][2] - hv[2], av[h][3] - hv[3]);
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int c = tid + 256 * h;
+        const int t = c % N, kc = c / N;
+        if (kc < 4) {
+          const int o = (t >> 3) * 128 + kc * 32 + (t & 7) * 4;
+          float hv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) hv[u] = tf32_hi(bv[h][u]);
+          *reinterpret_cast<float4*>(S + 2 * abytes + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<float4*>(S + 2 * abytes + bbytes + o) =
+              make_float4(bv[h][0] - hv[0], bv[h][1] - hv[1], bv[h][2] - hv[2], bv[h][3] - hv[3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar[buf]);
+    }
+    // ---- epilogue: TMEM -> Out (warp w: lane quarter w % 4, column half w / 4) ----
+    mbar_wait(&bar[4], 0);
+    tc_fence_after();
+    const int quarter = warp & 3, half = warp >> 2;
+    const int i = i0 + 32 * quarter + lane;
+    const int nh = N / 2;
+    for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)c0, v);
+      if (i < k) {
+        float* o = out + ((size_t)q * k + i) * d + c0;
+        if (c0 + 16 <= d && (d & 3) == 0) {
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4)
+            *reinterpret_cast<float4*>(o + 4 * c4) = make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (c0 + t < d) o[t] = v[t];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+}  // namespace
+
+// Tensor-core projection (d <= 256); returns cudaErrorNotSupported otherwise.
+cudaError_t launch_project_tc(const float* phi, const float* mass, const float* F, int64_t b,
+                              int64_t n, int k, int d, float* out, cudaStream_t st) {
+  if (d > 256 || d < 1 || k < 1 || n < 1 || b < 1) return cudaErrorNotSupported;
+  const int N = (d + 15) & ~15;
+  const size_t smem = (size_t)(2 * (2 * 128 * kPjK + 2 * N * kPjK)) * 4 + 64;
+  const size_t req = smem < 233472 / 3 + 1 ? 233472 / 3 + 1 : smem;  // <= 2 CTAs per SM (TMEM 256 cols)
+  cudaError_t e = cudaFuncSetAttribute(proj_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)req);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((k + 127) / 128), (unsigned)b);
+  proj_tc_kernel<<<grid, kPjThreads, req, st>>>(phi, mass, F, n, k, d, N, out);
   return cudaGetLastError();
 }
 
