@@ -154,48 +154,106 @@ __global__ void __launch_bounds__(256) gemm_nt_kernel(const float* __restrict__ 
 // ("TN" GEMM over the vertex dimension), FP32 SIMT, deterministic (no split-K
 // atomics): one CTA per (64 x 64) output tile.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ phi,
-                                                      const float* __restrict__ mass,
-                                                      const float* __restrict__ F, int64_t n,
-                                                      int k, int d, float* __restrict__ out) {
-  __shared__ __align__(16) float ps[GK][GT + 4];
-  __shared__ __align__(16) float fs[GK][GT + 4];
+constexpr int PJ_T = 128, PJ_K = 16;
+
+// Out[q] = Phi_q^T diag(Mass_q) F_q, FP32 SIMT: 128 (basis) x 128 (feature) CTA tile,
+// 8 x 8 outputs per thread, 16-vertex chunks double-buffered in shared memory with
+// the next chunk prefetched into registers (coalesced 16-byte row loads of Phi and
+// F; the Mass scaling is applied on the way to shared memory).  FMA-bound.
+__global__ void __launch_bounds__(256, 2) project_kernel(const float* __restrict__ phi,
+                                                         const float* __restrict__ mass,
+                                                         const float* __restrict__ F, int64_t n,
+                                                         int k, int d, float* __restrict__ out) {
+  __shared__ __align__(16) float As[2][PJ_K][PJ_T];
+  __shared__ __align__(16) float Bs[2][PJ_K][PJ_T];
   const int q = blockIdx.z;
   const float* Pq = phi + (size_t)q * n * k;
   const float* Fq = F + (size_t)q * n * d;
   const float* Mq = mass + (size_t)q * n;
-  const int i0 = blockIdx.y * GT, t0 = blockIdx.x * GT;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][4] = {};
-  for (int64_t v0 = 0; v0 < n; v0 += GK) {
-    for (int e = threadIdx.x; e < GT * GK; e += 256) {
-      const int vv = e / GT, c = e % GT;  // coalesced along the row of Phi / F
-      const int64_t gv = v0 + vv;
-      const bool inb = gv < n;
-      ps[vv][c] = (inb && i0 + c < k) ? Pq[gv * k + i0 + c] : 0.f;
-      fs[vv][c] = (inb && t0 + c < d) ? Mq[gv] * Fq[gv * d + t0 + c] : 0.f;
+  const int i0 = blockIdx.y * PJ_T, t0 = blockIdx.x * PJ_T;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool avec = (k & 3) == 0, bvec = (d & 3) == 0;
+  // loader mapping: element chunk e = tid + 256h (h = 0, 1): row vv = e >> 5, col c4 = (e & 31) * 4
+  float4 ra[2], rb[2];
+  auto load = [&](int64_t v0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = tid + 256 * h, vv = e >> 5, c = (e & 31) * 4;
+      const int64_t v = v0 + vv;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f), y = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (v < n) {
+        const float* pr = Pq + v * k + i0 + c;
+        if (avec && i0 + c + 3 < k) {
+          x = __ldg(reinterpret_cast<const float4*>(pr));
+        } else {
+          x.x = i0 + c < k ? __ldg(pr) : 0.f;
+          x.y = i0 + c + 1 < k ? __ldg(pr + 1) : 0.f;
+          x.z = i0 + c + 2 < k ? __ldg(pr + 2) : 0.f;
+          x.w = i0 + c + 3 < k ? __ldg(pr + 3) : 0.f;
+        }
+        const float m = __ldg(Mq + v);
+        const float* fr = Fq + v * d + t0 + c;
+        if (bvec && t0 + c + 3 < d) {
+          y = __ldg(reinterpret_cast<const float4*>(fr));
+        } else {
+          y.x = t0 + c < d ? __ldg(fr) : 0.f;
+          y.y = t0 + c + 1 < d ? __ldg(fr + 1) : 0.f;
+          y.z = t0 + c + 2 < d ? __ldg(fr + 2) : 0.f;
+          y.w = t0 + c + 3 < d ? __ldg(fr + 3) : 0.f;
+        }
+        y.x *= m;
+        y.y *= m;
+        y.z *= m;
+        y.w *= m;
+      }
+      ra[h] = x;
+      rb[h] = y;
     }
-    __syncthreads();
+  };
+  auto store = [&](int buf) {
 #pragma unroll
-    for (int vv = 0; vv < GK; ++vv) {
-      const float4 a = *reinterpret_cast<const float4*>(&ps[vv][ty * 4]);
-      const float4 b = *reinterpret_cast<const float4*>(&fs[vv][tx * 4]);
-      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) acc[u][w] = fmaf(av[u], bv[w], acc[u][w]);
+    for (int h = 0; h < 2; ++h) {
+      const int e = tid + 256 * h, vv = e >> 5, c = (e & 31) * 4;
+      *reinterpret_cast<float4*>(&As[buf][vv][c]) = ra[h];
+      *reinterpret_cast<float4*>(&Bs[buf][vv][c]) = rb[h];
     }
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int w = 0; w < 8; ++w) acc[u][w] = 0.f;
+  const int64_t nch = (n + PJ_K - 1) / PJ_K;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const int buf = (int)(ch & 1);
+    if (ch + 1 < nch) load((ch + 1) * PJ_K);  // in flight during the FMAs below
+#pragma unroll
+    for (int vv = 0; vv < PJ_K; ++vv) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][vv][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][vv][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][vv][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][vv][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc[u][w] = fmaf(av[u], bv[w], acc[u][w]);
+    }
+    if (ch + 1 < nch) store(buf ^ 1);
     __syncthreads();
   }
   float* o = out + (size_t)q * k * d;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int gi = i0 + ty * 4 + u;
+  for (int u = 0; u < 8; ++u) {
+    const int gi = i0 + (u < 4 ? ty * 4 + u : 64 + ty * 4 + u - 4);
     if (gi >= k) continue;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int gt = t0 + tx * 4 + w;
+    for (int w = 0; w < 8; ++w) {
+      const int gt = t0 + (w < 4 ? tx * 4 + w : 64 + tx * 4 + w - 4);
       if (gt < d) o[(size_t)gi * d + gt] = acc[u][w];
     }
   }
@@ -308,7 +366,7 @@ cudaError_t launch_project(const float* phi, const float* mass, const float* F, 
     const cudaError_t e = launch_project_tc(phi, mass, F, b, n, k, d, out, st);
     if (e != cudaErrorNotSupported) return e;
   }
-  dim3 grid((d + GT - 1) / GT, (k + GT - 1) / GT, (unsigned)b);
+  dim3 grid((d + PJ_T - 1) / PJ_T, (k + PJ_T - 1) / PJ_T, (unsigned)b);
   project_kernel<<<grid, 256, 0, st>>>(phi, mass, F, n, k, d, out);
   return cudaGetLastError();
 }
