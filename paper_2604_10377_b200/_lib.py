@@ -6,10 +6,13 @@ is present, every compute entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libfmap_cuda.so"
+if os.environ.get("FMAP_LIB_VARIANT"):  # developer A/B: a second in-tree build, libfmap_cuda_<v>.so
+    LIB_PATH = LIB_PATH.with_name(f"libfmap_cuda_{os.environ['FMAP_LIB_VARIANT']}.so")
 
 FMAP_OK = 0
 FMAP_INVALID_ARGUMENT = 1
