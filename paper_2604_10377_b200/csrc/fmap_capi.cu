@@ -36,6 +36,9 @@ struct fmap_ctx {
   int64_t launches = 0;
   int max_smem_optin = 0;
   int num_sms = 0;
+  // host-buffer pipelining (fmap_solve_f32): second compute stream + copy stream
+  cudaStream_t comp2 = nullptr, copy = nullptr;
+  cudaEvent_t cev[20] = {};  // start | done | per chunk: H2D done, solve done (x 8 chunks)
 };
 
 namespace {
@@ -356,6 +359,111 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   return FMAP_OK;
 }
 
+// Host-buffer solve with the copies pipelined against the solver (the headline e2e
+// path): the batch is cut into pair chunks; chunk c+1's H2D and chunk c-1's D2H run
+// on a copy stream while chunk c is validated and solved, and chunks alternate
+// between two compute streams (each with its own L scratch) so that one chunk's
+// tail overlaps the next chunk's start.  Same semantics as solve_core (device
+// validation before any result is exposed, lowest failing index, no partial
+// results on error); used when no fault injection / residual is requested.
+int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const float* rhs,
+                         const float* mask, float lambda, const fmap_solver_options& opts, float* C_out,
+                         fmap_report* rep, int nchunk) {
+  const size_t kk = (size_t)k * k;
+  const size_t bytes = (size_t)b * kk * sizeof(float);
+  const int64_t cb = (b + nchunk - 1) / nchunk;  // pairs per chunk
+  const int64_t csys = cb * k;
+  const size_t tcb = tc_scratch_bytes((int)k, csys, ctx->num_sms);
+  const size_t staging = carve_size({bytes, bytes, bytes, bytes, tcb, tcb});
+  if (rep) rep->peak_extra_bytes = staging;
+  if (opts.has_memory_cap && staging > opts.memory_cap_bytes) {
+    if (rep) {
+      rep->required_bytes = staging;
+      rep->cap_bytes = opts.memory_cap_bytes;
+    }
+    return set_err(ctx, FMAP_MEMORY_CAP,
+                   "cuda route needs " + std::to_string(staging) + " bytes of device staging, above the cap of " +
+                       std::to_string(opts.memory_cap_bytes));
+  }
+  int st = arena_reserve(ctx, staging);
+  if (st) return st;
+  if (!ctx->comp2) FMAP_CK(ctx, cudaStreamCreateWithFlags(&ctx->comp2, cudaStreamNonBlocking));
+  if (!ctx->copy) FMAP_CK(ctx, cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : ctx->cev)
+    if (!e) FMAP_CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  float* dG = cv.take<float>((size_t)b * kk);
+  float* dR = cv.take<float>((size_t)b * kk);
+  float* dM = cv.take<float>((size_t)b * kk);
+  float* dC = cv.take<float>((size_t)b * kk);
+  float* scr[2] = {cv.take<float>(tcb / sizeof(float)), cv.take<float>(tcb / sizeof(float))};
+  if ((st = reset_ctrl(ctx))) return st;
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  FMAP_CK(ctx, cudaEventRecord(ctx->cev[0], ctx->stream));
+  FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->cev[0], 0));
+  FMAP_CK(ctx, cudaStreamWaitEvent(ctx->comp2, ctx->cev[0], 0));
+  cudaStream_t comp[2] = {ctx->stream, ctx->comp2};
+  SolveParams p{};
+  p.k = (int)k;
+  p.K4 = ((int)k + 3) & ~3;
+  p.Rp = p.K4 + 4;
+  p.lambda = lambda;
+  p.ridge = opts.ridge;
+  p.rcond_thr = opts.rcond_threshold < 0.f ? 1e-7f : opts.rcond_threshold;
+  p.rhs_unit = -1;
+  p.fail_min = d_fail(ctx);
+  p.rcond_min_bits = d_rcond(ctx);
+  p.flags = d_flags(ctx);
+  p.gram = dG;
+  p.rhs = dR;
+  p.mask = dM;
+  p.C = dC;
+  ctx->launches = 0;
+  for (int c = 0; c < nchunk; ++c) {
+    const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
+    if (nq <= 0) break;
+    const size_t off = (size_t)q0 * kk, nb = (size_t)nq * kk * sizeof(float);
+    cudaEvent_t h2d = ctx->cev[2 + 2 * c], done = ctx->cev[3 + 2 * c];
+    FMAP_CK(ctx, cudaMemcpyAsync(dG + off, gram + off, nb, cudaMemcpyHostToDevice, ctx->copy));
+    FMAP_CK(ctx, cudaMemcpyAsync(dR + off, rhs + off, nb, cudaMemcpyHostToDevice, ctx->copy));
+    FMAP_CK(ctx, cudaMemcpyAsync(dM + off, mask + off, nb, cudaMemcpyHostToDevice, ctx->copy));
+    FMAP_CK(ctx, cudaEventRecord(h2d, ctx->copy));
+    cudaStream_t s = comp[c & 1];
+    FMAP_CK(ctx, cudaStreamWaitEvent(s, h2d, 0));
+    FMAP_CK(ctx, launch_validate(dG + off, dR + off, dM + off, (size_t)nq * kk, d_flags(ctx), s));
+    p.nsys = nq * k;
+    p.sys_offset = q0 * k;
+    p.tc_scratch = scr[c & 1];
+    FMAP_CK(ctx, launch_chol_solve(p, 0, s));
+    ctx->launches += 2;
+    FMAP_CK(ctx, cudaEventRecord(done, s));
+    FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy, done, 0));
+    FMAP_CK(ctx, cudaMemcpyAsync(C_out + off, dC + off, nb, cudaMemcpyDeviceToHost, ctx->copy));
+  }
+  FMAP_CK(ctx, cudaEventRecord(ctx->cev[1], ctx->copy));
+  FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[1], 0));
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  unsigned long long fail;
+  float rcond;
+  unsigned flags;
+  if ((st = read_ctrl(ctx, &fail, &rcond, &flags))) return st;
+  float ms = 0.f;
+  FMAP_CK(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (rep) {
+    rep->wall_seconds = ms * 1e-3;
+    rep->min_rcond = rcond;
+  }
+  if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, flags_message(flags));
+  if (fail != kNoFail) {
+    if (rep) rep->failing_system = (int64_t)fail;
+    return set_err(ctx, FMAP_SINGULAR,
+                   "row system " + std::to_string(fail) +
+                       " is numerically singular (Cholesky pivot / rcond estimate / non-finite solution)");
+  }
+  ctx->last_error.clear();
+  return FMAP_OK;
+}
+
 bool host_finite(const float* p, size_t n) {
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) return false;
@@ -411,6 +519,10 @@ int fmap_ctx_destroy(fmap_ctx* ctx) {
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->comp2) cudaStreamDestroy(ctx->comp2);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  for (cudaEvent_t& e : ctx->cev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   return FMAP_OK;
 }
@@ -465,6 +577,12 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   fmap_solver_options o;
   default_opts(&o);
   if (opts) o = *opts;
+  // pipelined copies (tensor-core solver, >= 8 pairs, no fault injection / residual)
+  const char* pipe = std::getenv("FMAP_PIPELINE");  // chunks (opt-in; measured slower at cfg2)
+  const int nchunk = pipe ? std::max(1, std::min(8, std::atoi(pipe))) : 1;
+  if (nchunk > 1 && !o.inject_fault && !o.compute_residual && b >= 2 * nchunk && !std::getenv("FMAP_SOLVER") &&
+      k <= max_resolution(ctx) && tc_supported((int)k, ctx->max_smem_optin))
+    return solve_host_pipelined(ctx, b, k, gram, rhs, mask, lambda, o, C_out, report, nchunk);
   if (o.has_memory_cap && staging > o.memory_cap_bytes) {
     if (report) {
       report->required_bytes = staging;

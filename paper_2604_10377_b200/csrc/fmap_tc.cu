@@ -44,6 +44,8 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
+#include <algorithm>
 
 namespace fmap {
 
@@ -350,9 +352,9 @@ __device__ __forceinline__ void trsm_row(const float* __restrict__ LT, const flo
 // same time read different Gram matrices instead of all hammering one.
 __device__ __forceinline__ void sys_of(const SolveParams& p, int64_t sl, int64_t& q, int& i) {
   const int k = p.k;
-  if (p.sys_offset == 0 && p.nsys % k == 0) {
+  if (p.sys_offset % k == 0 && p.nsys % k == 0) {  // whole pairs (a batch or a chunk of one)
     const int64_t b = p.nsys / k;
-    q = sl % b;
+    q = p.sys_offset / k + sl % b;
     i = (int)(sl / b);
   } else {
     const int64_t sys = p.sys_offset + sl;
@@ -863,8 +865,9 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const TcLayout L = make_layout(p.k);
+  TcLayout L = make_layout(p.k);
   if (L.tmem_cols > 512 || L.cps < 1 || L.threads > 384 || !p.tc_scratch) return cudaErrorNotSupported;
+  if (const char* c = std::getenv("FMAP_TC_CPS")) L.cps = std::max(1, std::min(L.cps, std::atoi(c)));  // diagnostics
   // cap residency at L.cps CTAs per SM through the shared-memory request, so no
   // CTA ever waits on a TMEM allocation
   size_t smem = (size_t)L.floats * 4;

@@ -131,9 +131,56 @@ __device__ __forceinline__ void dfD(float (&a)[16], float& inv, int g, float* xb
   }
 }
 
+// (E) 4 pivots per shared-memory round: rows t..t+3 published, every lane solves
+// the 4x4 pivot block locally (applying the earlier pivots of the round to the
+// published rows) and applies the rank-4 update to its own row.
+__device__ __forceinline__ void dfE(float (&a)[16], float& inv, int g, float* xb) {
+#pragma unroll
+  for (int t = 0; t < 16; t += 4) {
+    float* slot = xb + ((t >> 2) & 1) * 64;
+    if (g >= t && g < t + 4) {
+      float* dst = slot + 16 * (g - t);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4)
+        *reinterpret_cast<float4*>(dst + 4 * c4) = make_float4(a[4 * c4], a[4 * c4 + 1], a[4 * c4 + 2], a[4 * c4 + 3]);
+    }
+    __syncwarp();
+    float r[4][16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const float4 v = *reinterpret_cast<const float4*>(slot + 16 * u + 4 * c4);
+        r[u][4 * c4] = v.x; r[u][4 * c4 + 1] = v.y; r[u][4 * c4 + 2] = v.z; r[u][4 * c4 + 3] = v.w;
+      }
+    float rs[4], l[4];
+    // local LDL of the published rows (pivots t..t+3), and the own row's multipliers
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      rs[u] = rsqrt_fast(r[u][t + u]);
+      const float rd = rs[u] * rs[u];
+#pragma unroll
+      for (int w = u + 1; w < 4; ++w) {
+        const float f = r[u][t + w] * rd;
+#pragma unroll
+        for (int c = t + w; c < 16; ++c) r[w][c] = fmaf(-f, r[u][c], r[w][c]);
+      }
+      l[u] = a[t + u] * rs[u];
+      const float m = l[u] * rs[u];
+#pragma unroll
+      for (int c = t + u + 1; c < 16; ++c) a[c] = fmaf(-m, r[u][c], a[c]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[t + u] = l[u];
+      if (g == t + u) inv = rs[u];
+    }
+  }
+}
+
 template <int V>
 __global__ void kern(long long* out, float* sink) {
-  __shared__ __align__(16) float xb[128];
+  __shared__ __align__(16) float xb[256];
   const int lane = threadIdx.x & 31, g = lane & 15;
   float a[16];
 #pragma unroll
@@ -149,7 +196,8 @@ __global__ void kern(long long* out, float* sink) {
     if (V == 0) dfA(b, inv, g);
     else if (V == 1) dfB(b, inv, g, xb + 16 * (lane >> 4));
     else if (V == 2) dfC(b, inv, g, xb + 32 * (lane >> 4));
-    else dfD(b, inv, g, xb + 64 * (lane >> 4));
+    else if (V == 3) dfD(b, inv, g, xb + 64 * (lane >> 4));
+    else dfE(b, inv, g, xb + 128 * (lane >> 4));
     float s = inv;
 #pragma unroll
     for (int c = 0; c < 16; ++c) s += b[c];
@@ -159,6 +207,18 @@ __global__ void kern(long long* out, float* sink) {
     if (it > 2 && t1 - t0 < best) best = t1 - t0;
   }
   if (lane == 0) out[V] = best;
+  // correctness probe: store L row of lane 5 (t <= 5) for cross-variant comparison
+  if (lane == 5) {
+    float b[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) b[c] = a[c];
+    float iv = 0.f;
+    if (V == 0) dfA(b, iv, g);
+    else if (V == 2) dfC(b, iv, g, xb);
+    else if (V == 3) dfD(b, iv, g, xb);
+    else if (V == 4) dfE(b, iv, g, xb);
+    for (int c = 0; c <= 5; ++c) sink[8 + 8 * V + c] = b[c];
+  }
   if (acc == 1.2345f) sink[0] = acc;
 }
 
@@ -171,8 +231,13 @@ int main() {
   kern<1><<<1, 32>>>(d, s);
   kern<2><<<1, 32>>>(d, s);
   kern<3><<<1, 32>>>(d, s);
-  long long h[4];
-  cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+  kern<4><<<1, 32>>>(d, s);
+  long long h[5];
+  cudaMemcpy(h, d, 40, cudaMemcpyDeviceToHost);
+  printf("4-pivot (E): %lld cycles\n", h[4]);
+  float L[64];
+  cudaMemcpy(L, s, 256, cudaMemcpyDeviceToHost);
+  for (int v = 0; v < 5; ++v) { if (v == 1) continue; printf("variant %d row5:", v); for (int c = 0; c <= 5; ++c) printf(" %.6f", L[8 + 8 * v + c]); printf("\n"); }
   printf("diag16 shfl (A): %lld\nsmem-row LDLt div+shfl (B): %lld\nsmem-row LDLt rcp (C): %lld\n2-pivot (D): %lld cycles\n%s\n",
          h[0], h[1], h[2], h[3], cudaGetErrorString(cudaGetLastError()));
   return 0;
