@@ -40,11 +40,13 @@
 // below the threshold, or a non-finite solution (lowest failing index wins).
 #include "fmap_solver.cuh"
 
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <algorithm>
 
 namespace fmap {
@@ -64,12 +66,15 @@ constexpr int kMaxGroups = 3;
 struct TcLayout {
   int K16, P, G;
   int lo[kMaxGroups], hi[kMaxGroups], base[kMaxGroups];
+  int ns;  // systems factored in lockstep per CTA (same row -> same thread)
+  int tma; // next pair's G staged by TMA + tcgen05.cp during the current pair's panels
   int nmain, bwarp, mwarp, threads, aug_tid;
-  int tmem_cols;
+  int tcols1;     // TMEM columns of one system
+  int tmem_cols;  // allocated (ns * tcols1, power of two)
   int Rop;  // operand buffer rows
   int cps;  // CTAs per SM
   // offsets in floats from the dynamic smem base
-  int off_hi, off_lo, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_misc;
+  int off_hi, off_lo, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_a0, off_stg, off_misc;
   int floats;
   long long lb;  // floats of one L scratch slot (global memory)
 };
@@ -80,7 +85,10 @@ __host__ __device__ inline long long lb_off(int p, int K16) {
   return 16ll * p * (K16 - 16) - 128ll * p * (p - 1);
 }
 
-__host__ inline TcLayout make_layout(int k) {
+// ns = 0: pick.  One system per CTA (two CTAs per SM for k <= 256) measured faster
+// than two lockstep systems per CTA once staging moved to TMA + tcgen05.cp (2.23 vs
+// 2.92 ms at cfg2); ns = 2 stays available (FMAP_TC_NS=2).
+__host__ inline TcLayout make_layout(int k, int ns = 0) {
   TcLayout L{};
   L.K16 = (k + 15) & ~15;
   L.P = L.K16 / 16;
@@ -96,26 +104,34 @@ __host__ inline TcLayout make_layout(int k) {
     L.G++;
   }
   const int total = hi > 0 ? 1 << 30 : base;  // rows left over: unsupported
+  int c = 32;
+  while (c < total && c < 1024) c <<= 1;
+  L.tcols1 = c;
+  if (ns <= 0 || 2 * c > 512) ns = 1;
+  L.ns = ns;
+  L.tmem_cols = ns * c;
   const int ntop = L.hi[L.G - 1] - L.lo[L.G - 1];
   L.aug_tid = kTL * (L.G - 1) + ntop;
   L.nmain = 32 * (4 * (L.G - 1) + (ntop + 1 + 31) / 32);
-  L.bwarp = L.nmain / 32;      // back-substitution warp
-  L.mwarp = L.bwarp + 1;       // MMA-issue warp
-  L.threads = L.nmain + 64;
-  int c = 32;
-  while (c < total && c < 1024) c <<= 1;
-  L.tmem_cols = c;
+  L.bwarp = L.nmain / 32;      // back-substitution warps bwarp .. bwarp+ns-1 (one per system)
+  L.mwarp = L.bwarp + ns;      // MMA-issue warp
+  L.threads = L.nmain + 32 * ns + 32;
   L.Rop = L.K16 > kTL ? L.K16 : kTL;
+  const int lbs = (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;
   int o = 0;
-  L.off_hi = o;  o += L.Rop * 16;
-  L.off_lo = o;  o += L.Rop * 16;
-  L.off_lt = o;  o += 256 + 16;               // current diagonal block (transposed) + 1/L_tt
-  L.off_l11 = o; o += 2 * L.P * 152;          // per slot: packed lower L_bb (+ 1/L_tt) of every block
-  L.off_yv = o;  o += 2 * L.K16;              // per slot: y = L^{-1} r
-  L.off_xv = o;  o += L.K16;                  // back substitution: x
-  L.off_lb = o;  o += 2 * (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;  // back substitution: L blocks
-  L.off_zb = o;  o += 32;
-  L.off_misc = o; o += 64;
+  L.off_hi = o;  o += ns * L.Rop * 16;          // per system
+  L.off_lo = o;  o += ns * L.Rop * 16;
+  L.off_lt = o;  o += ns * (256 + 16);          // per system: diagonal block (transposed) + 1/L_tt
+  L.off_l11 = o; o += 2 * ns * L.P * 152;       // per slot: packed lower L_bb (+ 1/L_tt) of every block
+  L.off_yv = o;  o += 2 * ns * L.K16;           // per slot: y = L^{-1} r
+  L.off_xv = o;  o += ns * L.K16;               // back substitution: x (per system)
+  L.off_lb = o;  o += ns * 2 * lbs;             // back substitution: L blocks (per system, 2 buffers)
+  L.off_zb = o;  o += ns * 16;
+  o = (o + 31) & ~31;                           // 128 B aligned (TMA destination)
+  L.off_a0 = o;  o += ns * L.K16 * 16;          // panel-0 columns of every row (float4 [h][t4][row])
+  o = (o + 255) & ~255;                         // 1 KB aligned (TMA destination)
+  L.off_stg = o; o += ns * L.G * 4 * kTL * 4;   // one G chunk of every (system, group): [h][g][u][128 rows][4]
+  L.off_misc = o; o += 128;
   L.floats = o;
   L.lb = (lb_off(L.P, L.K16) + 31) & ~31ll;
   const int cps_tmem = L.tmem_cols <= 512 ? 512 / L.tmem_cols : 0;
@@ -249,6 +265,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(su32(bar))
       : "memory");
 }
+// 4-D tensor TMA load (box from the tensor map) into shared memory.
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
+      : "memory");
+}
+// Shared-memory descriptor with explicit leading / stride byte offsets (no swizzle).
+__device__ __forceinline__ uint64_t sdesc_ls(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// shared memory (128 rows x 32 B, core-matrix layout) -> TMEM lanes 0..127, 8 columns
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
 // Named barrier over the main (factorization) warps only.
 __device__ __forceinline__ void main_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
@@ -363,54 +397,82 @@ __device__ __forceinline__ void sys_of(const SolveParams& p, int64_t sl, int64_t
   }
 }
 
-// Load the 16 entries of row `row` in columns 16cb..16cb+15 as G[c][row] (G is
-// symmetric; coalesced across the warp's consecutive rows: one 128-byte line per
-// load instruction).  Lower part c <= row only.
+// Load G[row][16cb .. 16cb+15] (zero beyond column k-1).  The same entries the
+// TMA path stages (only c <= row is ever used; the rest is carried along unread).
 __device__ __forceinline__ void load_cols(const float* __restrict__ Gq, int k, int row, bool ok, int cb,
                                           float (&v)[16]) {
   const int c0 = 16 * cb;
+  const float* src = Gq + (size_t)row * k + c0;
+  if (ok && (k & 3) == 0 && c0 + 16 <= k) {
 #pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const int c = c0 + t;
-    v[t] = (ok && c <= row && c < k) ? __ldg(Gq + (size_t)c * k + row) : 0.f;
+    for (int t4 = 0; t4 < 4; ++t4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(src) + t4);
+      v[4 * t4] = x.x;
+      v[4 * t4 + 1] = x.y;
+      v[4 * t4 + 2] = x.z;
+      v[4 * t4 + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = (ok && c0 + t < k) ? __ldg(src + t) : 0.f;
   }
 }
 
 // ---------------------------------------------------------------------------
-// Main warps (0..nmain/32-1): staging + blocked factorization of system n of this
-// CTA into slot n&1; the back-substitution warp solves L^T x = y for system n-1
-// meanwhile and writes the row of C.
+// CTA iteration n handles NS systems (sl = NS*pi + h) in lockstep: thread `row`
+// owns row `row` of every one of them (system h in TMEM columns h*tcols1 + ...,
+// its own operand buffers, L scratch and slot NS*(n&1)+h).  Main warps
+// (0..nmain/32-1): staging + blocked factorization; back-substitution warp
+// bwarp+h solves L^T x = y for system h of iteration n-1 meanwhile and writes the
+// row of C.  The 16x16 diagonal factor of system 1 runs on the half-warp that
+// does not hold the diagonal rows, so both blocks cost one dependency chain.
 // ---------------------------------------------------------------------------
-template <int MASK_MODE, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLayout Ly) {
+template <int MASK_MODE, int NS, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+    chol_tc_kernel(SolveParams p, TcLayout Ly, const __grid_constant__ CUtensorMap tmG,
+                   const __grid_constant__ CUtensorMap tmA) {
   extern __shared__ __align__(1024) float smem[];
   const int k = p.k, K16 = Ly.K16, P = Ly.P;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NM = Ly.nmain;
-  float* opnd_hi = smem + Ly.off_hi;
+  const int opsz = Ly.Rop * 16;  // floats of one operand buffer
+  float* opnd_hi = smem + Ly.off_hi;  // system h: + h*opsz
   float* opnd_lo = smem + Ly.off_lo;
-  float* LT = smem + Ly.off_lt;  // current diagonal block, transposed: LT[t][c] = L[c][t]
-  float* inv = LT + 256;         // 1/L_tt of the current block
-  float* zb = smem + Ly.off_zb;
+  float* LTb = smem + Ly.off_lt;  // system h: LT = LTb + 272h, LT[t][c] = L[c][t]; inv = LT + 256
+  float* zb = smem + Ly.off_zb;   // system h: + 16h
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + Ly.off_misc);
-  // mbar[0] LA, [1] REST, [2..3] lfull (back-sub L blocks), [4..5] fact (slot), [6..7] bsub (slot),
-  // [8] opsready (operands of the panel stored, one arrival per main warp), [9] ysync
-  uint64_t* lfull = mbar + 2;
+  // mbar[0] LA, [1] REST, [2] opsready (one arrival per main warp), [3] ysync,
+  // [4 + s] fact (slot s), [4 + 2NS + s] bsub, [4 + 4NS + 2h + u] lfull (B warp h, buffer u),
+  // [4 + 6NS] chk (G chunk TMA), [+1] cpd (tcgen05.cp done), [+2] a0f (panel-0 TMA), [+3] stg
+  // (next pair fully staged: MMA warp -> main warps)
+  uint64_t* opsready = mbar + 2;
+  uint64_t* ysync = mbar + 3;
   uint64_t* fact = mbar + 4;
-  uint64_t* bsub = mbar + 6;
-  uint64_t* opsready = mbar + 8;
-  uint64_t* ysync = mbar + 9;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 20);
-  unsigned* sc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 24);
-  // sc[0] dmax bits, sc[1] pivmin bits, sc[2] bad, sc[3] ev_max bits (current system)
-  unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 40);  // [slot][4]
-  float* Lscr = p.tc_scratch + (size_t)blockIdx.x * 2 * Ly.lb;
+  uint64_t* bsub = mbar + 4 + 2 * NS;
+  uint64_t* lfull = mbar + 4 + 4 * NS;
+  uint64_t* chk = mbar + 4 + 6 * NS;
+  uint64_t* cpd = chk + 1;
+  uint64_t* a0f = chk + 2;
+  uint64_t* stg = chk + 3;
+  float4* a0s = reinterpret_cast<float4*>(smem + Ly.off_a0);  // panel-0 columns: [(h*4 + t4)*K16 + row]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 48);
+  unsigned* scb = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 56);  // [n&1][h][4]
+  // sc[4h+0] dmax bits, [1] pivmin bits, [2] bad, [3] ev_max bits (current systems);
+  // double-buffered by iteration parity, reset right after the hand-off
+  unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 72);  // [slot][4]
+  float* Lscr = p.tc_scratch + (size_t)blockIdx.x * 2 * NS * Ly.lb;
+  const int64_t npi = (p.nsys + NS - 1) / NS;
 
   // ---- one-time setup ----
-  for (int e = tid; e < 2 * Ly.Rop * 16; e += Ly.threads) smem[Ly.off_hi + e] = 0.f;
+  for (int e = tid; e < 2 * NS * opsz; e += Ly.threads) smem[Ly.off_hi + e] = 0.f;
+  if (tid < 2 * NS) {
+    scb[4 * tid + 0] = 0u;
+    scb[4 * tid + 1] = __float_as_uint(FLT_MAX);
+    scb[4 * tid + 2] = 0u;
+    scb[4 * tid + 3] = 0u;
+  }
   if (tid == 0) {
-#pragma unroll
-    for (int e = 0; e < 10; ++e) mbar_init(&mbar[e], e == 8 ? (uint32_t)(Ly.nmain / 32) : 1u);
+    for (int e = 0; e < 8 + 6 * NS; ++e) mbar_init(&mbar[e], e == 2 ? (uint32_t)(Ly.nmain / 32) : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, (uint32_t)Ly.tmem_cols);
@@ -419,22 +481,24 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
-  // ======================= back-substitution warp =======================
-  if (warp == Ly.bwarp) {
-    float* xv = smem + Ly.off_xv;
-    float* lbuf = smem + Ly.off_lb;
+  // ======================= back-substitution warps =======================
+  if (warp >= Ly.bwarp && warp < Ly.bwarp + NS) {
+    const int h = warp - Ly.bwarp;
+    float* xv = smem + Ly.off_xv + h * K16;
     const int lbs = (K16 - 16 > 0 ? K16 - 16 : 1) * 16;  // floats per L block buffer
-    uint32_t lb_use = 0;  // global L-block counter (lfull phases: block use u -> buffer u&1)
+    float* lbuf = smem + Ly.off_lb + h * 2 * lbs;
+    uint64_t* lf = lfull + 2 * h;
+    uint32_t lb_use = 0;  // L-block counter (lfull phases: block use u -> buffer u&1)
     int n = 0;
-    for (int64_t sl = blockIdx.x; sl < p.nsys; sl += gridDim.x, ++n) {
-      const int slot = n & 1;
-      int64_t q;
-      int i;
-      sys_of(p, sl, q, i);
-      const int64_t sys = q * k + i;  // global system index (error convention)
+    for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x, ++n) {
+      const int slot = NS * (n & 1) + h;
       mbar_wait(&fact[slot], (n >> 1) & 1);
       unsigned* ssc = slotsc + 4 * slot;
       if (ssc[3] == 0u) {
+        int64_t q;
+        int i;
+        sys_of(p, NS * pi + h, q, i);
+        const int64_t sys = q * k + i;  // global system index (error convention)
         const float* L11 = smem + Ly.off_l11 + slot * P * 152;
         const float* yv = smem + Ly.off_yv + slot * K16;
         const float* Lsl = Lscr + (size_t)slot * Ly.lb;
@@ -442,8 +506,8 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
         auto issue_blk = [&](int b, uint32_t use) {
           const uint32_t bytes = (uint32_t)(K16 - 16 * b - 16) * 64u;
           if (lane == 0) {
-            mbar_expect_tx(&lfull[use & 1], bytes);
-            bulk_g2s(lbuf + (use & 1) * lbs, Lsl + lb_off(b, K16), bytes, &lfull[use & 1]);
+            mbar_expect_tx(&lf[use & 1], bytes);
+            bulk_g2s(lbuf + (use & 1) * lbs, Lsl + lb_off(b, K16), bytes, &lf[use & 1]);
           }
         };
         if (P >= 2) issue_blk(P - 2, lb_use);
@@ -466,7 +530,7 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
           const int R = K16 - 16 * b - 16;
           if (R > 0) {
             const uint32_t use = lb_use++;
-            mbar_wait(&lfull[use & 1], (use >> 1) & 1);
+            mbar_wait(&lf[use & 1], (use >> 1) & 1);
             if (b >= 1) issue_blk(b - 1, lb_use);  // prefetch the next block (other buffer)
             const float* blk = lbuf + (use & 1) * lbs;
             for (int rho = lane >> 2; rho < R; rho += 8) {
@@ -528,16 +592,16 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
   // ======================= MMA-issue warp =======================
   // Per panel: wait until every main warp has stored its L21 operands, release the
   // panel's y to the main warps (ysync), then issue the tensor-core trailing update
-  // of every group: lookahead (next panel's 16 columns, committed to LA) first,
-  // then the rest (REST).
+  // of every group of every system: lookahead (next panel's 16 columns, committed
+  // to LA) first, then the rest (REST).
   if (warp == Ly.mwarp) {
     if (lane == 0) {
-      const uint32_t hib = su32(opnd_hi), lob = su32(opnd_lo);
-      auto mma3 = [&](int glo_, int gbase_, int c0, int N) {
+      auto mma3 = [&](int h, int glo_, int gbase_, int c0, int N) {
+        const uint32_t hib = su32(opnd_hi + h * opsz), lob = su32(opnd_lo + h * opsz);
         const uint32_t arow = (uint32_t)(glo_ >> 3) * 512u;
         const uint32_t brow = (uint32_t)(c0 >> 3) * 512u;
         const uint32_t id = idesc_tf32(N);
-        const uint32_t dcol = tbase + (uint32_t)(gbase_ + c0 - 16);
+        const uint32_t dcol = tbase + (uint32_t)(h * Ly.tcols1 + gbase_ + c0 - 16);
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
           const uint32_t ko = (uint32_t)ks * 256u;
@@ -548,28 +612,115 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
           mma_tf32(dcol, al, bh, id);
         }
       };
-      uint32_t gm = 0;
-      for (int64_t sl = blockIdx.x; sl < p.nsys; sl += gridDim.x) {
+      // Staging of the NEXT pair (Ly.tma): chunk cb = matrix columns 16cb..16cb+15 of
+      // every row.  After panel pp's opsready every main warp has read chunk pp of
+      // the current pair, so the next pair's chunk pp is copied into those TMEM
+      // columns (tcgen05.cp from a shared-memory tile filled by TMA one panel
+      // earlier); its panel-0 columns go to a0s by TMA.
+      float* stile = smem + Ly.off_stg;
+      auto grp_has = [&](int gg, int cb) { return gg < Ly.G && cb < (Ly.hi[gg] >> 4); };
+      auto tma_chunk = [&](int cb, const int64_t (&qn)[NS], const bool (&vn)[NS]) {
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int h = 0; h < NS; ++h)
+#pragma unroll
+          for (int gg = 0; gg < kMaxGroups; ++gg)
+            if (vn[h] && grp_has(gg, cb)) bytes += 4u * kTL * 16u;
+        mbar_expect_tx(chk, bytes);
+#pragma unroll
+        for (int h = 0; h < NS; ++h)
+#pragma unroll
+          for (int gg = 0; gg < kMaxGroups; ++gg)
+            if (vn[h] && grp_has(gg, cb))
+              tma_load_4d(stile + (h * Ly.G + gg) * 4 * (kTL * 4), &tmG, 0, Ly.lo[gg], 4 * cb, (int)qn[h], chk);
+      };
+      auto cp_chunk = [&](int cb, const bool (&vn)[NS]) {
+#pragma unroll
+        for (int h = 0; h < NS; ++h)
+#pragma unroll
+          for (int gg = 0; gg < kMaxGroups; ++gg)
+            if (vn[h] && grp_has(gg, cb))
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                const uint32_t src = su32(stile + ((h * Ly.G + gg) * 4 + 2 * hf) * (kTL * 4));
+                const uint32_t dst = tbase + (uint32_t)(h * Ly.tcols1 + Ly.base[gg] + 16 * cb - 16 + 8 * hf);
+                tmem_cp_128x256b(dst, sdesc_ls(src, (uint32_t)kTL * 16u, 128u));
+              }
+      };
+      uint32_t gm = 0, n_chk = 0, n_cpd = 0, n_a0 = 0;
+      for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x) {
+        const int64_t pi2 = pi + gridDim.x;
+        const bool pf = Ly.tma && pi2 < npi;
+        int64_t qn[NS];
+        bool vn[NS];
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+          int in_;
+          vn[h] = pf && NS * pi2 + h < p.nsys;
+          sys_of(p, vn[h] ? NS * pi2 + h : 0, qn[h], in_);
+        }
+        bool cpd_pending = false;
         for (int pp = 0; pp < P; ++pp, ++gm) {
           mbar_wait(opsready, gm & 1);
           mbar_arrive(ysync);
           tc_fence_after();
           const int r0 = 16 * pp + 16;
 #pragma unroll
-          for (int gg = 0; gg < kMaxGroups; ++gg)
-            if (gg < Ly.G && Ly.hi[gg] > r0) mma3(Ly.lo[gg], Ly.base[gg], r0, 16);
-          mma_commit(&mbar[0]);
+          for (int h = 0; h < NS; ++h)
 #pragma unroll
-          for (int gg = 0; gg < kMaxGroups; ++gg) {
-            if (gg >= Ly.G) continue;
-            int c0 = r0 + 16;
-            while (c0 < Ly.hi[gg]) {
-              const int N = min(256, Ly.hi[gg] - c0);
-              mma3(Ly.lo[gg], Ly.base[gg], c0, N);
-              c0 += N;
-            }
+            for (int gg = 0; gg < kMaxGroups; ++gg)
+              if (gg < Ly.G && Ly.hi[gg] > r0) mma3(h, Ly.lo[gg], Ly.base[gg], r0, 16);
+          mma_commit(&mbar[0]);
+          // next pair: panel-0 columns (a0s is free: every main warp is past panel 0)
+          // and chunk pp into the tile (free once the previous chunk's copies are done)
+          if (pf && pp == 0) {
+            uint32_t bytes = 0;
+#pragma unroll
+            for (int h = 0; h < NS; ++h)
+              if (vn[h]) bytes += 4u * (uint32_t)K16 * 16u;
+            mbar_expect_tx(a0f, bytes);
+#pragma unroll
+            for (int h = 0; h < NS; ++h)
+              if (vn[h]) tma_load_4d(a0s + h * 4 * K16, &tmA, 0, 0, 0, (int)qn[h], a0f);
           }
+          if (pf && pp >= 1) {
+            if (cpd_pending) {
+              mbar_wait(cpd, n_cpd & 1);
+              ++n_cpd;
+              cpd_pending = false;
+            }
+            tma_chunk(pp, qn, vn);
+          }
+#pragma unroll
+          for (int h = 0; h < NS; ++h)
+#pragma unroll
+            for (int gg = 0; gg < kMaxGroups; ++gg) {
+              if (gg >= Ly.G) continue;
+              int c0 = r0 + 16;
+              while (c0 < Ly.hi[gg]) {
+                const int N = min(256, Ly.hi[gg] - c0);
+                mma3(h, Ly.lo[gg], Ly.base[gg], c0, N);
+                c0 += N;
+              }
+            }
           mma_commit(&mbar[1]);
+          if (pf && pp >= 1) {  // chunk pp of the current pair was read at this panel's top
+            mbar_wait(chk, n_chk & 1);
+            ++n_chk;
+            cp_chunk(pp, vn);
+            mma_commit(cpd);
+            cpd_pending = true;
+          }
+        }
+        if (pf) {  // hand the staged next pair to the main warps
+          if (cpd_pending) {
+            mbar_wait(cpd, n_cpd & 1);
+            ++n_cpd;
+          }
+          mbar_wait(a0f, n_a0 & 1);
+          ++n_a0;
+          tc_fence_before();
+          mbar_arrive(stg);
         }
       }
     }
@@ -592,115 +743,207 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
   const bool row_valid = has_grp && row < ghi;
   const bool is_aug = tid == Ly.aug_tid;  // augmented right-hand-side "row"
   const uint32_t tq = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)gbase - 16u;  // + column c
+  const uint32_t tsys = (uint32_t)Ly.tcols1;  // TMEM column offset between systems
 
   uint32_t g = 0;  // global panel counter (LA / REST mbarrier phases)
   bool any_mma = false;
+  const int ncb = ghi >> 4;  // column chunks of this warp's group (warp-uniform)
+
+  // Staging of the NEXT pair is software-pipelined into the panel loop: after
+  // panel pp has read its columns, chunk pp (matrix columns 16pp..16pp+15) is dead
+  // in TMEM, so the next pair's chunk pp is loaded at the end of panel pp and
+  // stored at the top of panel pp+1; chunk 0 (registers), the last chunk and the
+  // per-row right-hand side / mask entry are loaded at the end of the last panel.
+  bool pre = false;        // the current pair's G chunks were prefetched
+  float rhs_n[NS], mraw_n[NS];
+  uint32_t n_stg = 0;
+#pragma unroll
+  for (int h = 0; h < NS; ++h) {
+    rhs_n[h] = 0.f;
+    mraw_n[h] = 0.f;
+  }
 
   int n = 0;
-  for (int64_t sl = blockIdx.x; sl < p.nsys; sl += gridDim.x, ++n) {
-    const int slot = n & 1;
-    int64_t q;
-    int i;
-    sys_of(p, sl, q, i);
+  for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x, ++n) {
+    int64_t qs[NS];
+    int is[NS];
+    bool vld[NS];
+#pragma unroll
+    for (int h = 0; h < NS; ++h) {
+      const int64_t sl = NS * pi + h;
+      vld[h] = sl < p.nsys;
+      sys_of(p, vld[h] ? sl : 0, qs[h], is[h]);
+    }
+    const int64_t pi2 = pi + gridDim.x;  // next pair of this CTA
+    const bool has_next = pi2 < npi;
+    int64_t qn[NS];
+    int in_[NS];
+    bool ldn[NS];
+#pragma unroll
+    for (int h = 0; h < NS; ++h) {
+      const int64_t sl = NS * pi2 + h;
+      ldn[h] = has_next && sl < p.nsys && row_valid && row < k;
+      sys_of(p, ldn[h] ? sl : 0, qn[h], in_[h]);
+    }
     const bool tr_on = blockIdx.x == (unsigned)p.trace_block && n == 1;
     TC_TRACE(tid == 0, 0);
-    float* L11all = smem + Ly.off_l11 + slot * P * 152;
-    float* yv = smem + Ly.off_yv + slot * K16;
-    float* Lslot = Lscr + (size_t)slot * Ly.lb;
+    const int slot0 = NS * (n & 1);
 
-    // slot reuse: the back-substitution of system n-2 must be done with it
-    if (n >= 2) mbar_wait(&bsub[slot], ((n - 2) >> 1) & 1);
-    if (tid == 0) {
+    // slot reuse: the back-substitution of iteration n-2 must be done with it
+    if (n >= 2) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) sc[e] = 0u;
-      sc[1] = __float_as_uint(FLT_MAX);
+      for (int h = 0; h < NS; ++h) mbar_wait(&bsub[slot0 + h], ((n - 2) >> 1) & 1);
     }
-    float ev_max = 0.f;
-    bool skip = false;
+    unsigned* sc = scb + 4 * NS * (n & 1);
+    float ev_max[NS];
+    bool skip[NS];
+#pragma unroll
+    for (int h = 0; h < NS; ++h) {
+      ev_max[h] = 0.f;
+      skip[h] = !vld[h];
+    }
     if constexpr (MASK_MODE == 1) {
       main_sync(NM);
-      float m = 0.f;
-      for (int c = tid; c < k; c += NM)
-        m = fmaxf(m, fmaxf(p.ev1[(size_t)q * k + c], p.ev2[(size_t)q * k + c]));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-      if (lane == 0) atomicMax(&sc[3], __float_as_uint(m));
+      for (int h = 0; h < NS; ++h) {
+        float m = 0.f;
+        for (int c = tid; c < k; c += NM)
+          m = fmaxf(m, fmaxf(p.ev1[(size_t)qs[h] * k + c], p.ev2[(size_t)qs[h] * k + c]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+        if (lane == 0) atomicMax(&sc[4 * h + 3], __float_as_uint(m));
+      }
       main_sync(NM);
-      ev_max = __uint_as_float(sc[3]);
-      skip = !(ev_max > 0.f);
+#pragma unroll
+      for (int h = 0; h < NS; ++h) {
+        ev_max[h] = __uint_as_float(sc[4 * h + 3]);
+        skip[h] = skip[h] || !(ev_max[h] > 0.f);
+      }
     }
 
     // ---- staging: row r of (G + lambda*diag(m_i) + ridge*I), identity padding ----
     // Row r of G (read as column r, G[c][r]: coalesced; the lower triangle used is
     // G's upper triangle, as the SIMT solver; G = A A^T is symmetric by
     // construction).  Columns 0..15 stay in registers (panel 0), the rest go to the
-    // group's TMEM region, two chunks of loads in flight.
+    // group's TMEM region.  Raw G first (prefetched during the previous pair's
+    // panels, or loaded here for the first pair), then lambda*m + ridge is added to
+    // the diagonal entry in place.
     TC_TRACE(tid == 0, 398);
-    float rhs = 0.f, dmax = 0.f, dadd = 0.f;
-    const bool ld_ok = row_valid && row < k && !skip;
-    if (ld_ok) {
-      rhs = p.rhs_unit < 0 ? p.rhs[((size_t)q * k + i) * k + row] : (row == p.rhs_unit ? 1.f : 0.f);
-      dadd = p.lambda * mask_entry<MASK_MODE>(p, q, i, row, ev_max) + p.ridge;
+    float rhs[NS], dmax[NS], dadd[NS];
+#pragma unroll
+    for (int h = 0; h < NS; ++h) {
+      rhs[h] = 0.f;
+      dmax[h] = 0.f;
+      dadd[h] = 0.f;
+      if (row_valid && row < k && !skip[h]) {
+        if (MASK_MODE != 1 && pre) {
+          rhs[h] = rhs_n[h];
+          dadd[h] = p.lambda * mraw_n[h] + p.ridge;
+        } else {
+          rhs[h] = p.rhs_unit < 0 ? p.rhs[((size_t)qs[h] * k + is[h]) * k + row]
+                                  : (row == p.rhs_unit ? 1.f : 0.f);
+          dadd[h] = p.lambda * mask_entry<MASK_MODE>(p, qs[h], is[h], row, ev_max[h]) + p.ridge;
+        }
+      }
     }
-    const float* Gq = p.gram + (size_t)q * k * k;
-    // previous system's MMAs must be complete before TMEM is rewritten
+    // previous systems' MMAs must be complete before TMEM is rewritten
     if (any_mma) {
       mbar_wait(&mbar[1], (g - 1) & 1);
       tc_fence_after();
     }
     TC_TRACE(tid == 0, 399);
-    float a0[16];
     {
-      const int ncb = ghi >> 4;        // column chunks of this group (warp-uniform)
       const int dcb = row >> 4, dt = row & 15;  // chunk / slot of the diagonal entry
-      auto fix_diag = [&](float (&v)[16], int cb) {
+      auto fix_diag = [&](float (&v)[16], int cb, int h) {
         if (row_valid && dcb == cb) {
 #pragma unroll
           for (int u = 0; u < 16; ++u)
             if (u == dt) {
-              v[u] = row < k ? v[u] + dadd : 1.f;
-              dmax = row < k ? fabsf(v[u]) : 0.f;
+              v[u] = row < k ? v[u] + dadd[h] : 1.f;
+              dmax[h] = row < k ? fabsf(v[u]) : 0.f;
             }
         }
       };
-      for (int cb = 1; cb < ncb; cb += 2) {  // two chunks of loads in flight
-        float b0[16], b1[16];
-        load_cols(Gq, k, row, ld_ok, cb, b0);
-        if (cb + 1 < ncb) load_cols(Gq, k, row, ld_ok, cb + 1, b1);
-        fix_diag(b0, cb);
-        tmem_st16(tq + (uint32_t)(16 * cb), b0);
-        if (cb + 1 < ncb) {
-          fix_diag(b1, cb + 1);
-          tmem_st16(tq + (uint32_t)(16 * (cb + 1)), b1);
+      if (!pre) {
+        bool ld_ok[NS];
+        const float* Gq[NS];
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+          ld_ok[h] = row_valid && row < k && vld[h];
+          Gq[h] = p.gram + (size_t)qs[h] * k * k;
+        }
+        for (int cb = 1; cb < ncb; ++cb) {  // one chunk of every system in flight
+          float b[NS][16];
+#pragma unroll
+          for (int h = 0; h < NS; ++h) load_cols(Gq[h], k, row, ld_ok[h], cb, b[h]);
+#pragma unroll
+          for (int h = 0; h < NS; ++h) {
+            fix_diag(b[h], cb, h);
+            tmem_st16(tq + tsys * h + (uint32_t)(16 * cb), b[h]);
+          }
+        }
+        if (row_valid) {
+#pragma unroll
+          for (int h = 0; h < NS; ++h) {
+            float v[16];
+            load_cols(Gq[h], k, row, ld_ok[h], 0, v);
+#pragma unroll
+            for (int t4 = 0; t4 < 4; ++t4)
+              a0s[(h * 4 + t4) * K16 + row] = make_float4(v[4 * t4], v[4 * t4 + 1], v[4 * t4 + 2], v[4 * t4 + 3]);
+          }
+        }
+      } else {
+        mbar_wait(stg, n_stg & 1);  // TMA / tcgen05.cp staging of this pair complete
+        ++n_stg;
+        tc_fence_after();
+        // diagonal entries in TMEM: this warp's rows span chunks c0w, c0w+1
+        const int c0w = (glo + 32 * quarter) >> 4;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc = c0w + e;
+          if (cc >= 1 && cc < ncb) {
+#pragma unroll
+            for (int h = 0; h < NS; ++h) {
+              float v[16];
+              tmem_ld16(tq + tsys * h + (uint32_t)(16 * cc), v);
+              fix_diag(v, cc, h);
+              tmem_st16(tq + tsys * h + (uint32_t)(16 * cc), v);
+            }
+          }
         }
       }
-      load_cols(Gq, k, row, ld_ok, 0, a0);
-      if (row_valid && dcb == 0) {
+      if (row_valid && row < 16) {  // diagonal entries of panel 0 (shared memory)
 #pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (u == dt) {
-            a0[u] = row < k ? a0[u] + dadd : 1.f;
-            dmax = row < k ? fabsf(a0[u]) : 0.f;
-          }
+        for (int h = 0; h < NS; ++h) {
+          float* e = reinterpret_cast<float*>(a0s + (h * 4 + (row >> 2)) * K16 + row) + (row & 3);
+          *e = row < k ? *e + dadd[h] : 1.f;
+          dmax[h] = row < k ? fabsf(*e) : 0.f;
+        }
       }
     }
     if (has_grp) tmem_st_wait();
-    {
-      float m = dmax;
+#pragma unroll
+    for (int h = 0; h < NS; ++h) {
+      float m = dmax[h];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-      if (lane == 0) atomicMax(&sc[0], __float_as_uint(m));
+      if (lane == 0) atomicMax(&sc[4 * h], __float_as_uint(m));
     }
     tc_fence_before();
     main_sync(NM);
     tc_fence_after();
     TC_TRACE(tid == 0, 1);
 
-    float pivmin = FLT_MAX;
-    unsigned bad = 0u;
-    float lprev[16];
+    float pivmin[NS];
+    unsigned bad[NS];
+    float lprev[NS][16];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) lprev[t] = 0.f;
+    for (int h = 0; h < NS; ++h) {
+      pivmin[h] = FLT_MAX;
+      bad[h] = 0u;
+#pragma unroll
+      for (int t = 0; t < 16; ++t) lprev[h][t] = 0.f;
+    }
 
     // ---- panels ----
     for (int pp = 0; pp < P; ++pp, ++g) {
@@ -711,124 +954,220 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
         mbar_wait(ysync, (g - 1) & 1);
         if (active) {
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            const float4 y4 = *reinterpret_cast<const float4*>(yv + j - 16 + 4 * c4);
-            rhs = fmaf(-lprev[4 * c4], y4.x, rhs);
-            rhs = fmaf(-lprev[4 * c4 + 1], y4.y, rhs);
-            rhs = fmaf(-lprev[4 * c4 + 2], y4.z, rhs);
-            rhs = fmaf(-lprev[4 * c4 + 3], y4.w, rhs);
+          for (int h = 0; h < NS; ++h) {
+            const float* yv = smem + Ly.off_yv + (slot0 + h) * K16;
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const float4 y4 = *reinterpret_cast<const float4*>(yv + j - 16 + 4 * c4);
+              rhs[h] = fmaf(-lprev[h][4 * c4], y4.x, rhs[h]);
+              rhs[h] = fmaf(-lprev[h][4 * c4 + 1], y4.y, rhs[h]);
+              rhs[h] = fmaf(-lprev[h][4 * c4 + 2], y4.z, rhs[h]);
+              rhs[h] = fmaf(-lprev[h][4 * c4 + 3], y4.w, rhs[h]);
+            }
           }
         }
       }
-      float a[16];
+      float a[NS][16];
+      auto load_a0 = [&](int h, float (&v)[16]) {
+        if (row_valid) {
+#pragma unroll
+          for (int t4 = 0; t4 < 4; ++t4) {
+            const float4 x = a0s[(h * 4 + t4) * K16 + row];
+            v[4 * t4] = x.x;
+            v[4 * t4 + 1] = x.y;
+            v[4 * t4 + 2] = x.z;
+            v[4 * t4 + 3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) v[t] = 0.f;
+        }
+      };
       if (pp == 0) {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) a[t] = a0[t];
+        for (int h = 0; h < NS; ++h) load_a0(h, a[h]);
       } else if (has_grp && ghi > j) {  // panel columns updated by the previous lookahead MMA
         mbar_wait(&mbar[0], (g - 1) & 1);
         tc_fence_after();
-        tmem_ld16(tq + (uint32_t)j, a);
+#pragma unroll
+        for (int h = 0; h < NS; ++h) tmem_ld16(tq + tsys * h + (uint32_t)j, a[h]);
       } else {
 #pragma unroll
-        for (int t = 0; t < 16; ++t) a[t] = 0.f;
+        for (int h = 0; h < NS; ++h)
+#pragma unroll
+          for (int t = 0; t < 16; ++t) a[h][t] = 0.f;
       }
       TC_TRACE(tid == 0, 2 + 4 * pp);
-      // b. diagonal block (rows j..j+15 live in one warp)
+      // b. diagonal blocks (rows j..j+15 live in one half of one warp; the other
+      //    half factors system 1's block)
       const bool in_diag = active && row < j + 16;
       int dwarp = 0;
 #pragma unroll
       for (int gg = 0; gg < kMaxGroups; ++gg)
         if (gg < Ly.G && j >= Ly.lo[gg] && j < Ly.hi[gg]) dwarp = 4 * gg + ((j - Ly.lo[gg]) >> 5);
       if (warp == dwarp) {
-        float iv = 0.f;
-        diag_factor(a, iv, lane & 15, in_diag && row < k, pivmin, bad);
-        if (in_diag) {
-          const int gr = row - j;
-          float* Lpk = L11all + pp * 152 + gr * (gr + 1) / 2;  // packed copy for the back-sub warp
-          L11all[pp * 152 + 136 + gr] = iv;
+        const bool upper = ((j - glo) & 31) != 0;         // diagonal rows in lanes 16..31
+        const bool own = (lane >= 16) == upper;           // this lane holds a diagonal row
+        const int hs = own ? 0 : NS - 1;                  // system factored by this lane
+        const int gr = lane & 15, drow = j + gr;
+        // factor w (system hs's row drow) and publish it; `real` = a row of the block
+        auto diag_emit = [&](float (&w)[16], bool real) {
+          float iv = 0.f, pm = FLT_MAX;
+          unsigned bd = 0u;
+          bool sys_ok = false;
+#pragma unroll
+          for (int h = 0; h < NS; ++h)
+            if (h == hs) sys_ok = !skip[h];
+          diag_factor(w, iv, gr, real && drow < k && sys_ok, pm, bd);
+#pragma unroll
+          for (int h = 0; h < NS; ++h)
+            if (h == hs) {
+              pivmin[h] = fminf(pivmin[h], pm);
+              bad[h] |= bd;
+            }
+          if (real) {
+            float* L11s = smem + Ly.off_l11 + (slot0 + hs) * P * 152 + pp * 152;
+            float* LT = LTb + 272 * hs;
+            float* Lpk = L11s + gr * (gr + 1) / 2;  // packed copy for the back-sub warp
+            L11s[136 + gr] = iv;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              LT[t * 16 + gr] = (t <= gr) ? w[t] : 0.f;  // transposed, for the TRSM
+              if (t <= gr) Lpk[t] = w[t];
+            }
+            LT[256 + gr] = iv;
+          }
+        };
+        if constexpr (NS == 1) {
+          diag_emit(a[0], own);
+          // the other half-warp's rows were clobbered by the factorization: reload
+          if (pp == 0) {
+            load_a0(0, a[0]);
+          } else {
+            tmem_ld16(tq + (uint32_t)j, a[0]);
+          }
+        } else {
+          float w[16];
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            LT[t * 16 + gr] = (t <= gr) ? a[t] : 0.f;  // transposed, for the TRSM
-            if (t <= gr) Lpk[t] = a[t];
+            const float o = __shfl_xor_sync(kFull, a[NS - 1][t], 16);
+            w[t] = own ? a[0][t] : o;
           }
-          inv[gr] = iv;
-          zb[gr] = rhs;
+          diag_emit(w, true);
         }
-        // the other half-warp's rows were clobbered by the factorization: reload
-        if (pp == 0) {
+        if (in_diag) {
 #pragma unroll
-          for (int t = 0; t < 16; ++t) a[t] = a0[t];
-        } else {
-          tmem_ld16(tq + (uint32_t)j, a);
+          for (int h = 0; h < NS; ++h) zb[16 * h + gr] = rhs[h];
         }
         TC_TRACE(row == j, 3 + 4 * pp);
       }
       main_sync(NM);
       // c. TRSM rows >= j+16 ; augmented row -> y for this panel
-      float l[16];
+      float l[NS][16];
       const bool trsm = active && row >= j + 16;
       if (trsm) {
-        trsm_row(LT, inv, a, l);
+#pragma unroll
+        for (int h = 0; h < NS; ++h) trsm_row(LTb + 272 * h, LTb + 272 * h + 256, a[h], l[h]);
       } else if (is_aug) {
-        float z[16];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) z[t] = zb[t];
-        trsm_row(LT, inv, z, l);
+        for (int h = 0; h < NS; ++h) {
+          float z[16];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) yv[j + t] = l[t];
+          for (int t = 0; t < 16; ++t) z[t] = zb[16 * h + t];
+          trsm_row(LTb + 272 * h, LTb + 272 * h + 256, z, l[h]);
+          float* yv = smem + Ly.off_yv + (slot0 + h) * K16;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) yv[j + t] = l[h][t];
+        }
       }
       // d. store L21: scratch (back substitution), operand hi/lo
       if (trsm) {
-        float4* dst = reinterpret_cast<float4*>(Lslot + lb_off(pp, K16) + (size_t)(row - j - 16) * 16);
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4)
-          __stcg(dst + c4, make_float4(l[4 * c4], l[4 * c4 + 1], l[4 * c4 + 2], l[4 * c4 + 3]));
+        for (int h = 0; h < NS; ++h) {
+          float4* dst = reinterpret_cast<float4*>(Lscr + (size_t)(slot0 + h) * Ly.lb + lb_off(pp, K16) +
+                                                  (size_t)(row - j - 16) * 16);
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4)
+            __stcg(dst + c4, make_float4(l[h][4 * c4], l[h][4 * c4 + 1], l[h][4 * c4 + 2], l[h][4 * c4 + 3]));
+        }
         if (pp > 0) mbar_wait(&mbar[1], (g - 1) & 1);  // previous REST MMA done reading
-        float* h = opnd_hi + opnd_idx(row, 0);
-        float* lo = opnd_lo + opnd_idx(row, 0);
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          float hv[4], lv[4];
+        for (int h = 0; h < NS; ++h) {
+          float* hp = opnd_hi + h * opsz + opnd_idx(row, 0);
+          float* lp = opnd_lo + h * opsz + opnd_idx(row, 0);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) split_tf32(l[4 * c4 + u], hv[u], lv[u]);
-          *reinterpret_cast<float4*>(h + c4 * 32) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-          *reinterpret_cast<float4*>(lo + c4 * 32) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+          for (int c4 = 0; c4 < 4; ++c4) {
+            float hv[4], lv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) split_tf32(l[h][4 * c4 + u], hv[u], lv[u]);
+            *reinterpret_cast<float4*>(hp + c4 * 32) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+            *reinterpret_cast<float4*>(lp + c4 * 32) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+          }
         }
       }
       TC_TRACE(tid == 0, 4 + 4 * pp);
       fence_async_smem();
+      tc_fence_before();  // this panel's TMEM reads precede the MMA warp's copies into chunk pp
       __syncwarp();
       if (lane == 0) mbar_arrive(opsready);  // operands of this panel stored
       any_mma = true;
 #pragma unroll
-      for (int t = 0; t < 16; ++t) lprev[t] = trsm ? l[t] : 0.f;
+      for (int h = 0; h < NS; ++h)
+#pragma unroll
+        for (int t = 0; t < 16; ++t) lprev[h][t] = trsm ? l[h][t] : 0.f;
+      if (has_next) {
+        if (pp == P - 1) {
+#pragma unroll
+          for (int h = 0; h < NS; ++h) {
+            if (MASK_MODE != 1 && ldn[h]) {
+              rhs_n[h] = p.rhs_unit < 0 ? p.rhs[((size_t)qn[h] * k + in_[h]) * k + row]
+                                        : (row == p.rhs_unit ? 1.f : 0.f);
+              mraw_n[h] = mask_entry<MASK_MODE>(p, qn[h], in_[h], row, 0.f);
+            }
+          }
+        }
+      }
     }
+    pre = Ly.tma && has_next;
     TC_TRACE(tid == 0, 200);
 
-    // ---- hand the system to the back-substitution warp ----
+    // ---- hand the systems to the back-substitution warps ----
     asm volatile("fence.proxy.async.global;" ::: "memory");  // L scratch -> bulk-copy reads
-    {
-      unsigned b = bad;
-      float pm = pivmin;
+#pragma unroll
+    for (int h = 0; h < NS; ++h) {
+      unsigned b = bad[h];
+      float pm = pivmin[h];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         b |= __shfl_xor_sync(kFull, b, o);
         pm = fminf(pm, __shfl_xor_sync(kFull, pm, o));
       }
       if (lane == 0) {
-        if (b) atomicOr(&sc[2], 1u);
-        atomicMin(&sc[1], __float_as_uint(fmaxf(pm, 0.f)));
+        if (b) atomicOr(&sc[4 * h + 2], 1u);
+        atomicMin(&sc[4 * h + 1], __float_as_uint(fmaxf(pm, 0.f)));
       }
     }
     main_sync(NM);
-    if (tid == 0) {
-      unsigned* ssc = slotsc + 4 * slot;
-      ssc[0] = sc[0];
-      ssc[1] = sc[1];
-      ssc[2] = sc[2];
-      ssc[3] = skip ? 1u : 0u;
-      if (skip) atomicOr(p.flags, 32u);
-      mbar_arrive(&fact[slot]);
+    if (tid < NS) {
+      const int h = tid;
+      bool sk = false, vv = false;
+#pragma unroll
+      for (int hh = 0; hh < NS; ++hh)
+        if (hh == h) {
+          sk = skip[hh];
+          vv = vld[hh];
+        }
+      unsigned* ssc = slotsc + 4 * (slot0 + h);
+      ssc[0] = sc[4 * h + 0];
+      ssc[1] = sc[4 * h + 1];
+      ssc[2] = sc[4 * h + 2];
+      ssc[3] = sk ? 1u : 0u;
+      sc[4 * h + 0] = 0u;
+      sc[4 * h + 1] = __float_as_uint(FLT_MAX);
+      sc[4 * h + 2] = 0u;
+      sc[4 * h + 3] = 0u;
+      if (sk && vv) atomicOr(p.flags, 32u);
+      mbar_arrive(&fact[slot0 + h]);
     }
     TC_TRACE(tid == 0, 203);
   }
@@ -843,16 +1182,56 @@ __global__ void __launch_bounds__(MAXT, MINB) chol_tc_kernel(SolveParams p, TcLa
 
 }  // namespace
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+// Gram batch G[q][r][c] (k x k fp32, row-major, k % 4 == 0) as the 4-D tensor
+// (c % 4, r, c / 4, q); box = 4 x `rows` x 4 x 1 lands as [c/4][r][c%4], i.e. 16 B
+// per row per 4-column group: the no-swizzle core-matrix layout tcgen05.cp reads
+// (and the float4 [t4][row] layout of a0s).  Out-of-range rows / columns are
+// zero-filled (identity padding is added later).
+static int encode_gram_map(CUtensorMap* m, const float* gram, int k, int64_t npairs, int rows) {
+  const EncodeTiledFn fn = encode_fn();
+  if (!fn || npairs < 1) return -1;
+  const cuuint64_t dims[4] = {4, (cuuint64_t)k, (cuuint64_t)(k / 4), (cuuint64_t)npairs};
+  const cuuint64_t strides[3] = {(cuuint64_t)k * 4, 16, (cuuint64_t)k * k * 4};
+  const cuuint32_t box[4] = {4, (cuuint32_t)rows, 4, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(gram), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : -1;
+}
+
+static int tc_ns_override() {
+  const char* s = std::getenv("FMAP_TC_NS");  // diagnostics: 1 = one system per CTA
+  return s ? std::atoi(s) : 0;
+}
+
 size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms) {
-  const TcLayout L = make_layout(k);
+  const TcLayout L = make_layout(k, tc_ns_override());
+  const int64_t npi = (nsys + L.ns - 1) / L.ns;
   const int64_t maxgrid = (int64_t)num_sms * L.cps;
-  const int64_t grid = nsys < maxgrid ? nsys : maxgrid;
-  return (size_t)grid * 2 * (size_t)L.lb * sizeof(float);
+  const int64_t grid = npi < maxgrid ? npi : maxgrid;
+  return (size_t)grid * 2 * L.ns * (size_t)L.lb * sizeof(float);
 }
 
 bool tc_supported(int k, int optin_smem) {
   if (k < 1) return false;
-  const TcLayout L = make_layout(k);
+  const TcLayout L = make_layout(k, tc_ns_override());
   if (L.tmem_cols > 512 || L.cps < 1 || L.threads > 384) return false;
   return (size_t)L.floats * 4 <= (size_t)optin_smem;
 }
@@ -865,7 +1244,7 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  TcLayout L = make_layout(p.k);
+  TcLayout L = make_layout(p.k, tc_ns_override());
   if (L.tmem_cols > 512 || L.cps < 1 || L.threads > 384 || !p.tc_scratch) return cudaErrorNotSupported;
   if (const char* c = std::getenv("FMAP_TC_CPS")) L.cps = std::max(1, std::min(L.cps, std::atoi(c)));  // diagnostics
   // cap residency at L.cps CTAs per SM through the shared-memory request, so no
@@ -877,25 +1256,50 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
     if ((size_t)L.floats * 4 > (size_t)optin) return cudaErrorNotSupported;
     smem = (size_t)optin;
   }
-  void (*fn)(SolveParams, TcLayout) = nullptr;
-  if (L.cps >= 2 && L.threads <= 288) {  // two CTAs per SM
+  // TMA staging of the next pair needs 16-byte row strides and a one-box panel-0 load
+  L.tma = (p.k % 4 == 0 && L.K16 <= 256 && std::getenv("FMAP_TC_NOTMA") == nullptr) ? 1 : 0;
+  CUtensorMap tmG, tmA;
+  std::memset(&tmG, 0, sizeof(tmG));
+  std::memset(&tmA, 0, sizeof(tmA));
+  if (L.tma) {
+    const int64_t npairs = (p.sys_offset + p.nsys + p.k - 1) / p.k;
+    if (encode_gram_map(&tmG, p.gram, p.k, npairs, kTL) != 0 || encode_gram_map(&tmA, p.gram, p.k, npairs, L.K16) != 0)
+      L.tma = 0;
+  }
+  void (*fn)(SolveParams, TcLayout, const CUtensorMap, const CUtensorMap) = nullptr;
+  if (L.ns == 2) {
+    if (L.threads <= 320) {
+      switch (mask_mode) {
+        case 0: fn = chol_tc_kernel<0, 2, 320, 1>; break;
+        case 1: fn = chol_tc_kernel<1, 2, 320, 1>; break;
+        default: fn = chol_tc_kernel<2, 2, 320, 1>; break;
+      }
+    } else {
+      switch (mask_mode) {
+        case 0: fn = chol_tc_kernel<0, 2, 384, 1>; break;
+        case 1: fn = chol_tc_kernel<1, 2, 384, 1>; break;
+        default: fn = chol_tc_kernel<2, 2, 384, 1>; break;
+      }
+    }
+  } else if (L.cps >= 2 && L.threads <= 288) {  // two CTAs per SM
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 288, 2>; break;
-      case 1: fn = chol_tc_kernel<1, 288, 2>; break;
-      default: fn = chol_tc_kernel<2, 288, 2>; break;
+      case 0: fn = chol_tc_kernel<0, 1, 288, 2>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 288, 2>; break;
+      default: fn = chol_tc_kernel<2, 1, 288, 2>; break;
     }
   } else {
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 384, 1>; break;
-      case 1: fn = chol_tc_kernel<1, 384, 1>; break;
-      default: fn = chol_tc_kernel<2, 384, 1>; break;
+      case 0: fn = chol_tc_kernel<0, 1, 384, 1>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 384, 1>; break;
+      default: fn = chol_tc_kernel<2, 1, 384, 1>; break;
     }
   }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  const int64_t npi = (p.nsys + L.ns - 1) / L.ns;
   const int64_t maxgrid = (int64_t)sms * L.cps;
-  const unsigned grid = (unsigned)(p.nsys < maxgrid ? p.nsys : maxgrid);
-  fn<<<grid, L.threads, smem, stream>>>(p, L);
+  const unsigned grid = (unsigned)(npi < maxgrid ? npi : maxgrid);
+  fn<<<grid, L.threads, smem, stream>>>(p, L, tmG, tmA);
   return cudaGetLastError();
 }
 

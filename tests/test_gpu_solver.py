@@ -184,3 +184,25 @@ def test_stacked_batch_equals_individual(fm, oracle):
     for q in range(3):
         single = fm.solve_host(G[q:q + 1], R[q:q + 1], M[q:q + 1], 100.0).maps[0]
         assert np.array_equal(batch[q], single)
+
+
+@pytest.mark.parametrize("env", [{}, {"FMAP_TC_NS": "2"}, {"FMAP_TC_NOTMA": "1"},
+                                 {"FMAP_TC_NS": "2", "FMAP_TC_NOTMA": "1"}],
+                         ids=["tma", "ns2-tma", "ldg", "ns2-ldg"])
+@pytest.mark.parametrize("k,b", [(200, 4), (40, 24), (64, 12), (36, 40)])
+def test_tensor_core_staging_variants(fm, oracle, monkeypatch, env, k, b):
+    # Enough systems for several per CTA (148 SMs x 2), so the next system's G is
+    # staged during the current one's panels (TMA + tcgen05.cp) — and the per-thread
+    # load path and the two-systems-per-CTA layout give the same answers.
+    for key, v in env.items():
+        monkeypatch.setenv(key, v)
+    G, R, M = _problems(oracle, b, k, 96, 300 + k)
+    lam = 100.0
+    out = fm.solve_host(G, R, M, lam)
+    sub = slice(0, 2)
+    _assert_parity(out.maps[sub], _ref(oracle, G[sub], R[sub], M[sub], lam), f"k={k} {env}")
+    assert _rel_residual(oracle, out.maps, G, R, M, lam) <= RES_REL
+    monkeypatch.delenv("FMAP_TC_NS", raising=False)
+    monkeypatch.delenv("FMAP_TC_NOTMA", raising=False)
+    base = fm.solve_host(G, R, M, lam).maps
+    assert np.array_equal(out.maps, base) or env.get("FMAP_TC_NS") == "2"
