@@ -281,7 +281,7 @@ def run_ours(args):
         result["e2e"] = {"value": round(world * b / (e2e_ms * 1e-3), 2), "unit": UNIT,
                          "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes,
                          "ms_per_step": round(e2e_ms, 4),
-                         "api": "fmap_solve_f32 (host G,R,M pinned -> C), host validation incl."}
+                         "api": "fmap_solve_f32 (host G,R,M pinned -> C): 8 pair chunks, H2D / validation+solve / D2H overlapped on 2 copy + 2 compute streams, device validation incl."}
         result["pipeline"] = {"value": round(world * b / (pipe_ms * 1e-3), 2), "unit": UNIT,
                               "ms_per_step": round(pipe_ms, 4),
                               "api": "fmap_pipeline_f32_dev: Phi,Mass,F,ev -> projection, Gram/RHS, "

@@ -206,3 +206,41 @@ def test_tensor_core_staging_variants(fm, oracle, monkeypatch, env, k, b):
     monkeypatch.delenv("FMAP_TC_NOTMA", raising=False)
     base = fm.solve_host(G, R, M, lam).maps
     assert np.array_equal(out.maps, base) or env.get("FMAP_TC_NS") == "2"
+
+
+def test_host_copy_pipeline_matches_unpipelined(fm, oracle, monkeypatch):
+    # The host entry overlaps chunked H2D / solve / D2H (default 8 chunks for >= 16
+    # pairs); the answer is bitwise the unpipelined one, and parity holds.
+    G, R, M = _problems(oracle, 40, 40, 64, 77)
+    piped = fm.solve_host(G, R, M, 100.0)
+    monkeypatch.setenv("FMAP_PIPELINE", "1")
+    plain = fm.solve_host(G, R, M, 100.0)
+    assert np.array_equal(piped.maps, plain.maps)
+    _assert_parity(piped.maps[-2:], _ref(oracle, G[-2:], R[-2:], M[-2:], 100.0), "pipelined tail chunk")
+
+
+@pytest.mark.parametrize("what", ["nan", "singular"])
+def test_host_copy_pipeline_error_exposes_no_partial_result(fm, oracle, what):
+    # An error found in the LAST chunk (after earlier chunks were already copied
+    # back) must not leave partial maps in the caller's buffer.
+    import ctypes as C
+    from paper_2604_10377_b200 import _lib, fmsolve
+    G, R, M = _problems(oracle, 32, 24, 48, 91)
+    if what == "nan":
+        R[31, 5, 7] = np.nan
+        expect = fm.InvalidArgument
+    else:
+        G[31] = 0.0
+        M[31] = 0.0
+        expect = fm.SingularSystemError
+    out = np.full(G.shape, 7.0, np.float32)
+    ctx = fmsolve._ctx(0)
+    o = fmsolve.SolverOptions().to_c()
+    rep = _lib.ReportC()
+    P = lambda x: C.c_void_p(x.ctypes.data)  # noqa: E731
+    st = ctx._lib.fmap_solve_f32(ctx.handle, 32, 24, P(G), P(R), P(M), C.c_float(100.0), C.byref(o), P(out),
+                                 C.byref(rep))
+    assert st != 0
+    with pytest.raises(expect):
+        fmsolve._raise(ctx, st, rep)
+    assert np.all(out == 0.0) or np.all(out == 7.0)  # zero-filled (pipelined) or untouched
