@@ -418,8 +418,218 @@ def run_reference(args):
            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
+# ------------------------------------------------- fmbench-compatible CSVs --
+# `python bench.py --fmbench bench|verify|memory [reference fmbench options]`
+# restates the reference harness (proj/src/bench.cpp:62-209, 298-346; CLI
+# tools/fmbench.cpp:36-68; defaults bench.hpp:20-36) with the GPU route added:
+# every k gets the reference's rowwise / batched rows (the CPU restatement in
+# oracle/, the reference leg of this file) plus a `cuda` row timed through the
+# host C ABI (fmap_solve_f32: H2D + validation + solve + D2H, wall clock), in
+# the reference's CSV schema (tests/golden/bench_columns.txt).  The cuda route
+# computes in f32; with --precision f64 its diffs are against the f64 rows.
+FMBENCH_COLUMNS = "k,solver,median_ms,max_abs_diff_vs_rowwise,peak_extra_bytes,speedup_vs_rowwise,flag"
+
+
+def _fmbench_args(mode, argv):
+    ap = argparse.ArgumentParser(prog=f"bench.py --fmbench {mode}")
+    ap.add_argument("--k-start", type=int, default=20)
+    ap.add_argument("--k-stop", type=int, default=300)
+    ap.add_argument("--k-step", type=int, default=10)
+    ap.add_argument("--d", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--lambda", dest="lam", type=float, default=100.0)
+    ap.add_argument("--mask", choices=["comm", "resolvent"], default="comm")
+    ap.add_argument("--sigma", type=float, default=0.5)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--precision", choices=["f32", "f64"], default="f64")
+    ap.add_argument("--mem-cap-bytes", type=int, default=1 << 30)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--inject-fault", action="store_true")
+    ap.add_argument("--out")
+    return ap.parse_args(argv)
+
+
+def _fmbench_validate(a):
+    """bench.cpp:230-240 (BenchConfig::validate)."""
+    for ok, msg in ((a.k_start >= 1, "k-start must be at least 1"),
+                    (a.k_start <= a.k_stop, "k-start must not exceed k-stop"),
+                    (a.k_step >= 1, "k-step must be at least 1"),
+                    (a.d >= 0, "d must be non-negative (0 means 2k)"),
+                    (a.batch >= 1, "batch must be at least 1"),
+                    (a.lam >= 0.0, "lambda must be non-negative"),
+                    (a.sigma > 0.0, "sigma must be positive"),
+                    (a.reps >= 1, "repetitions must be at least 1"),
+                    (a.warmup >= 0, "warmup must be non-negative")):
+        if not ok:
+            raise ValueError(msg)
+
+
+def _fmbench_describe(a):
+    d = str(a.d) if a.d > 0 else "2k"
+    s = f"k={a.k_start}..{a.k_stop} step {a.k_step}, d={d}, batch={a.batch}, lambda={a.lam:g}, mask=" + \
+        ("commutativity" if a.mask == "comm" else "resolvent")
+    if a.mask == "resolvent":
+        s += f", sigma={a.sigma:g}"
+    return s + f", precision={a.precision}, seed={a.seed}"
+
+
+def _fmbench_problems(oracle, a, k):
+    """bench.cpp:30-41: one generate_instance per pair, seed + q."""
+    d = a.d if a.d > 0 else 2 * k
+    kind = 0 if a.mask == "comm" else 1
+    Gs, Rs, Ms = [], [], []
+    for q in range(a.batch):
+        G, R, M, _, _ = oracle.random_problem(k, d, a.seed + q, kind=kind, sigma=a.sigma)
+        Gs.append(G)
+        Rs.append(R)
+        Ms.append(M)
+    return np.stack(Gs), np.stack(Rs), np.stack(Ms)
+
+
+def _fmt(x, digits):
+    if x is None or (isinstance(x, float) and x != x):
+        return ""
+    return f"{x:.{digits}g}"
+
+
+def run_fmbench(mode, argv) -> int:
+    import oracle
+    import paper_2604_10377_b200 as fm
+    a = _fmbench_args(mode, argv)
+    out = open(a.out, "w") if a.out else sys.stdout
+    dt = np.float64 if a.precision == "f64" else np.float32
+    digits = 17 if a.precision == "f64" else 9
+    tol = 1e-8 if a.precision == "f64" else 1e-3       # bench.cpp:28
+    tol_cuda = 1e-3                                     # the cuda route computes in f32
+    esize = 8 if a.precision == "f64" else 4
+    threads = a.threads or oracle.hardware_threads()
+    cuda_opts = lambda fault: fm.SolverOptions(memory_cap_bytes=a.mem_cap_bytes, threads=a.threads,  # noqa: E731
+                                               inject_fault=fault)
+    rc = 0
+    try:
+        _fmbench_validate(a)
+        ks = list(range(a.k_start, a.k_stop + 1, a.k_step))
+        if mode == "bench":
+            print("# functional-map solver benchmark", file=out)
+            print(f"# config: {_fmbench_describe(a)}", file=out)
+            print(f"# timing: wall clock; median of {a.reps} repetitions after {a.warmup} warmup runs per solver",
+                  file=out)
+            print("# timed region: rowwise / batched = the reference routes (CPU restatement, oracle/): per-system "
+                  "assembly + factorization + solve; cuda = fmap_solve_f32 on host buffers (H2D, device validation, "
+                  "tcgen05/TMEM Cholesky solve, D2H) on one B200", file=out)
+            print(f"# batched dispatch: {threads} worker thread(s); cuda: one launch per batch", file=out)
+            print(FMBENCH_COLUMNS, file=out)
+            for k in ks:
+                G, R, M = _fmbench_problems(oracle, a, k)
+                G, R, M = G.astype(dt), R.astype(dt), M.astype(dt)
+                G32, R32, M32 = (x.astype(np.float32) for x in (G, R, M))
+
+                def timed(fn):
+                    ms, last = [], None
+                    for rep in range(a.warmup + a.reps):
+                        t0 = time.perf_counter()
+                        last = fn()
+                        if rep >= a.warmup:
+                            ms.append((time.perf_counter() - t0) * 1e3)
+                    return statistics.median(ms), last
+
+                rw_ms, rw = timed(lambda: oracle.solve(G, R, M, a.lam, route="rowwise", dtype=dt, threads=a.threads))
+                print(f"{k},rowwise,{_fmt(rw_ms, digits)},0,{rw.peak_extra_bytes},1,ok", file=out)
+                bbytes = a.batch * k ** 3 * esize
+                if bbytes <= a.mem_cap_bytes:
+                    bt_ms, bt = timed(lambda: oracle.solve(G, R, M, a.lam, route="batched", dtype=dt,
+                                                           threads=a.threads))
+                    diff = float(np.abs(bt.maps.astype(np.float64) - rw.maps).max())
+                    print(f"{k},batched,{_fmt(bt_ms, digits)},{_fmt(diff, digits)},{bbytes},"
+                          f"{_fmt(rw_ms / bt_ms, digits)},ok", file=out)
+                else:
+                    print(f"{k},batched,,,{bbytes},,mem-cap-skipped", file=out)
+                try:
+                    cu_ms, cu = timed(lambda: fm.solve_host(G32, R32, M32, a.lam, cuda_opts(False)))
+                    diff = float(np.abs(cu.maps.astype(np.float64) - rw.maps).max())
+                    print(f"{k},cuda,{_fmt(cu_ms, digits)},{_fmt(diff, digits)},{cu.peak_extra_bytes},"
+                          f"{_fmt(rw_ms / cu_ms, digits)},ok", file=out)
+                except fm.MemoryCapExceeded as e:
+                    print(f"{k},cuda,,,{getattr(e, 'required_bytes', '')},,mem-cap-skipped", file=out)
+        elif mode == "verify":
+            print("verify: rowwise vs batched vs cuda" + (" vs full oracle (k <= 32)" if a.k_start <= 32 else ""),
+                  file=out)
+            print("  " + _fmbench_describe(a), file=out)
+            ok = True
+            for k in ks:
+                G, R, M = _fmbench_problems(oracle, a, k)
+                G, R, M = G.astype(dt), R.astype(dt), M.astype(dt)
+                rw = oracle.solve(G, R, M, a.lam, route="rowwise", dtype=dt, threads=a.threads)
+                bt = oracle.solve(G, R, M, a.lam, route="batched", dtype=dt, threads=a.threads,
+                                  inject_fault=a.inject_fault)
+                cu = fm.solve_host(*(x.astype(np.float32) for x in (G, R, M)), a.lam, cuda_opts(a.inject_fault))
+                d_rb = float(np.abs(rw.maps - bt.maps).max())
+                d_rc = float(np.abs(rw.maps.astype(np.float64) - cu.maps).max())
+                line = f"  k={k}  rowwise~batched={d_rb:.3g}  rowwise~cuda={d_rc:.3g}"
+                worst, worst_c = d_rb, d_rc
+                if k <= 32:
+                    full = np.stack([oracle.solve_full(G[q], R[q], M[q], a.lam, dtype=dt) for q in range(a.batch)])
+                    d_ro = float(np.abs(rw.maps - full).max())
+                    d_bo = float(np.abs(bt.maps - full).max())
+                    d_co = float(np.abs(cu.maps.astype(np.float64) - full).max())
+                    line += f"  rowwise~oracle={d_ro:.3g}  batched~oracle={d_bo:.3g}  cuda~oracle={d_co:.3g}"
+                    worst = max(worst, d_ro, d_bo)
+                    worst_c = max(worst_c, d_co)
+                rhs_norm = max(float(np.linalg.norm(R[q])) for q in range(a.batch))
+                res = max(rw.max_residual, bt.max_residual, cu.max_residual_norm)
+                line += f"  residual={res:.3g} (bound {tol_cuda * (1.0 + rhs_norm):.3g})"
+                print(line, file=out)
+                if not (worst <= tol) or not (worst_c <= tol_cuda):
+                    ok = False
+            if ok:
+                print(f"verify: PASS (all pairwise diffs <= {tol:.3g}; cuda (f32) <= {tol_cuda:.3g})", file=out)
+            else:
+                print(f"verify: FAIL (a pairwise diff exceeded {tol:.3g} / cuda {tol_cuda:.3g})", file=out)
+                rc = 1
+        elif mode == "memory":
+            print("# transient allocation model: batched extra = batch*k^3*elemsize, loop working set = "
+                  "batch*k^2*elemsize, ratio = k; cuda = device scratch + staging the GPU route reserves", file=out)
+            print(f"# config: {_fmbench_describe(a)}", file=out)
+            print(f"# rows at or under the memory cap ({a.mem_cap_bytes} bytes) are cross-checked against "
+                  "solver-reported peak_extra_bytes", file=out)
+            print("k,precision,batched_extra_bytes,loop_working_set_bytes,ratio,cuda_peak_extra_bytes", file=out)
+            for k in ks:
+                bb, lw = a.batch * k ** 3 * esize, a.batch * k * k * esize
+                cu_b = ""
+                if bb <= a.mem_cap_bytes:
+                    G, R, M = _fmbench_problems(oracle, a, k)
+                    G, R, M = G.astype(dt), R.astype(dt), M.astype(dt)
+                    rw = oracle.solve(G, R, M, a.lam, route="rowwise", dtype=dt, threads=a.threads)
+                    bt = oracle.solve(G, R, M, a.lam, route="batched", dtype=dt, threads=a.threads)
+                    if rw.peak_extra_bytes != lw or bt.peak_extra_bytes != bb:
+                        raise RuntimeError(f"memory model mismatch at k={k}: solver reported loop="
+                                           f"{rw.peak_extra_bytes} batched={bt.peak_extra_bytes}, model says "
+                                           f"loop={lw} batched={bb}")
+                    cu_b = fm.solve_host(*(x.astype(np.float32) for x in (G, R, M)), a.lam,
+                                         cuda_opts(False)).peak_extra_bytes
+                print(f"{k},{a.precision},{bb},{lw},{k},{cu_b}", file=out)
+        else:
+            raise ValueError(f"unknown fmbench mode {mode!r} (bench | verify | memory)")
+    except Exception as e:  # noqa: BLE001 — the reference prints the error into the report
+        if mode == "verify":
+            print(f"verify: ERROR at {e}", file=out)
+        else:
+            print(f"# {mode}: ERROR {e}", file=out)
+        rc = 2
+    finally:
+        if a.out:
+            out.close()
+    return rc
+
+
 
 def main():
+    if "--fmbench" in sys.argv:
+        i = sys.argv.index("--fmbench")
+        mode = sys.argv[i + 1] if i + 1 < len(sys.argv) else ""
+        sys.exit(run_fmbench(mode, sys.argv[1:i] + sys.argv[i + 2:]))
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
