@@ -272,10 +272,11 @@ def run_ours(args):
     # e2e + pipeline: each rank measures its own, max over ranks
     e2e_ms = _e2e(args, cfg, G, R, M, device, ctx, stream)
     pipe_ms = _pipeline(args, cfg, t, device, stream)
+    f64_ms = _f64_route(args, cfg, G, R, M, device, ctx, stream)
     if world > 1:
-        tt = torch.tensor([e2e_ms, pipe_ms], device=device, dtype=torch.float64)
+        tt = torch.tensor([e2e_ms, pipe_ms, f64_ms], device=device, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms, pipe_ms = (float(x) for x in tt.tolist())
+        e2e_ms, pipe_ms, f64_ms = (float(x) for x in tt.tolist())
     if rank == 0:
         nbytes = b * k * k * 4
         result["e2e"] = {"value": round(world * b / (e2e_ms * 1e-3), 2), "unit": UNIT,
@@ -286,6 +287,10 @@ def run_ours(args):
                               "ms_per_step": round(pipe_ms, 4),
                               "api": "fmap_pipeline_f32_dev: Phi,Mass,F,ev -> projection, Gram/RHS, "
                                      "fused resolvent mask, solver (device-resident)"}
+        result["f64_route"] = {"value": round(world * b / (f64_ms * 1e-3), 2), "unit": UNIT,
+                               "ms_per_step": round(f64_ms, 4), "dtype": "f64",
+                               "api": "fmap_solve_f64_dev (the reference's default precision; same "
+                                      "device-resident G, R, M in f64, validation + solve)"}
         if not args.no_cpu_baseline and world == 1:
             result["cpu_baseline"] = _cpu_baseline(args, G, R, M, k, cfg.lam)
         print(json.dumps(result), flush=True)
@@ -358,6 +363,36 @@ def _pipeline(args, cfg, t, device, stream) -> float:
     return e0.elapsed_time(e1) / steps
 
 
+def _f64_route(args, cfg, G, R, M, device, ctx, stream) -> float:
+    """Same step on the f64 route (inputs converted once, outside the timing)."""
+    import torch
+    import ctypes as C
+    from paper_2604_10377_b200 import fmsolve, _lib
+    b, k = cfg.batch, cfg.k
+    G64, R64, M64 = (x.double().contiguous() for x in (G, R, M))
+    C64 = torch.empty_like(G64)
+    opts = fmsolve.SolverOptions(compute_residual=False, rcond_threshold=-1.0).to_c()
+    P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+
+    def run():
+        rep = _lib.ReportC()
+        st = ctx._lib.fmap_solve_f64_dev(ctx.handle, b, k, P(G64), P(R64), P(M64), cfg.lam, C.byref(opts), P(C64),
+                                         C.byref(rep))
+        if st != 0:
+            raise RuntimeError(ctx.last_error())
+
+    torch.cuda.synchronize(device)
+    for _ in range(2):
+        run()
+    steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run()
+    torch.cuda.synchronize(device)
+    return (time.perf_counter() - t0) * 1e3 / steps
+
+
 def _cpu_baseline(args, G, R, M, k, lam) -> dict:
     """Oracle (restated reference batched route, all host threads) on a bounded
     sample of the same inputs; plus the serial rowwise route on a smaller one."""
@@ -426,7 +461,8 @@ def run_reference(args):
 # oracle/, the reference leg of this file) plus a `cuda` row timed through the
 # host C ABI (fmap_solve_f32: H2D + validation + solve + D2H, wall clock), in
 # the reference's CSV schema (tests/golden/bench_columns.txt).  The cuda route
-# computes in f32; with --precision f64 its diffs are against the f64 rows.
+# runs in the harness precision (f32: tcgen05 route, f64: fmap_solve_f64) and is
+# held to the same tolerance (bench.cpp:28).
 FMBENCH_COLUMNS = "k,solver,median_ms,max_abs_diff_vs_rowwise,peak_extra_bytes,speedup_vs_rowwise,flag"
 
 
@@ -502,7 +538,7 @@ def run_fmbench(mode, argv) -> int:
     dt = np.float64 if a.precision == "f64" else np.float32
     digits = 17 if a.precision == "f64" else 9
     tol = 1e-8 if a.precision == "f64" else 1e-3       # bench.cpp:28
-    tol_cuda = 1e-3                                     # the cuda route computes in f32
+    tol_cuda = tol                                      # the cuda route runs in the same precision
     esize = 8 if a.precision == "f64" else 4
     threads = a.threads or oracle.hardware_threads()
     cuda_opts = lambda fault: fm.SolverOptions(memory_cap_bytes=a.mem_cap_bytes, threads=a.threads,  # noqa: E731
@@ -524,7 +560,6 @@ def run_fmbench(mode, argv) -> int:
             for k in ks:
                 G, R, M = _fmbench_problems(oracle, a, k)
                 G, R, M = G.astype(dt), R.astype(dt), M.astype(dt)
-                G32, R32, M32 = (x.astype(np.float32) for x in (G, R, M))
 
                 def timed(fn):
                     ms, last = [], None
@@ -547,12 +582,14 @@ def run_fmbench(mode, argv) -> int:
                 else:
                     print(f"{k},batched,,,{bbytes},,mem-cap-skipped", file=out)
                 try:
-                    cu_ms, cu = timed(lambda: fm.solve_host(G32, R32, M32, a.lam, cuda_opts(False)))
+                    cu_ms, cu = timed(lambda: fm.solve_host(G, R, M, a.lam, cuda_opts(False), precision=a.precision))
                     diff = float(np.abs(cu.maps.astype(np.float64) - rw.maps).max())
                     print(f"{k},cuda,{_fmt(cu_ms, digits)},{_fmt(diff, digits)},{cu.peak_extra_bytes},"
                           f"{_fmt(rw_ms / cu_ms, digits)},ok", file=out)
                 except fm.MemoryCapExceeded as e:
                     print(f"{k},cuda,,,{getattr(e, 'required_bytes', '')},,mem-cap-skipped", file=out)
+                except fm.InvalidArgument:  # beyond the route's single-CTA resolution limit
+                    print(f"{k},cuda,,,,,k-limit-skipped", file=out)
         elif mode == "verify":
             print("verify: rowwise vs batched vs cuda" + (" vs full oracle (k <= 32)" if a.k_start <= 32 else ""),
                   file=out)
@@ -564,7 +601,7 @@ def run_fmbench(mode, argv) -> int:
                 rw = oracle.solve(G, R, M, a.lam, route="rowwise", dtype=dt, threads=a.threads)
                 bt = oracle.solve(G, R, M, a.lam, route="batched", dtype=dt, threads=a.threads,
                                   inject_fault=a.inject_fault)
-                cu = fm.solve_host(*(x.astype(np.float32) for x in (G, R, M)), a.lam, cuda_opts(a.inject_fault))
+                cu = fm.solve_host(G, R, M, a.lam, cuda_opts(a.inject_fault), precision=a.precision)
                 d_rb = float(np.abs(rw.maps - bt.maps).max())
                 d_rc = float(np.abs(rw.maps.astype(np.float64) - cu.maps).max())
                 line = f"  k={k}  rowwise~batched={d_rb:.3g}  rowwise~cuda={d_rc:.3g}"
@@ -584,9 +621,9 @@ def run_fmbench(mode, argv) -> int:
                 if not (worst <= tol) or not (worst_c <= tol_cuda):
                     ok = False
             if ok:
-                print(f"verify: PASS (all pairwise diffs <= {tol:.3g}; cuda (f32) <= {tol_cuda:.3g})", file=out)
+                print(f"verify: PASS (all pairwise diffs <= {tol:.3g})", file=out)
             else:
-                print(f"verify: FAIL (a pairwise diff exceeded {tol:.3g} / cuda {tol_cuda:.3g})", file=out)
+                print(f"verify: FAIL (a pairwise diff exceeded {tol:.3g})", file=out)
                 rc = 1
         elif mode == "memory":
             print("# transient allocation model: batched extra = batch*k^3*elemsize, loop working set = "
@@ -607,8 +644,7 @@ def run_fmbench(mode, argv) -> int:
                         raise RuntimeError(f"memory model mismatch at k={k}: solver reported loop="
                                            f"{rw.peak_extra_bytes} batched={bt.peak_extra_bytes}, model says "
                                            f"loop={lw} batched={bb}")
-                    cu_b = fm.solve_host(*(x.astype(np.float32) for x in (G, R, M)), a.lam,
-                                         cuda_opts(False)).peak_extra_bytes
+                    cu_b = fm.solve_host(G, R, M, a.lam, cuda_opts(False), precision=a.precision).peak_extra_bytes
                 print(f"{k},{a.precision},{bb},{lw},{k},{cu_b}", file=out)
         else:
             raise ValueError(f"unknown fmbench mode {mode!r} (bench | verify | memory)")

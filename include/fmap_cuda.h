@@ -89,6 +89,18 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
                    const float* mask, float lambda, const fmap_solver_options* opts,
                    float* C_out, fmap_report* report);
 
+/* Replaces solve_batched_many<double> (solver.hpp:225-322), the reference's
+ * default precision (bench.hpp:32): f64 end to end, rcond threshold 1e-14 when
+ * opts->rcond_threshold < 0 (solver.hpp:18-27), explicit mask only, k up to the
+ * single-CTA shared-memory limit (234 on B200; larger k -> INVALID_ARGUMENT).
+ * Same validation / SINGULAR / memory-cap / fault-hook contract as f32. */
+int fmap_solve_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* gram, const double* rhs,
+                   const double* mask, double lambda, const fmap_solver_options* opts,
+                   double* C_out, fmap_report* report);
+int fmap_solve_f64_dev(fmap_ctx* ctx, int64_t b, int64_t k, const double* d_gram,
+                       const double* d_rhs, const double* d_mask, double lambda,
+                       const fmap_solver_options* opts, double* d_C_out, fmap_report* report);
+
 /* Same contract on DEVICE pointers (inputs already resident in HBM). */
 int fmap_solve_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gram,
                        const float* d_rhs, const float* d_mask, float lambda,

@@ -31,7 +31,7 @@ EXPORTED = [
     "fmap_solve_ev_f32_dev", "fmap_mask_f32", "fmap_mask_f32_dev",
     "fmap_normal_equations_f32", "fmap_normal_equations_f32_dev", "fmap_project_f32_dev",
     "fmap_residual_f32_dev", "fmap_pipeline_f32_dev", "fmap_max_resolution",
-    "fmap_last_launch_count",
+    "fmap_last_launch_count", "fmap_solve_f64", "fmap_solve_f64_dev",
 ]
 
 
@@ -85,6 +85,8 @@ def load() -> C.CDLL:
             "fmap_default_options": (None, [opt]),
             "fmap_solve_f32": (I, [P, I64, I64, P, P, P, F, opt, P, rep]),
             "fmap_solve_f32_dev": (I, [P, I64, I64, P, P, P, F, opt, P, rep]),
+            "fmap_solve_f64": (I, [P, I64, I64, P, P, P, C.c_double, opt, P, rep]),
+            "fmap_solve_f64_dev": (I, [P, I64, I64, P, P, P, C.c_double, opt, P, rep]),
             "fmap_solve_ev_f32_dev": (I, [P, I64, I64, P, P, P, P, I, F, F, opt, P, rep]),
             "fmap_mask_f32": (I, [P, I64, I64, P, P, I, F, P]),
             "fmap_mask_f32_dev": (I, [P, I64, I64, P, P, I, F, P]),

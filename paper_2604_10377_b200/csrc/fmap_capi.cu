@@ -477,6 +477,105 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   return FMAP_OK;
 }
 
+
+// f64 route (fmap_f64.cu): same contract as solve_core for an explicit mask.
+int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const double* R, const double* M,
+                   double lambda, const fmap_solver_options* o, double* C, fmap_report* rep,
+                   size_t host_staging_bytes) {
+  fmap_solver_options opts;
+  default_opts(&opts);
+  if (o) opts = *o;
+  init_report(rep);
+  if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
+  if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
+  if (!(lambda >= 0.0)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "lambda must be non-negative");
+  if (!G || !R || !M || !C) return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
+  if (chol_f64_smem_bytes((int)k) > (size_t)ctx->max_smem_optin) {
+    int kmax = 1;
+    while (chol_f64_smem_bytes(kmax + 1) <= (size_t)ctx->max_smem_optin) ++kmax;
+    return set_err(ctx, FMAP_INVALID_ARGUMENT,
+                   "k = " + std::to_string(k) + " exceeds the f64 route's single-CTA limit " + std::to_string(kmax) +
+                       " on this device");
+  }
+  const size_t kk = (size_t)k * k;
+  const size_t scratch = carve_size({(size_t)b * sizeof(double), (size_t)k * sizeof(double)});
+  const uint64_t required = (uint64_t)scratch + host_staging_bytes;
+  if (rep) rep->peak_extra_bytes = required;
+  if (opts.has_memory_cap && required > opts.memory_cap_bytes) {
+    if (rep) {
+      rep->required_bytes = required;
+      rep->cap_bytes = opts.memory_cap_bytes;
+    }
+    return set_err(ctx, FMAP_MEMORY_CAP,
+                   "cuda route needs " + std::to_string(required) + " bytes of device scratch, above the cap of " +
+                       std::to_string(opts.memory_cap_bytes));
+  }
+  int st = arena_reserve(ctx, scratch + host_staging_bytes);
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena) + host_staging_bytes};
+  double* sq = cv.take<double>((size_t)b);
+  double* zrow = cv.take<double>((size_t)k);
+  if ((st = reset_ctrl(ctx))) return st;
+  ctx->launches = 0;
+  FMAP_CK(ctx, launch_validate_f64(G, R, M, (size_t)b * kk, d_flags(ctx), ctx->stream));
+  const double rthr = opts.rcond_threshold < 0.f ? 1e-14 : (double)opts.rcond_threshold;
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  FMAP_CK(ctx, launch_chol_f64(G, R, M, C, (int)k, b * k, lambda, (double)opts.ridge, rthr, -1, d_fail(ctx),
+                               d_rcond(ctx), ctx->stream));
+  ctx->launches += 2;
+  if (opts.inject_fault) {  // solver.hpp:269-273, as solve_core
+    std::vector<double> g0(k);
+    double m00 = 0.0;
+    FMAP_CK(ctx, cudaMemcpyAsync(g0.data(), G, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FMAP_CK(ctx, cudaMemcpyAsync(&m00, M, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    g0[0] += lambda * m00 + (double)opts.ridge;
+    int w = 0;
+    double best = -1.0;
+    for (int64_t c = 0; c < k; ++c)
+      if (std::fabs(g0[c]) > best) {
+        best = std::fabs(g0[c]);
+        w = (int)c;
+      }
+    const double alpha = -2.0 * g0[w];
+    FMAP_CK(ctx, launch_chol_f64(G, R, M, zrow, (int)k, 1, lambda, (double)opts.ridge, rthr, 0, d_fail(ctx),
+                                 d_rcond(ctx), ctx->stream));
+    FMAP_CK(ctx, launch_fault_combine_f64(C, zrow, (int)k, w, alpha, d_fail(ctx), ctx->stream));
+    ctx->launches += 2;
+  }
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  if (opts.compute_residual) {
+    FMAP_CK(ctx, launch_residual_f64(C, G, R, M, b, (int)k, lambda, sq, ctx->stream));
+    ctx->launches++;
+  }
+  unsigned long long fail;
+  float rcond;
+  unsigned flags;
+  if ((st = read_ctrl(ctx, &fail, &rcond, &flags))) return st;
+  float ms = 0.f;
+  FMAP_CK(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (rep) {
+    rep->wall_seconds = ms * 1e-3;
+    rep->min_rcond = rcond;
+  }
+  if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, flags_message(flags));
+  if (fail != kNoFail) {
+    if (rep) rep->failing_system = (int64_t)fail;
+    return set_err(ctx, FMAP_SINGULAR,
+                   "row system " + std::to_string(fail) +
+                       " is numerically singular (Cholesky pivot / rcond estimate / non-finite solution)");
+  }
+  if (opts.compute_residual && rep) {
+    std::vector<double> res(b);
+    FMAP_CK(ctx, cudaMemcpy(res.data(), sq, b * sizeof(double), cudaMemcpyDeviceToHost));
+    double mx = 0.0;
+    for (double v : res) mx = std::max(mx, std::sqrt(v));
+    rep->max_residual = mx;
+  }
+  ctx->last_error.clear();
+  return FMAP_OK;
+}
+
 bool host_finite(const float* p, size_t n) {
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) return false;
@@ -621,6 +720,53 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   FMAP_CK(ctx, cudaMemcpyAsync(dM, mask, bytes, cudaMemcpyHostToDevice, ctx->stream));
   st = solve_core(ctx, b, k, dG, dR, dM, nullptr, nullptr, 0, 0.f, lambda, &o, dC, report, true,
                   staging);
+  if (st) return st;
+  FMAP_CK(ctx, cudaMemcpyAsync(C_out, dC, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMAP_OK;
+}
+
+int fmap_solve_f64_dev(fmap_ctx* ctx, int64_t b, int64_t k, const double* d_gram, const double* d_rhs,
+                       const double* d_mask, double lambda, const fmap_solver_options* opts, double* d_C_out,
+                       fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  return solve_core_f64(ctx, b, k, d_gram, d_rhs, d_mask, lambda, opts, d_C_out, report, 0);
+}
+
+int fmap_solve_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* gram, const double* rhs, const double* mask,
+                   double lambda, const fmap_solver_options* opts, double* C_out, fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  init_report(report);
+  if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
+  if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
+  if (!gram || !rhs || !mask || !C_out) return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
+  if (!(lambda >= 0.0)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "lambda must be non-negative");
+  const size_t bytes = (size_t)b * k * k * sizeof(double);
+  const size_t staging = carve_size({bytes, bytes, bytes, bytes});
+  fmap_solver_options o;
+  default_opts(&o);
+  if (opts) o = *opts;
+  if (o.has_memory_cap && staging > o.memory_cap_bytes) {
+    if (report) {
+      report->required_bytes = staging;
+      report->cap_bytes = o.memory_cap_bytes;
+      report->peak_extra_bytes = staging;
+    }
+    return set_err(ctx, FMAP_MEMORY_CAP,
+                   "cuda route needs " + std::to_string(staging) + " bytes of device staging, above the cap of " +
+                       std::to_string(o.memory_cap_bytes));
+  }
+  int st = arena_reserve(ctx, staging + (1u << 20));
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  double* dG = cv.take<double>((size_t)b * k * k);
+  double* dR = cv.take<double>((size_t)b * k * k);
+  double* dM = cv.take<double>((size_t)b * k * k);
+  double* dC = cv.take<double>((size_t)b * k * k);
+  FMAP_CK(ctx, cudaMemcpyAsync(dG, gram, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(dR, rhs, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(dM, mask, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  st = solve_core_f64(ctx, b, k, dG, dR, dM, lambda, &o, dC, report, staging);
   if (st) return st;
   FMAP_CK(ctx, cudaMemcpyAsync(C_out, dC, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));

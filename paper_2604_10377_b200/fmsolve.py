@@ -260,8 +260,30 @@ def solve_cuda_many(problems: Sequence[RegularizedProblem], lam: float,
 
 
 def solve_host(G: np.ndarray, R: np.ndarray, M: np.ndarray, lam: float,
-               opts: Optional[SolverOptions] = None, device: int = 0) -> BatchSolveReport:
-    """Host-buffer batched entry: G, R, M are [b, k, k] arrays -> maps [b, k, k]."""
+               opts: Optional[SolverOptions] = None, device: int = 0,
+               precision: str = "f32") -> BatchSolveReport:
+    """Host-buffer batched entry: G, R, M are [b, k, k] arrays -> maps [b, k, k].
+
+    precision "f64" selects the f64 route (fmap_solve_f64: the reference's default
+    Scalar = double, rcond threshold 1e-14 unless opts sets one)."""
+    if precision == "f64":
+        opts = opts or SolverOptions(rcond_threshold=-1.0)
+        G, R, M = (np.ascontiguousarray(x, dtype=np.float64) for x in (G, R, M))
+        _require(G.ndim == 3 and G.shape == R.shape == M.shape and G.shape[1] == G.shape[2],
+                 "gram, rhs and mask must be [b, k, k]")
+        b, k, _ = G.shape
+        out = np.empty((b, k, k), np.float64)
+        rep = _lib.ReportC()
+        o = opts.to_c()
+        if opts.rcond_threshold == default_rcond_threshold():
+            o.rcond_threshold = -1.0  # the f32 default was not chosen for f64: use the f64 one (1e-14)
+        ctx = _ctx(device)
+        st = ctx._lib.fmap_solve_f64(ctx.handle, b, k, _ptr(G), _ptr(R), _ptr(M), float(lam), C.byref(o),
+                                     _ptr(out), C.byref(rep))
+        _raise(ctx, st, rep)
+        return BatchSolveReport(out, rep.max_residual, timedelta(seconds=rep.wall_seconds),
+                                int(rep.peak_extra_bytes), rep.min_rcond)
+    _require(precision == "f32", "precision must be 'f32' or 'f64'")
     opts = opts or SolverOptions()
     G, R, M = _f32(G), _f32(R), _f32(M)
     _require(G.ndim == 3 and G.shape == R.shape == M.shape and G.shape[1] == G.shape[2],
