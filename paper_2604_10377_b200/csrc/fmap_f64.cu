@@ -7,19 +7,20 @@
 // (/root/reference/proj/include/fmsolve/solver.hpp:147-170) inside
 // solve_batched_many<double> (:220-322); SPD by construction, so Cholesky.
 //
-// One CTA owns one system at a time (persistent over systems, one CTA per SM:
-// the packed lower triangle of a k = 200 system is 160 KB of shared memory):
+// One CTA (1024 threads) owns one system at a time (persistent over systems, one
+// CTA per SM: the packed lower triangle of a k = 200 system is 160 KB of shared
+// memory):
 //   * staging: row r of G (contiguous, coalesced across the warp's lanes) into
 //     the packed row-major lower triangle, lambda*m + ridge on the diagonal;
-//   * right-looking Cholesky, one column per step: the pivot's column is scaled
-//     into a contiguous vector (forward substitution of the right-hand side rides
-//     along), then the rank-1 trailing update with one warp per row (lanes over
-//     the row's contiguous columns);
+//   * blocked right-looking Cholesky, 8-column panels: warp 0 factors the 8x8
+//     diagonal block (and the panel's forward substitution), every row below
+//     solves its L21 entries against L11, then the trailing rank-8 update runs on
+//     the FP64 tensor path (DMMA, mma.sync m8n8k4 f64) — B200's SIMT FP64 pipe
+//     is vestigial (~1.2 TFLOP/s measured), the tensor path is not;
 //   * back substitution L^T x = y column-oriented (row j of L is contiguous).
-// FP64 on the SIMT pipe (no tcgen05 FP64 MMA); bound: the 2 barriers per column
-// on the per-system chain, not FLOPs.  Verdict as the f32 route: non-positive /
-// non-finite pivot, rcond estimate min(pivot)/max|diag| below the threshold, or a
-// non-finite solution; lowest failing global system index wins.
+// Verdict as the f32 route: non-positive / non-finite pivot, rcond estimate
+// min(pivot)/max|diag| below the threshold, or a non-finite solution; lowest
+// failing global system index wins.
 #include "fmap_solver.cuh"
 
 #include <cuda_runtime.h>
@@ -46,14 +47,14 @@ __global__ void __launch_bounds__(kT64, 1)
   extern __shared__ __align__(16) double sm64[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kT64 / 32;
+  constexpr int NB = 8;  // panel width
   double* A = sm64;                                    // padded packed lower triangle
-  double* col = A + ((packed_doubles(k) + 1) & ~(size_t)1);  // current column of L (+ zero pads)
-  double* y = col + ((k + 3) & ~1);                    // right-hand side -> partially eliminated
-  double* yy = y + k;                                  // y = L^{-1} r (final values)
+  double* y = A + ((packed_doubles(k) + 1) & ~(size_t)1);  // right-hand side -> y = L^{-1} r
+  double* yy = y + ((k + 3) & ~1);                     // final forward values
   double* xs = yy + k;                                 // back substitution work vector
   double* invd = xs + k;                               // 1 / L_jj
   __shared__ double red[NW];
-  __shared__ double s_inv[2], s_yj[2];
+  __shared__ double s_piv;
   __shared__ int sbad;
 
   for (int64_t sys = blockIdx.x; sys < nsys; sys += gridDim.x) {
@@ -74,7 +75,6 @@ __global__ void __launch_bounds__(kT64, 1)
       dm = fmax(dm, fabs(d));
       y[r] = rhs_unit < 0 ? R[((size_t)q * k + i) * k + r] : (r == rhs_unit ? 1.0 : 0.0);
     }
-    if (tid < 2) col[k + tid] = 0.0;  // pads read by the last column pair
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
     if (lane == 0) red[warp] = dm;
@@ -82,65 +82,144 @@ __global__ void __launch_bounds__(kT64, 1)
     double dmax = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) dmax = fmax(dmax, red[w]);
-    // pivot data of step j is produced by ONE thread (tid 0) and published through
-    // s_inv / s_yj (parity j & 1): for j = 0 here, for j + 1 right after warp 0 has
-    // updated row j + 1 (the only row it depends on)
-    double pivmin = DBL_MAX;
+    double pivmin = DBL_MAX;  // lane-local in warp 0 (diagonal pivots), reduced at the end
     bool bad = false;
-    auto pivot = [&](int jn) {
-      const double d = A[off(jn) + jn];
-      pivmin = fmin(pivmin, d);
-      bad |= !(d > 0.0) || !(d <= DBL_MAX);
-      const double inv = 1.0 / sqrt(d);
-      s_inv[jn & 1] = inv;
-      s_yj[jn & 1] = y[jn] * inv;
-    };
-    if (tid == 0) pivot(0);
-    __syncthreads();
 
-    // ---- factorization + forward substitution ----
-    for (int j = 0; j < k; ++j) {
-      const double inv = s_inv[j & 1], yj = s_yj[j & 1];
-      for (int r = j + 1 + tid; r < k; r += kT64) {
-        const double l = A[off(r) + j] * inv;
-        A[off(r) + j] = l;
-        col[r] = l;
-        y[r] = fma(-l, yj, y[r]);
-      }
-      if (tid == 0) {
-        yy[j] = yj;
-        invd[j] = inv;
-        col[j] = 0.0;  // a column pair starting at j leaves column j unchanged
+    // ---- blocked factorization (8-column panels) + forward substitution ----
+    for (int j0 = 0; j0 < k; j0 += NB) {
+      const int nb = min(NB, k - j0);
+      // (1) warp 0: 8x8 diagonal block, lane u = row j0+u (lower part only)
+      if (warp == 0) {
+        const int u = lane;
+        double a[NB];
+#pragma unroll
+        for (int t = 0; t < NB; ++t) a[t] = (u < nb && t <= u) ? A[off(j0 + u) + j0 + t] : 0.0;
+        double inv_u = 0.0;
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          if (t < nb) {
+            const double d = __shfl_sync(0xffffffffu, a[t], t);  // lane t's updated diagonal
+            const double inv = 1.0 / sqrt(d);
+            if (u == t) {
+              pivmin = fmin(pivmin, d);
+              bad |= !(d > 0.0) || !(d <= DBL_MAX);
+              inv_u = inv;
+            }
+            const double l = a[t] * inv;  // L[j0+u][j0+t] for u >= t
+            a[t] = l;
+#pragma unroll
+            for (int c = t + 1; c < NB; ++c) {
+              const double lc = __shfl_sync(0xffffffffu, l, c);
+              if (c <= u) a[c] = fma(-l, lc, a[c]);
+            }
+          }
+        }
+        // panel forward substitution: yb = L11^{-1} y[j0 .. j0+nb)
+        double yb = (u < nb) ? y[j0 + u] : 0.0;
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          if (t < nb) {
+            const double yt = __shfl_sync(0xffffffffu, yb * inv_u, t);
+            if (u > t) yb = fma(-a[t], yt, yb);
+            if (u == t) yb = yt;
+          }
+        }
+        if (u < nb) {
+#pragma unroll
+          for (int t = 0; t < NB; ++t)
+            if (t <= u) A[off(j0 + u) + j0 + t] = a[t];
+          invd[j0 + u] = inv_u;
+          yy[j0 + u] = yb;
+        }
       }
       __syncthreads();
-      // rank-1 update, rows r (short) and r2 = k + j - r (long) per warp, column pairs
-      const int nrow = k - 1 - j, c0 = (j + 1) & ~1;
-      for (int t = warp; 2 * t < nrow; t += NW) {
-        const int r = j + 1 + t, r2 = k - 1 - t;
-        const double lr = col[r], lr2 = col[r2];
-        double* Ar = A + off(r);
-        double* Ar2 = A + off(r2);
-        for (int c = c0 + 2 * lane; c <= r2; c += 64) {
-          const double2 cc = *reinterpret_cast<const double2*>(col + c);
-          double2 v = *reinterpret_cast<double2*>(Ar2 + c);
-          v.x = fma(-lr2, cc.x, v.x);
-          v.y = fma(-lr2, cc.y, v.y);
-          *reinterpret_cast<double2*>(Ar2 + c) = v;
-          if (c <= r && r != r2) {
-            double2 u = *reinterpret_cast<double2*>(Ar + c);
-            u.x = fma(-lr, cc.x, u.x);
-            u.y = fma(-lr, cc.y, u.y);
-            *reinterpret_cast<double2*>(Ar + c) = u;
+      // (2) rows below the block: L21 row (TRSM against L11), y update
+      const int nrest = k - j0 - nb;
+      for (int rr = tid; rr < nrest; rr += kT64) {
+        const int r = j0 + nb + rr;
+        double* Ar = A + off(r) + j0;
+        double l[NB];
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          if (t < nb) {
+            double v = Ar[t];
+            const double* L11t = A + off(j0 + t) + j0;
+#pragma unroll
+            for (int s2 = 0; s2 < t; ++s2) v = fma(-l[s2], L11t[s2], v);
+            l[t] = v * invd[j0 + t];
+          } else {
+            l[t] = 0.0;
+          }
+        }
+        double yr = y[r];
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          if (t < nb) {
+            Ar[t] = l[t];
+            yr = fma(-l[t], yy[j0 + t], yr);
+          }
+        }
+        y[r] = yr;
+      }
+      __syncthreads();
+      // (3) trailing rank-8 update of rows / columns >= j0+8 on the FP64 tensor
+      //     path (DMMA, mma.sync m8n8k4 f64): 8x8 tiles of the lower trailing
+      //     triangle, K = the panel's 8 columns in two k=4 steps.  Row r's panel
+      //     entries are contiguous (A[off(r) + j0 ...]); A fragment = -L rows,
+      //     B fragment = L rows of the tile's columns, C/D = the trailing block
+      //     (double2 per lane; only c <= r is stored back, so diagonal tiles never
+      //     touch the next row).  (Only full panels have a trailing part.)
+      if (nrest > 0) {
+        const int jb = j0 + NB;
+        const int T = (nrest + 7) >> 3;
+        const int g = lane >> 2, q4 = lane & 3;
+        const int ntiles = T * (T + 1) / 2;
+        for (int e = warp; e < ntiles; e += NW) {
+          {
+            // linear lower-triangle tile index -> (tr, tc), e = tr(tr+1)/2 + tc
+            int tr = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
+            while (tr * (tr + 1) / 2 > e) --tr;
+            while ((tr + 1) * (tr + 2) / 2 <= e) ++tr;
+            const int tc = e - tr * (tr + 1) / 2;
+            const int r0 = jb + 8 * tr, c0 = jb + 8 * tc;
+            const int ra = r0 + g, rb = c0 + g;  // A-fragment row, B-fragment column (= L row)
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+            if (ra < k) {
+              a0 = -A[off(ra) + j0 + q4];
+              a1 = -A[off(ra) + j0 + 4 + q4];
+            }
+            if (rb < k) {
+              b0 = A[off(rb) + j0 + q4];
+              b1 = A[off(rb) + j0 + 4 + q4];
+            }
+            const int cr = r0 + g, cc = c0 + 2 * q4;
+            const bool st = cr < k && cc <= cr;
+            double2 cv = make_double2(0.0, 0.0);
+            if (st) cv = *reinterpret_cast<const double2*>(A + off(cr) + cc);
+            double d0, d1;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+                         : "=d"(d0), "=d"(d1)
+                         : "d"(a0), "d"(b0), "d"(cv.x), "d"(cv.y));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+                         : "=d"(d0), "=d"(d1)
+                         : "d"(a1), "d"(b1), "d"(d0), "d"(d1));
+            if (st) *reinterpret_cast<double2*>(A + off(cr) + cc) = make_double2(d0, d1);
           }
         }
       }
-      if (warp == 0 && j + 1 < k) {  // warp 0 owns row j + 1: next pivot
-        __syncwarp();
-        if (lane == 0) pivot(j + 1);
-      }
       __syncthreads();
     }
-    if (tid == 0) sbad = bad ? 1 : 0;
+    if (warp == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        pivmin = fmin(pivmin, __shfl_xor_sync(0xffffffffu, pivmin, o));
+        bad |= __shfl_xor_sync(0xffffffffu, (int)bad, o) != 0;
+      }
+      if (lane == 0) {
+        sbad = bad ? 1 : 0;
+        s_piv = pivmin;
+      }
+    }
     // ---- back substitution L^T x = y (column-oriented: row j of L is contiguous) ----
     for (int r = tid; r < k; r += kT64) xs[r] = yy[r];
     __syncthreads();
@@ -157,7 +236,7 @@ __global__ void __launch_bounds__(kT64, 1)
       __syncthreads();
     }
     if (tid == 0) {
-      double rc = dmax > 0.0 ? fmax(pivmin, 0.0) / dmax : 0.0;
+      double rc = dmax > 0.0 ? fmax(s_piv, 0.0) / dmax : 0.0;
       if (!(rc >= 0.0)) rc = 0.0;
       if (sbad || nf || !(rc >= rthr)) atomicMin(fail_min, (unsigned long long)sys);
       atomicMin(rcond_min_bits, __float_as_uint((float)rc));
@@ -226,7 +305,7 @@ cudaError_t launch_fault_combine_f64(double* x, const double* z, int k, int w, d
 }
 
 size_t chol_f64_smem_bytes(int k) {
-  return (((packed_doubles(k) + 1) & ~(size_t)1) + ((k + 3) & ~1) + 4 * (size_t)k) * sizeof(double);
+  return (((packed_doubles(k) + 1) & ~(size_t)1) + ((k + 3) & ~1) + 3 * (size_t)k) * sizeof(double);
 }
 
 cudaError_t launch_chol_f64(const double* G, const double* R, const double* M, double* C, int k, int64_t nsys,
