@@ -358,11 +358,18 @@ cudaError_t launch_gemm_nt(const float* X, const float* Y, int64_t b, int M, int
 
 cudaError_t launch_project(const float* phi, const float* mass, const float* F, int64_t b,
                            int64_t n, int k, int d, float* out, cudaStream_t st) {
-  // tensor-core path (tcgen05, 3xTF32) with FMAP_PROJ=tc (d <= 256): 2.4x faster,
-  // but its rounding (~4e-5 of max|A| over n = 5000) lifts the pipeline's relative
-  // residual above the north_star's 1e-5, so the FP32 kernel stays the default
+  // tensor-core path (tcgen05, 3xTF32, accumulation folded into an fp32 sum every
+  // 256 vertices so the tensor core's biased accumulation stays bounded: 2.0e-6 of
+  // max|A| at cfg2 vs 3.4e-6 for the FP32 kernel, 0.97 vs 1.25 ms) whenever d <= 256
+  // and its grid (one CTA per pair and 128 basis functions) covers at least half
+  // the SMs; FMAP_PROJ=simt / tc forces either kernel.
   const char* sel = std::getenv("FMAP_PROJ");
-  if (sel && sel[0] == 't') {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tc_grid = b * ((k + 127) / 128);
+  const bool want_tc = sel ? sel[0] == 't' : (d <= 256 && 2 * tc_grid >= sms);
+  if (want_tc) {
     const cudaError_t e = launch_project_tc(phi, mass, F, b, n, k, d, out, st);
     if (e != cudaErrorNotSupported) return e;
   }

@@ -1318,6 +1318,11 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
 namespace {
 constexpr int kPjK = 16;      // vertices per stage
 constexpr int kPjThreads = 288;  // 8 producer warps + 1 MMA warp
+// The tensor core accumulates fp32 with a bias (its error grows linearly with the
+// number of accumulated products), so every kPjChunk stages (256 vertices) the
+// chunk's accumulator (TMEM columns 0..N-1) is folded by the producer warps into
+// a running sum (TMEM columns 256..256+N-1) with IEEE fp32 adds.
+constexpr int kPjChunk = 16;
 
 __device__ __forceinline__ float tf32_hi(float x) {  // round-to-nearest TF32
   uint32_t h;
@@ -1325,7 +1330,7 @@ __device__ __forceinline__ float tf32_hi(float x) {  // round-to-nearest TF32
   return __uint_as_float(h);
 }
 
-__global__ void __launch_bounds__(kPjThreads, 2) proj_tc_kernel(const float* __restrict__ phi,
+__global__ void __launch_bounds__(kPjThreads, 1) proj_tc_kernel(const float* __restrict__ phi,
                                                                   const float* __restrict__ mass,
                                                                   const float* __restrict__ F,
                                                                   int64_t n, int k, int d, int N,
@@ -1339,17 +1344,22 @@ __global__ void __launch_bounds__(kPjThreads, 2) proj_tc_kernel(const float* __r
   // per stage buffer: A_hi | A_lo (128 x 16) | B_hi | B_lo (N x 16)
   const int abytes = 128 * kPjK, bbytes = N * kPjK;  // floats
   const int sstride = 2 * abytes + 2 * bbytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sstride);  // full[2], empty[2], done
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
+  // full[2], empty[2], (unused), chunkdone (MMA -> producers), folded (producers -> MMA)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sstride);
+  uint64_t* chunkdone = bar + 5;
+  uint64_t* folded = bar + 6;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 7);
   if (tid == 0) {
     mbar_init(&bar[0], 8);
     mbar_init(&bar[1], 8);
     mbar_init(&bar[2], 1);
     mbar_init(&bar[3], 1);
     mbar_init(&bar[4], 1);
+    mbar_init(chunkdone, 1);
+    mbar_init(folded, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) tmem_alloc(tslot, 256);
+  if (warp == 0) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1361,6 +1371,11 @@ __global__ void __launch_bounds__(kPjThreads, 2) proj_tc_kernel(const float* __r
       const uint32_t id = idesc_tf32(N) & ~(1u << 13);  // D += A*B (no negation)
       for (int st = 0; st < nst; ++st) {
         const int buf = st & 1;
+        const int cs = st % kPjChunk;  // stage within its chunk
+        if (cs == 0 && st > 0) {       // the previous chunk's accumulator has been folded
+          mbar_wait(folded, ((st / kPjChunk) - 1) & 1);
+          tc_fence_after();
+        }
         mbar_wait(&bar[buf], (st >> 1) & 1);
         tc_fence_after();
         const uint32_t ah = su32(smem + buf * sstride), al = ah + abytes * 4;
@@ -1368,13 +1383,13 @@ __global__ void __launch_bounds__(kPjThreads, 2) proj_tc_kernel(const float* __r
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
           const uint32_t ko = (uint32_t)ks * 256u;
-          mma_tf32(tbase, sdesc(ah + ko), sdesc(bh + ko), id, (st > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32(tbase, sdesc(ah + ko), sdesc(bh + ko), id, (cs > 0 || ks > 0) ? 1u : 0u);
           mma_tf32(tbase, sdesc(ah + ko), sdesc(bl + ko), id, 1u);
           mma_tf32(tbase, sdesc(al + ko), sdesc(bh + ko), id, 1u);
         }
         mma_commit(&bar[2 + buf]);
+        if (cs == kPjChunk - 1 || st == nst - 1) mma_commit(chunkdone);
       }
-      mma_commit(&bar[4]);
     }
   } else {  // ---- producers (256 threads) ----
     for (int st = 0; st < nst; ++st) {
@@ -1431,16 +1446,38 @@ __global__ void __launch_bounds__(kPjThreads, 2) proj_tc_kernel(const float* __r
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar[buf]);
+      if (st % kPjChunk == kPjChunk - 1 || st == nst - 1) {
+        // fold this chunk (warp w: lane quarter w % 4, column half w / 4) into the sum
+        const int c = st / kPjChunk;
+        mbar_wait(chunkdone, c & 1);
+        tc_fence_after();
+        const int quarter = warp & 3, half = warp >> 2, nh = N / 2;
+        const uint32_t tl = tbase + ((uint32_t)(32 * quarter) << 16);
+        for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+          float v[16];
+          tmem_ld16(tl + (uint32_t)c0, v);
+          if (c > 0) {
+            float sv[16];
+            tmem_ld16(tl + 256u + (uint32_t)c0, sv);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] += sv[t];
+          }
+          tmem_st16(tl + 256u + (uint32_t)c0, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(folded);
+      }
     }
-    // ---- epilogue: TMEM -> Out (warp w: lane quarter w % 4, column half w / 4) ----
-    mbar_wait(&bar[4], 0);
-    tc_fence_after();
+    // ---- epilogue: the folded sum (TMEM columns 256..) -> Out; each warp reads
+    // exactly the quarter / column half it folded itself ----
     const int quarter = warp & 3, half = warp >> 2;
     const int i = i0 + 32 * quarter + lane;
     const int nh = N / 2;
     for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
       float v[16];
-      tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)c0, v);
+      tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + 256u + (uint32_t)c0, v);
       if (i < k) {
         float* o = out + ((size_t)q * k + i) * d + c0;
         if (c0 + 16 <= d && (d & 3) == 0) {
@@ -1457,7 +1494,7 @@ __global__ void __launch_bounds__(kPjThreads, 2) proj_tc_kernel(const float* __r
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, 256);
+  if (warp == 0) tmem_dealloc(tbase, 512);
 }
 }  // namespace
 
@@ -1467,7 +1504,7 @@ cudaError_t launch_project_tc(const float* phi, const float* mass, const float* 
   if (d > 256 || d < 1 || k < 1 || n < 1 || b < 1) return cudaErrorNotSupported;
   const int N = (d + 15) & ~15;
   const size_t smem = (size_t)(2 * (2 * 128 * kPjK + 2 * N * kPjK)) * 4 + 64;
-  const size_t req = smem < 233472 / 3 + 1 ? 233472 / 3 + 1 : smem;  // <= 2 CTAs per SM (TMEM 256 cols)
+  const size_t req = smem < 233472 / 2 + 1 ? 233472 / 2 + 1 : smem;  // 1 CTA per SM (TMEM 512 cols)
   cudaError_t e = cudaFuncSetAttribute(proj_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)req);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((k + 127) / 128), (unsigned)b);

@@ -159,23 +159,26 @@ def test_golden_solutions_on_gpu(fm):
         assert np.abs(got - C).max() <= TOL_REL * np.abs(C).max(), name
 
 
-def test_projection_tensor_core_kernel(fm, oracle, monkeypatch):
-    """tcgen05 3xTF32 projection (opt-in FMAP_PROJ=tc): parity with the FP32 oracle
-    within its documented accuracy (biased fp32 accumulation in the
-    tensor core, error ~ n * 2^-27 of max|A|; n = 1500 here)."""
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_projection_kernels_accuracy(fm, oracle, monkeypatch, kernel):
+    """Both projection kernels (tcgen05 3xTF32 with the accumulation folded into an
+    fp32 sum every 256 vertices, and the FP32 SIMT kernel) against the f64 oracle
+    at n = 12000, where an unfolded tensor-core accumulation would be off by ~1e-4
+    of max|A|: both must stay within 1e-5."""
     from paper_2604_10377_b200 import synth
     import ctypes as C
-    monkeypatch.setenv("FMAP_PROJ", "tc")
-    cfg = synth.PairConfig("t", 2, 50, 128, 1500, 1500)
+    monkeypatch.setenv("FMAP_PROJ", kernel)
+    n = 12000
+    cfg = synth.PairConfig("t", 2, 50, 128, n, n)
     data = synth.make_batch(cfg)
     t = {k: _dev(v) for k, v in data.items()}
     out = torch.empty((2, 50, 128), device="cuda")
     ctx = fm._lib.context(0)
-    st = ctx._lib.fmap_project_f32_dev(ctx.handle, 2, 1500, 50, 128, C.c_void_p(t["phi1"].data_ptr()),
+    st = ctx._lib.fmap_project_f32_dev(ctx.handle, 2, n, 50, 128, C.c_void_p(t["phi1"].data_ptr()),
                                        C.c_void_p(t["mass1"].data_ptr()), C.c_void_p(t["F1"].data_ptr()),
                                        C.c_void_p(out.data_ptr()))
     assert st == 0
     torch.cuda.synchronize()
     for q in range(2):
         ref = oracle.project_mass(data["phi1"][q], data["mass1"][q], data["F1"][q])
-        assert np.abs(out[q].cpu().numpy() - ref).max() <= 5e-5 * np.abs(ref).max()
+        assert np.abs(out[q].cpu().numpy() - ref).max() <= 1e-5 * np.abs(ref).max()
