@@ -265,6 +265,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(su32(bar))
       : "memory");
 }
+// 3-D / 2-D tensor TMA loads (box from the tensor map) into shared memory.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
 // 4-D tensor TMA load (box from the tensor map) into shared memory.
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             uint64_t* bar) {
@@ -1496,13 +1512,217 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_tc_kernel(const float* __r
   __syncthreads();
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
+
+// Same GEMM with the inputs streamed by TMA: a kPjR-deep ring of raw fp32 tiles
+// (Phi box 128 basis functions x 16 vertices, F box N channels x 16 vertices,
+// Mass 16 vertices) refilled by the MMA thread as soon as the stage that used the
+// slot has been converted; the 8 producer warps only convert shared memory to the
+// hi/lo K-major operands (Mass applied to F).  No loads in flight in registers, so
+// the per-stage cost is the conversion, not an HBM round trip.  Same MMA and
+// chunk-fold scheme as proj_tc_kernel.
+constexpr int kPjR = 4;
+
+__global__ void __launch_bounds__(kPjThreads, 1)
+    proj_tma_kernel(const __grid_constant__ CUtensorMap tmPhi, const __grid_constant__ CUtensorMap tmF,
+                    const __grid_constant__ CUtensorMap tmMass, int64_t n, int k, int d, int N,
+                    float* __restrict__ out) {
+  extern __shared__ __align__(1024) float smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = blockIdx.y, i0 = blockIdx.x * 128;
+  const int abytes = 128 * kPjK, bbytes = N * kPjK;  // floats
+  const int sstride = 2 * abytes + 2 * bbytes;
+  const int rstride = (2048 + 16 * N + 16 + 31) & ~31;  // raw slot: Phi [16][128] | F [16][N] | Mass [16]
+  float* raw = smem + 2 * sstride;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + kPjR * rstride);
+  uint64_t* opfull = bar;          // [2] producers -> MMA
+  uint64_t* opempty = bar + 2;     // [2] MMA -> producers
+  uint64_t* chunkdone = bar + 5;
+  uint64_t* folded = bar + 6;
+  uint64_t* rawfull = bar + 7;     // [kPjR] TMA -> producers
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 7 + kPjR);
+  if (tid == 0) {
+    mbar_init(&opfull[0], 8);
+    mbar_init(&opfull[1], 8);
+    mbar_init(&opempty[0], 1);
+    mbar_init(&opempty[1], 1);
+    mbar_init(chunkdone, 1);
+    mbar_init(folded, 8);
+    for (int r = 0; r < kPjR; ++r) mbar_init(&rawfull[r], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const int nst = (int)((n + kPjK - 1) / kPjK);
+  const uint32_t rawbytes = (uint32_t)(2048 + 16 * N + 16) * 4u;
+
+  if (warp == 8) {  // ---- TMA issue + MMA issue ----
+    if (lane == 0) {
+      auto issue_raw = [&](int s2) {
+        const int slot = s2 % kPjR;
+        float* rs = raw + slot * rstride;
+        mbar_expect_tx(&rawfull[slot], rawbytes);
+        tma_load_3d(rs, &tmPhi, i0, s2 * kPjK, q, &rawfull[slot]);
+        tma_load_3d(rs + 2048, &tmF, 0, s2 * kPjK, q, &rawfull[slot]);
+        tma_load_2d(rs + 2048 + 16 * N, &tmMass, s2 * kPjK, q, &rawfull[slot]);
+      };
+      for (int s2 = 0; s2 < kPjR && s2 < nst; ++s2) issue_raw(s2);
+      const uint32_t id = idesc_tf32(N) & ~(1u << 13);  // D += A*B (no negation)
+      for (int st = 0; st < nst; ++st) {
+        const int buf = st & 1;
+        const int cs = st % kPjChunk;
+        if (cs == 0 && st > 0) {
+          mbar_wait(folded, ((st / kPjChunk) - 1) & 1);
+          tc_fence_after();
+        }
+        mbar_wait(&opfull[buf], (st >> 1) & 1);  // also: raw slot st % kPjR has been converted
+        tc_fence_after();
+        if (st + kPjR < nst) issue_raw(st + kPjR);
+        const uint32_t ah = su32(smem + buf * sstride), al = ah + abytes * 4;
+        const uint32_t bh = al + abytes * 4, bl = bh + bbytes * 4;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t ko = (uint32_t)ks * 256u;
+          mma_tf32(tbase, sdesc(ah + ko), sdesc(bh + ko), id, (cs > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32(tbase, sdesc(ah + ko), sdesc(bl + ko), id, 1u);
+          mma_tf32(tbase, sdesc(al + ko), sdesc(bh + ko), id, 1u);
+        }
+        mma_commit(&opempty[buf]);
+        if (cs == kPjChunk - 1 || st == nst - 1) mma_commit(chunkdone);
+      }
+    }
+  } else {  // ---- producers (256 threads): raw fp32 tiles -> hi/lo operands ----
+    const int ia = tid & 127, vg = tid >> 7;  // A: basis function ia, vertices 8vg..8vg+7
+    for (int st = 0; st < nst; ++st) {
+      const int buf = st & 1, slot = st % kPjR;
+      mbar_wait(&rawfull[slot], (st / kPjR) & 1);
+      if (st >= 2) mbar_wait(&opempty[buf], ((st - 2) >> 1) & 1);  // MMAs of stage st-2 done
+      const float* rp = raw + slot * rstride;
+      const float* rf = rp + 2048;
+      const float* rm = rp + 2048 + 16 * N;
+      float* S = smem + buf * sstride;
+#pragma unroll
+      for (int h4 = 0; h4 < 2; ++h4) {
+        const int v4 = 2 * vg + h4;
+        float av[4], hv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          av[u] = rp[(4 * v4 + u) * 128 + ia];
+          hv[u] = tf32_hi(av[u]);
+        }
+        const int o = (ia >> 3) * 128 + v4 * 32 + (ia & 7) * 4;
+        *reinterpret_cast<float4*>(S + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<float4*>(S + abytes + o) =
+            make_float4(av[0] - hv[0], av[1] - hv[1], av[2] - hv[2], av[3] - hv[3]);
+      }
+      if (tid < N) {
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+          float bv[4], hv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            bv[u] = rf[(4 * v4 + u) * N + tid] * rm[4 * v4 + u];
+            hv[u] = tf32_hi(bv[u]);
+          }
+          const int o = (tid >> 3) * 128 + v4 * 32 + (tid & 7) * 4;
+          *reinterpret_cast<float4*>(S + 2 * abytes + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<float4*>(S + 2 * abytes + bbytes + o) =
+              make_float4(bv[0] - hv[0], bv[1] - hv[1], bv[2] - hv[2], bv[3] - hv[3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&opfull[buf]);
+      if (st % kPjChunk == kPjChunk - 1 || st == nst - 1) {
+        const int c = st / kPjChunk;
+        mbar_wait(chunkdone, c & 1);
+        tc_fence_after();
+        const int quarter = warp & 3, half = warp >> 2, nh = N / 2;
+        const uint32_t tl = tbase + ((uint32_t)(32 * quarter) << 16);
+        for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+          float v[16];
+          tmem_ld16(tl + (uint32_t)c0, v);
+          if (c > 0) {
+            float sv[16];
+            tmem_ld16(tl + 256u + (uint32_t)c0, sv);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] += sv[t];
+          }
+          tmem_st16(tl + 256u + (uint32_t)c0, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(folded);
+      }
+    }
+    const int quarter = warp & 3, half = warp >> 2;
+    const int i = i0 + 32 * quarter + lane;
+    const int nh = N / 2;
+    for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + 256u + (uint32_t)c0, v);
+      if (i < k) {
+        float* o = out + ((size_t)q * k + i) * d + c0;
+        if (c0 + 16 <= d) {
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4)
+            *reinterpret_cast<float4*>(o + 4 * c4) = make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (c0 + t < d) o[t] = v[t];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
 }  // namespace
 
 // Tensor-core projection (d <= 256); returns cudaErrorNotSupported otherwise.
+// Row-major fp32 tensor [dim2][dim1][dim0] as a TMA map with box {b0, b1, 1}
+// (rank 3) or [dim1][dim0] with box {b0, 1} (rank 2).
+static int encode_plain_map(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims, const cuuint32_t* box) {
+  const EncodeTiledFn fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t strides[2] = {dims[0] * 4, rank == 3 ? dims[0] * dims[1] * 4 : 0};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : -1;
+}
+
 cudaError_t launch_project_tc(const float* phi, const float* mass, const float* F, int64_t b,
                               int64_t n, int k, int d, float* out, cudaStream_t st) {
   if (d > 256 || d < 1 || k < 1 || n < 1 || b < 1) return cudaErrorNotSupported;
   const int N = (d + 15) & ~15;
+  // TMA-streamed kernel when every row stride is 16-byte aligned
+  if (k % 4 == 0 && d % 4 == 0 && n % 4 == 0 && !std::getenv("FMAP_PROJ_NOTMA")) {
+    CUtensorMap tp, tf, tm;
+    const cuuint64_t dp[3] = {(cuuint64_t)k, (cuuint64_t)n, (cuuint64_t)b};
+    const cuuint32_t bp[3] = {128, (cuuint32_t)kPjK, 1};
+    const cuuint64_t df[3] = {(cuuint64_t)d, (cuuint64_t)n, (cuuint64_t)b};
+    const cuuint32_t bf[3] = {(cuuint32_t)N, (cuuint32_t)kPjK, 1};
+    const cuuint64_t dm[2] = {(cuuint64_t)n, (cuuint64_t)b};
+    const cuuint32_t bm[2] = {(cuuint32_t)kPjK, 1};
+    if (encode_plain_map(&tp, phi, 3, dp, bp) == 0 && encode_plain_map(&tf, F, 3, df, bf) == 0 &&
+        encode_plain_map(&tm, mass, 2, dm, bm) == 0) {
+      const int rstride = (2048 + 16 * N + 16 + 31) & ~31;
+      const size_t smem = (size_t)(2 * (2 * 128 * kPjK + 2 * N * kPjK) + kPjR * rstride) * 4 + 256;
+      cudaError_t e = cudaFuncSetAttribute(proj_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      dim3 grid((unsigned)((k + 127) / 128), (unsigned)b);
+      proj_tma_kernel<<<grid, kPjThreads, smem, st>>>(tp, tf, tm, n, k, d, N, out);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = (size_t)(2 * (2 * 128 * kPjK + 2 * N * kPjK)) * 4 + 64;
   const size_t req = smem < 233472 / 2 + 1 ? 233472 / 2 + 1 : smem;  // 1 CTA per SM (TMEM 512 cols)
   cudaError_t e = cudaFuncSetAttribute(proj_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)req);
