@@ -86,53 +86,59 @@ __global__ void __launch_bounds__(kT64, 1)
     bool bad = false;
 
     // ---- blocked factorization (8-column panels) + forward substitution ----
-    for (int j0 = 0; j0 < k; j0 += NB) {
+    // (1) warp 0: 8x8 diagonal block at j0, lane u = row j0+u (lower part only),
+    //     and the panel's forward-substitution values.  For j0 > 0 it runs inside
+    //     the previous panel's trailing update, right after warp 0 has updated
+    //     that block (tile (0,0) of the update), hidden behind the other warps'
+    //     tiles.
+    auto diag_block = [&](int j0) {
       const int nb = min(NB, k - j0);
-      // (1) warp 0: 8x8 diagonal block, lane u = row j0+u (lower part only)
-      if (warp == 0) {
-        const int u = lane;
-        double a[NB];
+      const int u = lane;
+      double a[NB];
 #pragma unroll
-        for (int t = 0; t < NB; ++t) a[t] = (u < nb && t <= u) ? A[off(j0 + u) + j0 + t] : 0.0;
-        double inv_u = 0.0;
+      for (int t = 0; t < NB; ++t) a[t] = (u < nb && t <= u) ? A[off(j0 + u) + j0 + t] : 0.0;
+      double inv_u = 0.0;
 #pragma unroll
-        for (int t = 0; t < NB; ++t) {
-          if (t < nb) {
-            const double d = __shfl_sync(0xffffffffu, a[t], t);  // lane t's updated diagonal
-            const double inv = 1.0 / sqrt(d);
-            if (u == t) {
-              pivmin = fmin(pivmin, d);
-              bad |= !(d > 0.0) || !(d <= DBL_MAX);
-              inv_u = inv;
-            }
-            const double l = a[t] * inv;  // L[j0+u][j0+t] for u >= t
-            a[t] = l;
-#pragma unroll
-            for (int c = t + 1; c < NB; ++c) {
-              const double lc = __shfl_sync(0xffffffffu, l, c);
-              if (c <= u) a[c] = fma(-l, lc, a[c]);
-            }
+      for (int t = 0; t < NB; ++t) {
+        if (t < nb) {
+          const double d = __shfl_sync(0xffffffffu, a[t], t);  // lane t's updated diagonal
+          const double inv = 1.0 / sqrt(d);
+          if (u == t) {
+            pivmin = fmin(pivmin, d);
+            bad |= !(d > 0.0) || !(d <= DBL_MAX);
+            inv_u = inv;
           }
-        }
-        // panel forward substitution: yb = L11^{-1} y[j0 .. j0+nb)
-        double yb = (u < nb) ? y[j0 + u] : 0.0;
+          const double l = a[t] * inv;  // L[j0+u][j0+t] for u >= t
+          a[t] = l;
 #pragma unroll
-        for (int t = 0; t < NB; ++t) {
-          if (t < nb) {
-            const double yt = __shfl_sync(0xffffffffu, yb * inv_u, t);
-            if (u > t) yb = fma(-a[t], yt, yb);
-            if (u == t) yb = yt;
+          for (int c = t + 1; c < NB; ++c) {
+            const double lc = __shfl_sync(0xffffffffu, l, c);
+            if (c <= u) a[c] = fma(-l, lc, a[c]);
           }
-        }
-        if (u < nb) {
-#pragma unroll
-          for (int t = 0; t < NB; ++t)
-            if (t <= u) A[off(j0 + u) + j0 + t] = a[t];
-          invd[j0 + u] = inv_u;
-          yy[j0 + u] = yb;
         }
       }
-      __syncthreads();
+      // panel forward substitution: yb = L11^{-1} y[j0 .. j0+nb)
+      double yb = (u < nb) ? y[j0 + u] : 0.0;
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        if (t < nb) {
+          const double yt = __shfl_sync(0xffffffffu, yb * inv_u, t);
+          if (u > t) yb = fma(-a[t], yt, yb);
+          if (u == t) yb = yt;
+        }
+      }
+      if (u < nb) {
+#pragma unroll
+        for (int t = 0; t < NB; ++t)
+          if (t <= u) A[off(j0 + u) + j0 + t] = a[t];
+        invd[j0 + u] = inv_u;
+        yy[j0 + u] = yb;
+      }
+    };
+    if (warp == 0) diag_block(0);
+    __syncthreads();
+    for (int j0 = 0; j0 < k; j0 += NB) {
+      const int nb = min(NB, k - j0);
       // (2) rows below the block: L21 row (TRSM against L11), y update
       const int nrest = k - j0 - nb;
       for (int rr = tid; rr < nrest; rr += kT64) {
@@ -174,7 +180,9 @@ __global__ void __launch_bounds__(kT64, 1)
         const int T = (nrest + 7) >> 3;
         const int g = lane >> 2, q4 = lane & 3;
         const int ntiles = T * (T + 1) / 2;
-        for (int e = warp; e < ntiles; e += NW) {
+        // warp 0: tile 0 (the next diagonal block) then its factorization;
+        // warps 1..NW-1: tiles 1.. round-robin
+        for (int e = warp == 0 ? 0 : warp - 1 + 1; e < (warp == 0 ? 1 : ntiles); e += (warp == 0 ? 1 : NW - 1)) {
           {
             // linear lower-triangle tile index -> (tr, tc), e = tr(tr+1)/2 + tc
             int tr = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
@@ -205,6 +213,10 @@ __global__ void __launch_bounds__(kT64, 1)
                          : "d"(a1), "d"(b1), "d"(d0), "d"(d1));
             if (st) *reinterpret_cast<double2*>(A + off(cr) + cc) = make_double2(d0, d1);
           }
+        }
+        if (warp == 0) {  // the next diagonal block is final now (only this panel's update was pending)
+          __syncwarp();
+          diag_block(jb);
         }
       }
       __syncthreads();
