@@ -232,18 +232,39 @@ __global__ void __launch_bounds__(kT64, 1)
         s_piv = pivmin;
       }
     }
-    // ---- back substitution L^T x = y (column-oriented: row j of L is contiguous) ----
+    // ---- back substitution L^T x = y in 8-row blocks from the bottom: warp 0
+    //      solves the block's 8x8 transposed triangle (shuffles), then every
+    //      thread removes the block's contribution from the rows above it (row c
+    //      of L is contiguous, so A[off(c) + r] is coalesced over r) ----
     for (int r = tid; r < k; r += kT64) xs[r] = yy[r];
     __syncthreads();
     double* Crow = rhs_unit < 0 ? C + ((size_t)q * k + i) * k : C;
     bool nf = false;
-    for (int j = k - 1; j >= 0; --j) {
-      const double xj = xs[j] * invd[j];
-      const double* Lj = A + off(j);
-      for (int r = tid; r < j; r += kT64) xs[r] = fma(-Lj[r], xj, xs[r]);
-      if (tid == 0) {
-        Crow[j] = xj;
-        nf |= !(fabs(xj) <= DBL_MAX);
+    for (int c0 = ((k - 1) / NB) * NB; c0 >= 0; c0 -= NB) {
+      const int nbb = min(NB, k - c0);
+      if (warp == 0) {
+        double v = lane < nbb ? xs[c0 + lane] : 0.0;
+#pragma unroll
+        for (int t = NB - 1; t >= 0; --t) {
+          if (t < nbb) {
+            const double xt = __shfl_sync(0xffffffffu, v, t) * invd[c0 + t];
+            if (lane < t) v = fma(-A[off(c0 + t) + c0 + lane], xt, v);
+            if (lane == t) v = xt;
+          }
+        }
+        if (lane < nbb) {
+          xs[c0 + lane] = v;
+          Crow[c0 + lane] = v;
+        }
+        nf |= __any_sync(0xffffffffu, lane < nbb && !(fabs(v) <= DBL_MAX));
+      }
+      __syncthreads();
+      for (int r = tid; r < c0; r += kT64) {
+        double acc = xs[r];
+#pragma unroll
+        for (int t = 0; t < NB; ++t)
+          if (t < nbb) acc = fma(-A[off(c0 + t) + r], xs[c0 + t], acc);
+        xs[r] = acc;
       }
       __syncthreads();
     }
