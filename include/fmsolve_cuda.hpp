@@ -11,8 +11,8 @@
 // Error behaviour is the reference's (types.hpp:25-67, solver.hpp:229-322):
 // std::invalid_argument on validation, MemoryCapExceeded before allocating,
 // SingularSystemError(lowest failing system index), nothing returned on error.
-// Arithmetic is fp32 (SolverOptions<float>); a double instantiation converts
-// at the boundary.  peak_extra_bytes is the cuda route's own device accounting
+// Scalar = float runs the fp32 tcgen05 route, Scalar = double the f64 route
+// (fmap_solve_f64, rcond threshold 1e-14 by default).  peak_extra_bytes is the cuda route's own device accounting
 // (SURVEY D9), not the b*k^3 of the batched route.
 //
 // Two modes:
@@ -32,6 +32,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #ifndef FMSOLVE_CUDA_STANDALONE
@@ -180,27 +181,37 @@ BatchSolveReport<Scalar> solve_cuda_many(std::span<const RegularizedProblem<Scal
     require(p.resolution() == k, "all problems in a batch must share the spectral resolution");
   }
   const std::size_t b = problems.size(), kk = (std::size_t)k * k;
-  std::vector<float> G(b * kk), R(b * kk), M(b * kk), C(b * kk);
+  // Scalar = double -> the f64 route (fmap_solve_f64: f64 end to end, the
+  // reference's default precision); Scalar = float -> the fp32 tensor-core route.
+  using Elem = std::conditional_t<sizeof(Scalar) == sizeof(double), double, float>;
+  std::vector<Elem> G(b * kk), R(b * kk), M(b * kk), C(b * kk);
   for (std::size_t q = 0; q < b; ++q) {
     const auto& p = problems[q];
     for (std::size_t e = 0; e < kk; ++e) {
-      G[q * kk + e] = (float)p.neq.gram.data()[e];
-      R[q * kk + e] = (float)p.neq.rhs.data()[e];
-      M[q * kk + e] = (float)p.mask.data()[e];
+      G[q * kk + e] = (Elem)p.neq.gram.data()[e];
+      R[q * kk + e] = (Elem)p.neq.rhs.data()[e];
+      M[q * kk + e] = (Elem)p.mask.data()[e];
     }
   }
   fmap_solver_options o;
   fmap_default_options(&o);
   o.ridge = (float)opts.ridge;
-  o.rcond_threshold = sizeof(Scalar) == sizeof(float) ? (float)opts.rcond_threshold : -1.f;
+  // the f64 route reads a negative threshold as its own default (1e-14)
+  o.rcond_threshold = opts.rcond_threshold == SolverOptions<Scalar>{}.rcond_threshold ? -1.f
+                                                                                       : (float)opts.rcond_threshold;
   o.has_memory_cap = opts.memory_cap_bytes ? 1 : 0;
   o.memory_cap_bytes = opts.memory_cap_bytes ? *opts.memory_cap_bytes : 0;
   o.threads = opts.threads;
   o.inject_fault = opts.inject_fault ? 1 : 0;
   fmap_report rep;
   fmap_ctx* ctx = cuda_detail::context(device);
-  const int st = fmap_solve_f32(ctx, (int64_t)b, (int64_t)k, G.data(), R.data(), M.data(),
-                                (float)lambda, &o, C.data(), &rep);
+  int st;
+  if constexpr (sizeof(Elem) == sizeof(double))
+    st = fmap_solve_f64(ctx, (int64_t)b, (int64_t)k, G.data(), R.data(), M.data(), (double)lambda, &o, C.data(),
+                        &rep);
+  else
+    st = fmap_solve_f32(ctx, (int64_t)b, (int64_t)k, G.data(), R.data(), M.data(), (float)lambda, &o, C.data(),
+                        &rep);
   if (st != FMAP_OK) cuda_detail::raise(ctx, st, rep);
   BatchSolveReport<Scalar> out;
   out.maps.reserve(b);

@@ -90,6 +90,24 @@ int main() {
     } catch (const std::invalid_argument&) {
     }
   }
+  {  // Scalar = double: the f64 route, closed form to f64 accuracy (bench.cpp:28 tolerance 1e-8)
+    const int k = 8;
+    RegularizedProblem<double> p;
+    p.neq.gram = MatrixX<double>(k, k);
+    p.neq.rhs = MatrixX<double>(k, k);
+    p.mask = MatrixX<double>(k, k);
+    for (int i = 0; i < k; ++i) {
+      p.neq.gram(i, i) = 1.0;
+      p.neq.rhs(i, i) = 1.0;
+      for (int j = 0; j < k; ++j) p.mask(i, j) = 0.5 + 0.1 * ((i * 7 + j * 3) % 5);
+    }
+    auto r = solve_cuda(p, 10.0);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) {
+        const double e = i == j ? 1.0 / (1.0 + 10.0 * p.mask(i, i)) : 0.0;
+        if (std::fabs(r.map(i, j) - e) > 1e-13) ++fails;  // beyond what an fp32 route can reach
+      }
+  }
   std::printf("adapter checks: %s (%d failures)\n", fails ? "FAIL" : "PASS", fails);
   return fails ? 1 : 0;
 }
