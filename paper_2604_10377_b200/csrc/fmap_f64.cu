@@ -182,13 +182,15 @@ __global__ void __launch_bounds__(kT64, 1)
         const int ntiles = T * (T + 1) / 2;
         // warp 0: tile 0 (the next diagonal block) then its factorization;
         // warps 1..NW-1: tiles 1.. round-robin
-        for (int e = warp == 0 ? 0 : warp - 1 + 1; e < (warp == 0 ? 1 : ntiles); e += (warp == 0 ? 1 : NW - 1)) {
+        // tile e = tr(tr+1)/2 + tc walked with an incremental (tr, tc) cursor
+        const int e0 = warp == 0 ? 0 : warp, estep = warp == 0 ? ntiles : NW - 1;
+        int tr = 0, tc = e0;
+        while (tc > tr) {
+          tc -= tr + 1;
+          ++tr;
+        }
+        for (int e = e0; e < (warp == 0 ? 1 : ntiles); e += estep) {
           {
-            // linear lower-triangle tile index -> (tr, tc), e = tr(tr+1)/2 + tc
-            int tr = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
-            while (tr * (tr + 1) / 2 > e) --tr;
-            while ((tr + 1) * (tr + 2) / 2 <= e) ++tr;
-            const int tc = e - tr * (tr + 1) / 2;
             const int r0 = jb + 8 * tr, c0 = jb + 8 * tc;
             const int ra = r0 + g, rb = c0 + g;  // A-fragment row, B-fragment column (= L row)
             double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
@@ -212,6 +214,11 @@ __global__ void __launch_bounds__(kT64, 1)
                          : "=d"(d0), "=d"(d1)
                          : "d"(a1), "d"(b1), "d"(d0), "d"(d1));
             if (st) *reinterpret_cast<double2*>(A + off(cr) + cc) = make_double2(d0, d1);
+          }
+          tc += estep;
+          while (tc > tr && tr < T) {
+            tc -= tr + 1;
+            ++tr;
           }
         }
         if (warp == 0) {  // the next diagonal block is final now (only this panel's update was pending)
