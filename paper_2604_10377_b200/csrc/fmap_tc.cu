@@ -888,14 +888,28 @@ __global__ void __launch_bounds__(MAXT, MINB)
           ld_ok[h] = row_valid && row < k && vld[h];
           Gq[h] = p.gram + (size_t)qs[h] * k * k;
         }
-        for (int cb = 1; cb < ncb; ++cb) {  // one chunk of every system in flight
-          float b[NS][16];
+        if constexpr (NS == 1 && MAXT == 384) {  // one CTA per SM (K16 > 256): every system comes this way
+          for (int cb = 1; cb < ncb; cb += 2) {  // two chunks of loads in flight
+            float b0[16], b1[16];
+            load_cols(Gq[0], k, row, ld_ok[0], cb, b0);
+            if (cb + 1 < ncb) load_cols(Gq[0], k, row, ld_ok[0], cb + 1, b1);
+            fix_diag(b0, cb, 0);
+            tmem_st16(tq + (uint32_t)(16 * cb), b0);
+            if (cb + 1 < ncb) {
+              fix_diag(b1, cb + 1, 0);
+              tmem_st16(tq + (uint32_t)(16 * (cb + 1)), b1);
+            }
+          }
+        } else {
+          for (int cb = 1; cb < ncb; ++cb) {  // one chunk of every system in flight
+            float b[NS][16];
 #pragma unroll
-          for (int h = 0; h < NS; ++h) load_cols(Gq[h], k, row, ld_ok[h], cb, b[h]);
+            for (int h = 0; h < NS; ++h) load_cols(Gq[h], k, row, ld_ok[h], cb, b[h]);
 #pragma unroll
-          for (int h = 0; h < NS; ++h) {
-            fix_diag(b[h], cb, h);
-            tmem_st16(tq + tsys * h + (uint32_t)(16 * cb), b[h]);
+            for (int h = 0; h < NS; ++h) {
+              fix_diag(b[h], cb, h);
+              tmem_st16(tq + tsys * h + (uint32_t)(16 * cb), b[h]);
+            }
           }
         }
         if (row_valid) {
