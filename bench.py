@@ -553,8 +553,8 @@ def run_fmbench(mode, argv) -> int:
             print(f"# timing: wall clock; median of {a.reps} repetitions after {a.warmup} warmup runs per solver",
                   file=out)
             print("# timed region: rowwise / batched = the reference routes (CPU restatement, oracle/): per-system "
-                  "assembly + factorization + solve; cuda = fmap_solve_f32 on host buffers (H2D, device validation, "
-                  "tcgen05/TMEM Cholesky solve, D2H) on one B200", file=out)
+                  "assembly + factorization + solve; cuda = fmap_solve_f32 (--precision f32: H2D, device validation, "
+                  "tcgen05/TMEM Cholesky solve, D2H) or fmap_solve_f64 (--precision f64: DMMA Cholesky) on one B200", file=out)
             print(f"# batched dispatch: {threads} worker thread(s); cuda: one launch per batch", file=out)
             print(FMBENCH_COLUMNS, file=out)
             for k in ks:

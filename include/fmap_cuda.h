@@ -18,6 +18,14 @@
  *   F                   : [b][n][d]
  *   ev                  : [b][k]
  * System s of a batch is (pair q = s / k, row i = s % k)  (solver.hpp:262-263).
+ *
+ * Preconditions beyond the reference's (which factors every row system by
+ * partial-pivot LU): each system G + lambda*diag(M[i,:]) + ridge*I is factored by
+ * Cholesky from the lower triangle of G, so gram must be symmetric (checked on
+ * the device: |G[r][c] - G[c][r]| <= 1e-4 * max(|G[r][c]|, |G[c][r]|,
+ * sqrt|G[r][r] G[c][c]|), else FMAP_INVALID_ARGUMENT) and a system that is not
+ * positive definite is reported FMAP_SINGULAR.  G = A A^T (normal_equations)
+ * satisfies both whenever the reference's LU succeeds on an SPD system.
  */
 #ifndef FMAP_CUDA_H
 #define FMAP_CUDA_H

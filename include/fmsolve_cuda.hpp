@@ -1,12 +1,21 @@
 // fmsolve_cuda.hpp — header-only C++ adapter: the reference's solver API on top
 // of the libfmap_cuda C ABI (include/fmap_cuda.h).
 //
-// Drop-in for the batched route of /root/reference/proj/include/fmsolve/solver.hpp:
+// Drop-in for the batched route of /root/reference/proj/include/fmsolve/solver.hpp.
+// Namespace fmsolve::cuda holds the reference's own names and signatures, so a
+// caller switches routes by qualifying the call:
 //
-//   reference (solver.hpp)                          here (route "cuda")
-//   solve_batched_many(span<problems>, λ, opts, ws)  solve_cuda_many(span<problems>, λ, opts)
-//   solve_batched(problem | a,b,mask, λ, opts, ws)   solve_cuda(problem | a,b,mask, λ, opts)
-//   build_mask(kind, ev1, ev2, sigma)  masks.hpp:85  build_mask_cuda(kind, ev1, ev2, sigma)
+//   reference (fmsolve::)                              route "cuda" (fmsolve::cuda::)
+//   solve_batched_many(span, λ, opts, ws)  solver.hpp:225   solve_batched_many(span, λ, opts, ws)
+//   solve_batched(problem, λ, opts, ws)    solver.hpp:352   solve_batched(problem, λ, opts, ws)
+//   solve_batched(a, b, mask, λ, opts, ws) solver.hpp:360   solve_batched(a, b, mask, λ, opts, ws)
+//   build_mask(kind, ev1, ev2, sigma)      masks.hpp:85     build_mask(kind, ev1, ev2, sigma)
+//
+// The BatchedWorkspace (solver.hpp:86-93) is honoured the reference's way: its
+// vectors grow monotonically and are reused across calls, here as the packed
+// host staging of G/R/M (lhs) and C (rhs); the device arena lives in the
+// per-thread context.  fmsolve::solve_cuda_many / solve_cuda / build_mask_cuda
+// are the same calls with an explicit device ordinal.
 //
 // Error behaviour is the reference's (types.hpp:25-67, solver.hpp:229-322):
 // std::invalid_argument on validation, MemoryCapExceeded before allocating,
@@ -123,6 +132,12 @@ struct RegularizedProblem {
   std::ptrdiff_t resolution() const { return mask.rows(); }
 };
 
+template <typename Scalar>
+struct BatchedWorkspace {
+  std::vector<Scalar> lhs;
+  std::vector<Scalar> rhs;
+};
+
 }  // namespace fmsolve
 #endif
 
@@ -163,11 +178,14 @@ inline void require(bool cond, const char* msg) {
 
 }  // namespace cuda_detail
 
-/// solve_batched_many (solver.hpp:225-322) through the GPU route.
+/// solve_batched_many (solver.hpp:225-322) through the GPU route on `device`.
+/// Scalar = float runs the fp32 tcgen05 route, Scalar = double the f64 route.
 template <typename Scalar>
 BatchSolveReport<Scalar> solve_cuda_many(std::span<const RegularizedProblem<Scalar>> problems,
                                          Scalar lambda, const SolverOptions<Scalar>& opts = {},
-                                         int device = 0) {
+                                         int device = 0, BatchedWorkspace<Scalar>* workspace = nullptr) {
+  static_assert(std::is_same_v<Scalar, float> || std::is_same_v<Scalar, double>,
+                "the cuda route computes in float or double");
   using cuda_detail::require;
   require(!problems.empty(), "no problems to solve");
   const std::ptrdiff_t k = problems.front().resolution();
@@ -181,16 +199,21 @@ BatchSolveReport<Scalar> solve_cuda_many(std::span<const RegularizedProblem<Scal
     require(p.resolution() == k, "all problems in a batch must share the spectral resolution");
   }
   const std::size_t b = problems.size(), kk = (std::size_t)k * k;
-  // Scalar = double -> the f64 route (fmap_solve_f64: f64 end to end, the
-  // reference's default precision); Scalar = float -> the fp32 tensor-core route.
-  using Elem = std::conditional_t<sizeof(Scalar) == sizeof(double), double, float>;
-  std::vector<Elem> G(b * kk), R(b * kk), M(b * kk), C(b * kk);
+  // packed [b][k][k] host staging, reused across calls through the workspace
+  BatchedWorkspace<Scalar> local;
+  BatchedWorkspace<Scalar>& ws = workspace ? *workspace : local;
+  if (ws.lhs.size() < 3 * b * kk) ws.lhs.resize(3 * b * kk);
+  if (ws.rhs.size() < b * kk) ws.rhs.resize(b * kk);
+  Scalar* G = ws.lhs.data();
+  Scalar* R = G + b * kk;
+  Scalar* M = R + b * kk;
+  Scalar* C = ws.rhs.data();
   for (std::size_t q = 0; q < b; ++q) {
     const auto& p = problems[q];
     for (std::size_t e = 0; e < kk; ++e) {
-      G[q * kk + e] = (Elem)p.neq.gram.data()[e];
-      R[q * kk + e] = (Elem)p.neq.rhs.data()[e];
-      M[q * kk + e] = (Elem)p.mask.data()[e];
+      G[q * kk + e] = p.neq.gram.data()[e];
+      R[q * kk + e] = p.neq.rhs.data()[e];
+      M[q * kk + e] = p.mask.data()[e];
     }
   }
   fmap_solver_options o;
@@ -206,18 +229,16 @@ BatchSolveReport<Scalar> solve_cuda_many(std::span<const RegularizedProblem<Scal
   fmap_report rep;
   fmap_ctx* ctx = cuda_detail::context(device);
   int st;
-  if constexpr (sizeof(Elem) == sizeof(double))
-    st = fmap_solve_f64(ctx, (int64_t)b, (int64_t)k, G.data(), R.data(), M.data(), (double)lambda, &o, C.data(),
-                        &rep);
+  if constexpr (std::is_same_v<Scalar, double>)
+    st = fmap_solve_f64(ctx, (int64_t)b, (int64_t)k, G, R, M, lambda, &o, C, &rep);
   else
-    st = fmap_solve_f32(ctx, (int64_t)b, (int64_t)k, G.data(), R.data(), M.data(), (float)lambda, &o, C.data(),
-                        &rep);
+    st = fmap_solve_f32(ctx, (int64_t)b, (int64_t)k, G, R, M, lambda, &o, C, &rep);
   if (st != FMAP_OK) cuda_detail::raise(ctx, st, rep);
   BatchSolveReport<Scalar> out;
   out.maps.reserve(b);
   for (std::size_t q = 0; q < b; ++q) {
     out.maps.emplace_back(k, k);
-    for (std::size_t e = 0; e < kk; ++e) out.maps.back().data()[e] = (Scalar)C[q * kk + e];
+    for (std::size_t e = 0; e < kk; ++e) out.maps.back().data()[e] = C[q * kk + e];
   }
   out.max_residual_norm = (Scalar)rep.max_residual;
   out.wall_time = std::chrono::duration<double>(rep.wall_seconds);
@@ -228,9 +249,10 @@ BatchSolveReport<Scalar> solve_cuda_many(std::span<const RegularizedProblem<Scal
 /// solve_batched(problem, λ, opts) (solver.hpp:352-358) through the GPU route.
 template <typename Scalar>
 SolveReport<Scalar> solve_cuda(const RegularizedProblem<Scalar>& problem, Scalar lambda,
-                               const SolverOptions<Scalar>& opts = {}, int device = 0) {
+                               const SolverOptions<Scalar>& opts = {}, int device = 0,
+                               BatchedWorkspace<Scalar>* workspace = nullptr) {
   auto batch = solve_cuda_many(std::span<const RegularizedProblem<Scalar>>(&problem, 1), lambda,
-                               opts, device);
+                               opts, device, workspace);
   SolveReport<Scalar> r;
   r.map = std::move(batch.maps.front());
   r.residual_norm = batch.max_residual_norm;
@@ -275,4 +297,36 @@ MatrixX<Scalar> build_mask_cuda(MaskKind kind, const Vec& ev1, const Vec& ev2,
   return out;
 }
 
+namespace cuda {
+
+/// Route "cuda" under the reference's own names and signatures (device 0).
+template <typename Scalar>
+BatchSolveReport<Scalar> solve_batched_many(std::span<const RegularizedProblem<Scalar>> problems, Scalar lambda,
+                                            const SolverOptions<Scalar>& opts = {},
+                                            BatchedWorkspace<Scalar>* workspace = nullptr) {
+  return solve_cuda_many(problems, lambda, opts, 0, workspace);
+}
+
+template <typename Scalar>
+SolveReport<Scalar> solve_batched(const RegularizedProblem<Scalar>& problem, Scalar lambda,
+                                  const SolverOptions<Scalar>& opts = {},
+                                  BatchedWorkspace<Scalar>* workspace = nullptr) {
+  return solve_cuda(problem, lambda, opts, 0, workspace);
+}
+
+#ifndef FMSOLVE_CUDA_STANDALONE
+template <typename Scalar>
+SolveReport<Scalar> solve_batched(const MatrixX<Scalar>& a, const MatrixX<Scalar>& b, const MatrixX<Scalar>& mask,
+                                  Scalar lambda, const SolverOptions<Scalar>& opts = {},
+                                  BatchedWorkspace<Scalar>* workspace = nullptr) {
+  return solve_cuda(make_problem(a, b, mask), lambda, opts, 0, workspace);
+}
+#endif
+
+template <typename Scalar, typename Vec>
+MatrixX<Scalar> build_mask(MaskKind kind, const Vec& ev1, const Vec& ev2, Scalar sigma = Scalar(0.5)) {
+  return build_mask_cuda<Scalar>(kind, ev1, ev2, sigma, 0);
+}
+
+}  // namespace cuda
 }  // namespace fmsolve

@@ -40,9 +40,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir.mkdir(exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", str(ROOT / "include"), "-Xptxas", "-v"]
-    objs = []
-    for src in SOURCES:
+    def compile_one(src: str) -> str:
         obj = objdir / (Path(src).stem + ".o")
+        if not force and not _stale(obj, [CSRC / src, *CSRC.glob("*.cuh"), ROOT / "include" / "fmap_cuda.h"]):
+            return str(obj)
         cmd = [*common, "-c", str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -50,7 +51,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(res.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-cudart", "static"]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -27,8 +27,14 @@ struct fmap_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   std::string last_error;
+  // Two grow-only device arenas (BatchedWorkspace analogue, solver.hpp:86-93):
+  // `arena` holds what an entry point stages (host copies, pipeline
+  // intermediates), `scr` the solver's own scratch.  solve_core only ever grows
+  // `scr`, so pointers an entry point carved out of `arena` stay valid.
   void* arena = nullptr;
   size_t arena_bytes = 0;
+  void* scr = nullptr;
+  size_t scr_bytes = 0;
   // control block: [0] fail_min (u64) | [8] rcond bits (u32) | [12] flags (u32)
   unsigned char* d_ctrl = nullptr;
   unsigned char* h_ctrl = nullptr;  // pinned
@@ -62,23 +68,38 @@ unsigned long long* d_fail(fmap_ctx* c) { return reinterpret_cast<unsigned long 
 unsigned* d_rcond(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 8); }
 unsigned* d_flags(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 12); }
 
-// Grow-only device arena (BatchedWorkspace analogue, solver.hpp:86-93).
-// Growth preserves the contents so callers may stage data before reserving more.
-int arena_reserve(fmap_ctx* ctx, size_t bytes) {
-  if (bytes <= ctx->arena_bytes) return FMAP_OK;
+// Grow-only device arena.  Growth drops the old contents (the stream is drained
+// first, so no queued kernel still reads it): callers reserve BEFORE carving.
+int grow(fmap_ctx* ctx, void** buf, size_t* have, size_t bytes) {
+  if (bytes <= *have) return FMAP_OK;
   const size_t rounded = (bytes + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
-  void* fresh = nullptr;
-  FMAP_CK(ctx, cudaMalloc(&fresh, rounded));
-  if (ctx->arena) {
-    FMAP_CK(ctx, cudaMemcpyAsync(fresh, ctx->arena, ctx->arena_bytes, cudaMemcpyDeviceToDevice,
-                                 ctx->stream));
+  if (*buf) {
     FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
-    FMAP_CK(ctx, cudaFree(ctx->arena));
+    FMAP_CK(ctx, cudaFree(*buf));
+    *buf = nullptr;
+    *have = 0;
   }
-  ctx->arena = fresh;
-  ctx->arena_bytes = rounded;
+  FMAP_CK(ctx, cudaMalloc(buf, rounded));
+  *have = rounded;
   return FMAP_OK;
 }
+int arena_reserve(fmap_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->arena, &ctx->arena_bytes, bytes); }
+int scratch_reserve(fmap_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->scr, &ctx->scr_bytes, bytes); }
+
+// Every entry point runs on the context's device and restores the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess || prev == dev) {
+      prev = -1;
+      return;
+    }
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 struct Carve {
   char* base;
@@ -148,6 +169,9 @@ std::string flags_message(unsigned f) {
   if (f & 1u) return "gram contains non-finite entries";
   if (f & 2u) return "rhs contains non-finite entries";
   if (f & 4u) return "mask contains non-finite entries";
+  if (f & 64u)
+    return "gram must be symmetric: the cuda route factors G + lambda*diag(m_i) by Cholesky and reads one "
+           "triangle of G (G = A A^T from normal_equations always is)";
   return "invalid input";
 }
 
@@ -186,7 +210,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   const size_t tc_bytes = use_tc ? tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms) : 0;
   const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
                                      need_mask_scratch ? (size_t)b * kk * sizeof(float) : 0,
-                                     (size_t)k * sizeof(float), tc_bytes});
+                                     (size_t)k * sizeof(float), tc_bytes, (size_t)b * k * sizeof(float)});
   const uint64_t required = (uint64_t)scratch + host_staging_bytes;
   if (rep) rep->peak_extra_bytes = required;
   if (opts.has_memory_cap && required > opts.memory_cap_bytes) {
@@ -199,14 +223,15 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
                        " bytes of device scratch, above the cap of " +
                        std::to_string(opts.memory_cap_bytes));
   }
-  int st = arena_reserve(ctx, scratch + host_staging_bytes);
+  int st = scratch_reserve(ctx, scratch);
   if (st) return st;
-  Carve cv{reinterpret_cast<char*>(ctx->arena) + host_staging_bytes};
+  Carve cv{reinterpret_cast<char*>(ctx->scr)};
   double* partial = cv.take<double>(res_partial);
   double* res_out = cv.take<double>((size_t)b);
   float* mask_scratch = cv.take<float>(need_mask_scratch ? (size_t)b * kk : 0);
   float* zrow = cv.take<float>((size_t)k);
   float* tc_scr = cv.take<float>(tc_bytes / sizeof(float));
+  float* rowsum = cv.take<float>((size_t)b * k);
 
   if ((st = reset_ctrl(ctx))) return st;
   ctx->launches = 0;
@@ -220,6 +245,9 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     }
     ctx->launches++;
   }
+  // symmetry check + row 1-norms of G (rcond certificate input)
+  FMAP_CK(ctx, launch_gram_check(G, b, (int)k, rowsum, d_flags(ctx), ctx->stream));
+  ctx->launches++;
 
   SolveParams p{};
   p.gram = G;
@@ -242,6 +270,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   p.rcond_min_bits = d_rcond(ctx);
   p.flags = d_flags(ctx);
   p.tc_scratch = use_tc ? tc_scr : nullptr;
+  p.gram_rowsum = rowsum;
 
   // debug: FMAP_TRACE_FILE=<path> dumps per-warp clock64 phase stamps of one block
   const char* trace_file = std::getenv("FMAP_TRACE_FILE");
@@ -368,7 +397,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
 // second copy stream (the other direction's copy engine) right after its solve.
 // Same checks as solve_core (device validation, lowest failing index); on any error
 // C_out is zero-filled, so no partial result is exposed.  Used when no fault
-// injection / residual is requested.
+// injection is requested; the residual (check_stationarity) runs per chunk.
 int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const float* rhs,
                          const float* mask, float lambda, const fmap_solver_options& opts, float* C_out,
                          fmap_report* rep, int nchunk) {
@@ -377,7 +406,9 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   const int64_t cb = (b + nchunk - 1) / nchunk;  // pairs per chunk
   const int64_t csys = cb * k;
   const size_t tcb = tc_scratch_bytes((int)k, csys, ctx->num_sms);
-  const size_t staging = carve_size({bytes, bytes, bytes, bytes, tcb, tcb});
+  const size_t npart = opts.compute_residual ? residual_partial_count(cb, (int)k) * nchunk : 0;
+  const size_t staging = carve_size({bytes, bytes, bytes, bytes, tcb, tcb, (size_t)b * k * sizeof(float),
+                                     npart * sizeof(double), opts.compute_residual ? (size_t)b * sizeof(double) : 0});
   if (rep) rep->peak_extra_bytes = staging;
   if (opts.has_memory_cap && staging > opts.memory_cap_bytes) {
     if (rep) {
@@ -401,6 +432,9 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   float* dM = cv.take<float>((size_t)b * kk);
   float* dC = cv.take<float>((size_t)b * kk);
   float* scr[2] = {cv.take<float>(tcb / sizeof(float)), cv.take<float>(tcb / sizeof(float))};
+  float* rowsum = cv.take<float>((size_t)b * k);
+  double* partial = cv.take<double>(npart);
+  double* res_out = cv.take<double>(opts.compute_residual ? (size_t)b : 0);
   if ((st = reset_ctrl(ctx))) return st;
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[0], ctx->stream));
@@ -423,6 +457,7 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   p.rhs = dR;
   p.mask = dM;
   p.C = dC;
+  p.gram_rowsum = rowsum;
   ctx->launches = 0;
   for (int c = 0; c < nchunk; ++c) {  // all H2D first: the copy stream never waits on the solver
     const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
@@ -441,11 +476,17 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
     cudaStream_t s = comp[c & 1];
     FMAP_CK(ctx, cudaStreamWaitEvent(s, h2d, 0));
     FMAP_CK(ctx, launch_validate(dG + off, dR + off, dM + off, (size_t)nq * kk, d_flags(ctx), s));
+    FMAP_CK(ctx, launch_gram_check(dG + off, nq, (int)k, rowsum + (size_t)q0 * k, d_flags(ctx), s));
     p.nsys = nq * k;
     p.sys_offset = q0 * k;
     p.tc_scratch = scr[c & 1];
     FMAP_CK(ctx, launch_chol_solve(p, 0, s));
-    ctx->launches += 2;
+    ctx->launches += 3;
+    if (opts.compute_residual) {  // check_stationarity per chunk (solver.hpp:314-320), overlapped
+      FMAP_CK(ctx, launch_residual(dC + off, dG + off, dR + off, dM + off, nq, (int)k, lambda,
+                                   partial + (size_t)c * residual_partial_count(cb, (int)k), res_out + q0, s));
+      ctx->launches += 2;
+    }
     FMAP_CK(ctx, cudaEventRecord(done, s));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy2, done, 0));
     FMAP_CK(ctx, cudaMemcpyAsync(C_out + off, dC + off, nb, cudaMemcpyDeviceToHost, ctx->copy2));
@@ -472,6 +513,13 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
     return set_err(ctx, FMAP_SINGULAR,
                    "row system " + std::to_string(fail) +
                        " is numerically singular (Cholesky pivot / rcond estimate / non-finite solution)");
+  }
+  if (opts.compute_residual && rep) {
+    std::vector<double> res(b);
+    FMAP_CK(ctx, cudaMemcpy(res.data(), res_out, b * sizeof(double), cudaMemcpyDeviceToHost));
+    double mx = 0.0;
+    for (double v : res) mx = std::max(mx, v);
+    rep->max_residual = mx;
   }
   ctx->last_error.clear();
   return FMAP_OK;
@@ -510,9 +558,9 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
                    "cuda route needs " + std::to_string(required) + " bytes of device scratch, above the cap of " +
                        std::to_string(opts.memory_cap_bytes));
   }
-  int st = arena_reserve(ctx, scratch + host_staging_bytes);
+  int st = scratch_reserve(ctx, scratch);
   if (st) return st;
-  Carve cv{reinterpret_cast<char*>(ctx->arena) + host_staging_bytes};
+  Carve cv{reinterpret_cast<char*>(ctx->scr)};
   double* sq = cv.take<double>((size_t)b);
   double* zrow = cv.take<double>((size_t)k);
   if ((st = reset_ctrl(ctx))) return st;
@@ -597,12 +645,16 @@ int fmap_ctx_create(int device, fmap_ctx** out) {
   *out = nullptr;
   fmap_ctx* ctx = new fmap_ctx();
   ctx->device = device;
+  DeviceGuard dg(device);  // the caller's current device is restored on return
   auto fail = [&](cudaError_t e) {
-    delete ctx;
+    fmap_ctx_destroy(ctx);
     (void)e;
     return FMAP_CUDA_ERROR;
   };
   cudaError_t e;
+  int ndev = 0;
+  if ((e = cudaGetDeviceCount(&ndev)) != cudaSuccess) return fail(e);
+  if (device < 0 || device >= ndev) return fail(cudaErrorInvalidDevice);
   if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(e);
   if ((e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(e);
@@ -623,9 +675,10 @@ int fmap_ctx_create(int device, fmap_ctx** out) {
 
 int fmap_ctx_destroy(fmap_ctx* ctx) {
   if (!ctx) return FMAP_OK;
-  cudaSetDevice(ctx->device);
+  DeviceGuard dg(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->scr) cudaFree(ctx->scr);
   if (ctx->d_ctrl) cudaFree(ctx->d_ctrl);
   if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -656,6 +709,7 @@ int fmap_solve_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gram,
                        const float* d_rhs, const float* d_mask, float lambda,
                        const fmap_solver_options* opts, float* d_C, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   return solve_core(ctx, b, k, d_gram, d_rhs, d_mask, nullptr, nullptr, 0, 0.f, lambda, opts,
                     d_C, report, true, 0);
 }
@@ -665,6 +719,7 @@ int fmap_solve_ev_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gr
                           int mask_kind, float sigma, float lambda,
                           const fmap_solver_options* opts, float* d_C, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (mask_kind != FMAP_MASK_COMMUTATIVITY && mask_kind != FMAP_MASK_RESOLVENT)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
   return solve_core(ctx, b, k, d_gram, d_rhs, nullptr, d_ev1, d_ev2,
@@ -676,6 +731,7 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
                    const float* mask, float lambda, const fmap_solver_options* opts,
                    float* C_out, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   init_report(report);
   if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
   if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
@@ -694,7 +750,7 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   // residual); FMAP_PIPELINE=<chunks> overrides the default (1 = unpipelined)
   const char* pipe = std::getenv("FMAP_PIPELINE");
   const int nchunk = pipe ? std::max(1, std::min(16, std::atoi(pipe))) : 8;
-  if (nchunk > 1 && !o.inject_fault && !o.compute_residual && b >= 2 * nchunk && !std::getenv("FMAP_SOLVER") &&
+  if (nchunk > 1 && !o.inject_fault && b >= 2 * nchunk && !std::getenv("FMAP_SOLVER") &&
       k <= max_resolution(ctx) && tc_supported((int)k, ctx->max_smem_optin))
     return solve_host_pipelined(ctx, b, k, gram, rhs, mask, lambda, o, C_out, report, nchunk);
   if (o.has_memory_cap && staging > o.memory_cap_bytes) {
@@ -708,7 +764,7 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
                        " bytes of device staging, above the cap of " +
                        std::to_string(o.memory_cap_bytes));
   }
-  int st = arena_reserve(ctx, staging + (64u << 20));
+  int st = arena_reserve(ctx, staging);
   if (st) return st;
   Carve cv{reinterpret_cast<char*>(ctx->arena)};
   float* dG = cv.take<float>((size_t)b * kk);
@@ -730,12 +786,14 @@ int fmap_solve_f64_dev(fmap_ctx* ctx, int64_t b, int64_t k, const double* d_gram
                        const double* d_mask, double lambda, const fmap_solver_options* opts, double* d_C_out,
                        fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   return solve_core_f64(ctx, b, k, d_gram, d_rhs, d_mask, lambda, opts, d_C_out, report, 0);
 }
 
 int fmap_solve_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* gram, const double* rhs, const double* mask,
                    double lambda, const fmap_solver_options* opts, double* C_out, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   init_report(report);
   if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
   if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
@@ -756,7 +814,7 @@ int fmap_solve_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* gram, cons
                    "cuda route needs " + std::to_string(staging) + " bytes of device staging, above the cap of " +
                        std::to_string(o.memory_cap_bytes));
   }
-  int st = arena_reserve(ctx, staging + (1u << 20));
+  int st = arena_reserve(ctx, staging);
   if (st) return st;
   Carve cv{reinterpret_cast<char*>(ctx->arena)};
   double* dG = cv.take<double>((size_t)b * k * k);
@@ -776,6 +834,7 @@ int fmap_solve_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* gram, cons
 int fmap_mask_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_ev1,
                       const float* d_ev2, int mask_kind, float sigma, float* d_mask_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalue vectors must be non-empty");
   if (mask_kind != 0 && mask_kind != 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
   if (mask_kind == 1 && !(sigma > 0.f))
@@ -783,19 +842,26 @@ int fmap_mask_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_ev1,
   int st = reset_ctrl(ctx);
   if (st) return st;
   FMAP_CK(ctx, launch_validate_ev(d_ev1, d_ev2, (size_t)b * k, d_flags(ctx), ctx->stream));
+  ctx->launches = 1;
+  if (mask_kind == 1) {  // masks.hpp:58-59: the resolvent mask normalises by the pair's max eigenvalue
+    FMAP_CK(ctx, launch_ev_max_check(d_ev1, d_ev2, b, (int)k, d_flags(ctx), ctx->stream));
+    ctx->launches++;
+  }
   FMAP_CK(ctx, launch_mask(d_ev1, d_ev2, b, (int)k, mask_kind, sigma, d_mask_out, ctx->stream));
-  ctx->launches = 2;
+  ctx->launches++;
   unsigned long long fail;
   float rc;
   unsigned flags;
   if ((st = read_ctrl(ctx, &fail, &rc, &flags))) return st;
-  if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalues must be non-negative");
+  if (flags & 16u) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalues must be non-negative and finite");
+  if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, flags_message(flags));
   return FMAP_OK;
 }
 
 int fmap_mask_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* ev1, const float* ev2,
                   int mask_kind, float sigma, float* mask_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalue vectors must be non-empty");
   if (mask_kind != 0 && mask_kind != 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
   // masks.hpp:48-53 / 79-89 validation order
@@ -836,6 +902,7 @@ int fmap_normal_equations_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d
                                   const float* d_A, const float* d_B, float* d_gram,
                                   float* d_rhs) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (b < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "descriptor A must be non-empty");
   FMAP_CK(ctx, launch_gemm_nt(d_A, d_A, b, (int)k, (int)k, (int)d, d_gram, ctx->stream));
@@ -847,6 +914,7 @@ int fmap_normal_equations_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d
 int fmap_normal_equations_f32(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d, const float* A,
                               const float* B, float* gram_out, float* rhs_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (b < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "descriptor A must be non-empty");
   const size_t nab = (size_t)b * k * d, ng = (size_t)b * k * k;
@@ -872,6 +940,7 @@ int fmap_project_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t
                          const float* d_phi, const float* d_mass, const float* d_F,
                          float* d_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (b < 1 || n < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "basis and features must be non-empty");
   FMAP_CK(ctx, launch_project(d_phi, d_mass, d_F, b, n, (int)k, (int)d, d_out, ctx->stream));
@@ -883,12 +952,13 @@ int fmap_residual_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_C,
                           const float* d_gram, const float* d_rhs, const float* d_mask,
                           float lambda, double* d_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
   const size_t np = residual_partial_count(b, (int)k);
-  int st = arena_reserve(ctx, np * sizeof(double));
+  int st = scratch_reserve(ctx, np * sizeof(double));
   if (st) return st;
   FMAP_CK(ctx, launch_residual(d_C, d_gram, d_rhs, d_mask, b, (int)k, lambda,
-                               reinterpret_cast<double*>(ctx->arena), d_out, ctx->stream));
+                               reinterpret_cast<double*>(ctx->scr), d_out, ctx->stream));
   ctx->launches = 2;
   return FMAP_OK;
 }
@@ -901,6 +971,7 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
                           const fmap_solver_options* opts, float* d_Cxy, float* d_Cyx,
                           fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
   init_report(report);
   if (b < 1 || n1 < 1 || n2 < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "pipeline dimensions must be positive");
@@ -911,9 +982,8 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
   fmap_solver_options o;
   default_opts(&o);
   if (opts) o = *opts;
-  // the pipeline's own scratch lives below the solver's scratch in the arena
-  int st = arena_reserve(ctx, scratch + (64u << 20) +
-                                  (size_t)b * k * k * sizeof(float) * (o.compute_residual ? 1 : 0));
+  // the pipeline's intermediates live in the staging arena, the solver's scratch in ctx->scr
+  int st = arena_reserve(ctx, scratch);
   if (st) return st;
   Carve cv{reinterpret_cast<char*>(ctx->arena)};
   float* A = cv.take<float>(nab);

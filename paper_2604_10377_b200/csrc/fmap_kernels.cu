@@ -99,6 +99,77 @@ __global__ void validate_ev_kernel(const float* __restrict__ e1, const float* __
   if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
 }
 
+// Resolvent masks normalise by max(ev1, ev2) of their pair (masks.hpp:58-59): an
+// all-zero spectrum is rejected (bit 5) instead of producing a NaN mask.  One
+// warp per pair.
+__global__ void ev_max_check_kernel(const float* __restrict__ e1, const float* __restrict__ e2, int64_t b,
+                                    int k, unsigned* flags) {
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= b) return;
+  float m = 0.f;
+  for (int c = threadIdx.x & 31; c < k; c += 32)
+    m = fmaxf(m, fmaxf(e1[(size_t)q * k + c], e2[(size_t)q * k + c]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0 && !(m > 0.f)) atomicOr(flags, 32u);
+}
+
+// Per pair q, 32 rows per CTA: S[q][r] = sum_c |G[q][r][c]| (the row 1-norms the
+// solver's rcond certificate needs: G is symmetric, so they are its column sums
+// too) and the symmetry check the Cholesky route relies on (it reads one
+// triangle, the reference's LU reads both): bit 6 when
+//   |G[r][c] - G[c][r]| > 1e-4 * max(|G[r][c]|, |G[c][r]|, sqrt|G[r][r] G[c][c]|),
+// a bound rounding-level asymmetry of a float G = A A^T (d * eps ~ 1.5e-5 at d = 256)
+// stays well below.  Fixed summation order (deterministic S).
+__global__ void __launch_bounds__(256) gram_check_kernel(const float* __restrict__ G, int k,
+                                                         float* __restrict__ S, unsigned* flags) {
+  __shared__ float t1[32][33], t2[32][33];
+  const int nt = (k + 31) / 32;
+  const int64_t q = blockIdx.x / nt;
+  const int I = (int)(blockIdx.x % nt) * 32;
+  const float* Gq = G + (size_t)q * k * k;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  float rs[4] = {0.f, 0.f, 0.f, 0.f};
+  float dI[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = I + ty + 8 * u;
+    dI[u] = r < k ? fabsf(Gq[(size_t)r * k + r]) : 0.f;
+  }
+  unsigned f = 0;
+  for (int J = 0; J < k; J += 32) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = ty + 8 * u;
+      t1[r][tx] = (I + r < k && J + tx < k) ? Gq[(size_t)(I + r) * k + J + tx] : 0.f;
+      t2[r][tx] = (J + r < k && I + tx < k) ? Gq[(size_t)(J + r) * k + I + tx] : 0.f;
+    }
+    __syncthreads();
+    const int c = J + tx;
+    const float dc = c < k ? fabsf(Gq[(size_t)c * k + c]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = ty + 8 * u;
+      const float a = t1[r][tx], at = t2[tx][r];  // G[I+r][c], G[c][I+r]
+      rs[u] += fabsf(a);
+      if (I + r < k && c < k) {
+        const float sc = fmaxf(fmaxf(fabsf(a), fabsf(at)), sqrtf(dI[u] * dc));
+        if (!(fabsf(a - at) <= 1e-4f * sc)) f |= 64u;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    float v = rs[u];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int r = I + ty + 8 * u;
+    if (tx == 0 && r < k && S) S[(size_t)q * k + r] = v;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (tx == 0 && f) atomicOr(flags, f);
+}
+
 // ---------------------------------------------------------------------------
 // Batched "NT" GEMM family, FP32 SIMT, 64x64 CTA tile, 4x4 per thread:
 //   out[q][m][n] = sum_t X[q][m][t] * Y[q][n][t]          (gram, rhs)
@@ -346,6 +417,17 @@ cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsig
                                cudaStream_t st) {
   const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 4);
   validate_ev_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(e1, e2, n, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ev_max_check(const float* e1, const float* e2, int64_t b, int k, unsigned* flags,
+                                cudaStream_t st) {
+  ev_max_check_kernel<<<(unsigned)((b + 7) / 8), 256, 0, st>>>(e1, e2, b, k, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_check(const float* G, int64_t b, int k, float* S, unsigned* flags, cudaStream_t st) {
+  gram_check_kernel<<<(unsigned)(b * ((k + 31) / 32)), 256, 0, st>>>(G, k, S, flags);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,9 @@ cudaError_t launch_validate(const float* g, const float* r, const float* m, size
                             unsigned* flags, cudaStream_t st);
 cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsigned* flags,
                                cudaStream_t st);
+cudaError_t launch_ev_max_check(const float* e1, const float* e2, int64_t b, int k, unsigned* flags,
+                                cudaStream_t st);
+cudaError_t launch_gram_check(const float* G, int64_t b, int k, float* S, unsigned* flags, cudaStream_t st);
 cudaError_t launch_gemm_nt(const float* X, const float* Y, int64_t b, int M, int N, int K,
                            float* out, cudaStream_t st);
 cudaError_t launch_project(const float* phi, const float* mass, const float* F, int64_t b,

@@ -55,6 +55,7 @@ struct SolveParams {
   unsigned int* rcond_min_bits;  // float bits of the smallest rcond estimate
   unsigned int* flags;           // validation flags (bit 5: empty spectrum)
   float* tc_scratch;             // tensor-core solver: per-CTA L scratch (tc_scratch_bytes)
+  const float* gram_rowsum;      // [b][k] sum_c |G[q][r][c]| (launch_gram_check): rcond certificate
   long long* trace;              // debug phase trace (nullptr = off)
   int trace_block;
   int force_single;              // debug: force one system per CTA

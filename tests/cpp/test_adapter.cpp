@@ -108,6 +108,31 @@ int main() {
         if (std::fabs(r.map(i, j) - e) > 1e-13) ++fails;  // beyond what an fp32 route can reach
       }
   }
+  {  // the reference's signature: fmsolve::cuda::solve_batched_many(span, lambda, opts, workspace)
+    const int k = 6, b = 3;
+    MatrixX<float> mask(k, k);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) mask(i, j) = 0.25f * (float)((i + 2 * j) % 3);
+    std::vector<RegularizedProblem<float>> probs;
+    for (int q = 0; q < b; ++q) probs.push_back(diag_problem(k, std::vector<float>(k, 1.f + q), mask));
+    BatchedWorkspace<float> ws;
+    auto r = fmsolve::cuda::solve_batched_many<float>(std::span<const RegularizedProblem<float>>(probs), 2.f, {},
+                                                      &ws);
+    if (ws.lhs.size() < (size_t)(3 * b * k * k) || ws.rhs.size() < (size_t)(b * k * k)) ++fails;
+    const float* lhs0 = ws.lhs.data();
+    auto r2 = fmsolve::cuda::solve_batched_many<float>(std::span<const RegularizedProblem<float>>(probs), 2.f, {},
+                                                       &ws);
+    if (ws.lhs.data() != lhs0) ++fails;  // grown once, reused (solver.hpp:86-93)
+    for (int q = 0; q < b; ++q)
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) {
+          // G = (1+q) I, R = I  ->  C(i,i) = 1 / (1 + q + 2 M(i,i))
+          const float e = i == j ? 1.f / (1.f + q + 2.f * mask(i, i)) : 0.f;
+          if (std::fabs(r.maps[q](i, j) - e) > 1e-6f || r2.maps[q](i, j) != r.maps[q](i, j)) ++fails;
+        }
+    auto one = fmsolve::cuda::solve_batched<float>(probs[1], 2.f);
+    if (std::fabs(one.map(0, 0) - 1.f / (2.f + 2.f * mask(0, 0))) > 1e-6f) ++fails;
+  }
   std::printf("adapter checks: %s (%d failures)\n", fails ? "FAIL" : "PASS", fails);
   return fails ? 1 : 0;
 }

@@ -77,8 +77,8 @@ def test_bench_mem_cap_skips_batched_row_only():
 @pytest.mark.gpu
 def test_verify_passes_and_catches_injected_fault():
     # f64 (the reference default): the k^2 x k^2 oracle runs for k <= 32 (in f32 it
-    # is numerically singular from k ~ 24 on, as in the reference); the cuda route
-    # computes in f32 and is held to the f32 tolerance
+    # is numerically singular from k ~ 24 on, as in the reference); at --precision
+    # f64 the cuda route is fmap_solve_f64 (f64 end to end) and is held to 1e-8
     rc, out = _run("verify", "--k-start", "12", "--k-stop", "36", "--k-step", "12", "--batch", "2", "--precision",
                    "f64")
     assert rc == 0, out
