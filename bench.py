@@ -12,10 +12,13 @@ and Gram excluded).  `e2e` is the same metric through the host-buffer C ABI
 (`fmap_solve_f32`) with pinned host G, R, M in and C out every step.
 `pipeline` adds the device end-to-end path (Phi, Mass, F, ev -> C).
 
-Multi-GPU (torchrun, one process per GPU): pairs are sharded, each rank owns
-a fixed 64-pair slice (weak scaling), no collective in the timed region; the
-device time is the max over ranks.  `--gather` also times the final gather of
-C to rank 0 (NCCL), reported separately.
+Multi-GPU (`--gpus N`: self-launches N ranks through torch.distributed.run
+unless already under torchrun; one process per GPU, NCCL): STRONG scaling of
+the fixed global batch (cfg2's 64 pairs), rank g solving the contiguous pair
+range shard.pair_range(64, N, g) (the reference's chunking rule,
+solver.hpp:292-296), and the final gather of C to rank 0 (NCCL gather over
+NVLink) INSIDE the timed region; per-step device time = max over ranks.
+NCCL_DEBUG=INFO goes to per-rank files (nccl_debug_file in the JSON line).
 
 `--impl reference` times the CPU reference path (the C++ restatement of the
 reference's batched route, oracle/, with every host thread) on a bounded
@@ -107,15 +110,17 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- workload --
-def make_inputs(workload: str, rank: int, device):
-    """Generate the rank's shard on the host (seeded), project + Gram + mask on
+def make_inputs(workload: str, rank: int, world: int, device):
+    """Generate the rank's pair range of the global batch on the host (seeded per
+    pair, so every shard is the single-GPU run's pairs), project + Gram + mask on
     the GPU with our own kernels (untimed, like the reference's build_problems)."""
     import torch
-    from paper_2604_10377_b200 import synth, fmsolve, _lib
+    from paper_2604_10377_b200 import synth, fmsolve, _lib, shard
     import ctypes as C
     cfg = synth.CONFIGS[workload]
-    b = cfg.batch
-    data = synth.make_batch(cfg, q0=rank * b, count=b)
+    rg = shard.pair_range(cfg.batch, world, rank)
+    b = rg.size
+    data = synth.make_batch(cfg, q0=rg.lo, count=b)
     t = {k: torch.from_numpy(v).to(device) for k, v in data.items()}
     k, d = cfg.k, cfg.d
     A = torch.empty((b, k, d), device=device)
@@ -136,7 +141,7 @@ def make_inputs(workload: str, rank: int, device):
             raise RuntimeError(ctx.last_error())
     torch.cuda.synchronize(device)
     ctx.set_stream(None)
-    return cfg, t, G, R, M
+    return cfg, b, t, G, R, M
 
 
 # ----------------------------------------------------------------- our arm --
@@ -146,18 +151,26 @@ def run_ours(args):
     import ctypes as C
     from paper_2604_10377_b200 import fmsolve, _lib
 
+    from paper_2604_10377_b200 import shard
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    nccl_log = None
     if world > 1:
+        logdir = ROOT / "gpurun_out" if (ROOT / "gpurun_out").is_dir() else Path("/tmp")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", str(logdir / "nccl_bench.%h.%p.log"))
+        nccl_log = os.environ["NCCL_DEBUG_FILE"]
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
 
-    cfg, t, G, R, M = make_inputs(args.workload, rank, device)
-    b, k = cfg.batch, cfg.k
-    C_out = torch.empty_like(G)
+    cfg, b, t, G, R, M = make_inputs(args.workload, rank, world, device)
+    k = cfg.k
+    gb = cfg.batch  # global batch (strong scaling)
+    gat = shard.MapGather(gb, k, world, rank, device)
+    C_out = gat.local
     opts = fmsolve.SolverOptions(compute_residual=False).to_c()
     ctx = _lib.context(local)
     stream = torch.cuda.Stream(device)
@@ -173,11 +186,17 @@ def run_ours(args):
             raise RuntimeError(f"solve failed: {ctx.last_error()}")
         return rep
 
+    def gather():
+        with torch.cuda.stream(stream):
+            gat()
+
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):
             flush.zero_()
         step()
+        gather()
     launches_per_step = ctx.last_launch_count
+    launch_names = ctx.last_launches
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
@@ -192,6 +211,7 @@ def run_ours(args):
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             rep = step()                           # the API call syncs its stream at the end
+            gather()                               # final gather of C to rank 0 (N > 1)
             with torch.cuda.stream(stream):
                 e1.record(stream)
             e1.synchronize()
@@ -203,20 +223,20 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
 
-    fmaps = world * b * args.steps
+    fmaps = gb * args.steps
     value = fmaps / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
 
     gather_ms = None
-    if world > 1 and args.gather:
-        out = torch.empty((world,) + tuple(C_out.shape), device=device) if True else None
+    if world > 1:  # the gather alone (it is also inside every timed step)
         torch.cuda.synchronize(device)
         dist.barrier()
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
-        g0.record()
-        dist.all_gather_into_tensor(out, C_out)
-        g1.record()
+        with torch.cuda.stream(stream):
+            g0.record(stream)
+            gat()
+            g1.record(stream)
         g1.synchronize()
         gt = torch.tensor([g0.elapsed_time(g1)], device=device, dtype=torch.float64)
         dist.all_reduce(gt, op=dist.ReduceOp.MAX)
@@ -253,22 +273,28 @@ def run_ours(args):
         result = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: seeded BASELINE cfg generator (mass-orthonormal Phi via QR, "
                     "N(0,1) features, U(0,1)j^2 spectra to 200), random-init, no dataset",
-            "config": {"workload": args.workload, "pairs_per_gpu": b, "global_batch": b * world,
+            "config": {"workload": args.workload, "global_batch": gb, "pairs_rank0": b,
                        "k": k, "d": cfg.d, "n": cfg.n_src, "lambda": cfg.lam,
-                       "mask": f"resolvent sigma={cfg.sigma}", "parallelism": f"pairs sharded x{world}",
+                       "mask": f"resolvent sigma={cfg.sigma}",
+                       "parallelism": f"contiguous pair ranges x{world} (strong scaling) + NCCL gather of C to rank 0"
+                                      if world > 1 else "1 GPU",
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
                        "timed": "solve-only, device-resident G,R,M -> C via fmap_solve_f32_dev "
-                                "(validation + tcgen05/TMEM Cholesky solver), the reference's timed region"},
+                                "(validation + symmetry/row-norm check + tcgen05/TMEM Cholesky solver with "
+                                "the rcond verdict), the reference's timed region"
+                                + ("; plus the gather of C to rank 0" if world > 1 else "")},
             "roofline": roofline,
             "gpu_launches": int(launches_per_step * args.steps),
+            "launches_per_step": launch_names,
             "clocks": clocks,
             "vs_paper_2080ti_batch1": round(value / PAPER_2080TI_FMAPS, 1),
         }
         if gather_ms is not None:
             result["gather_ms"] = round(gather_ms, 4)
+            result["nccl_debug_file"] = nccl_log
     # e2e + pipeline: each rank measures its own, max over ranks
     e2e_ms = _e2e(args, cfg, G, R, M, device, ctx, stream)
     pipe_ms = _pipeline(args, cfg, t, device, stream)
@@ -279,15 +305,19 @@ def run_ours(args):
         e2e_ms, pipe_ms, f64_ms = (float(x) for x in tt.tolist())
     if rank == 0:
         nbytes = b * k * k * 4
-        result["e2e"] = {"value": round(world * b / (e2e_ms * 1e-3), 2), "unit": UNIT,
+        result["e2e"] = {"value": round(gb / (e2e_ms * 1e-3), 2), "unit": UNIT,
                          "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes,
                          "ms_per_step": round(e2e_ms, 4),
-                         "api": "fmap_solve_f32 (host G,R,M pinned -> C): 8 pair chunks, H2D / validation+solve / D2H overlapped on 2 copy + 2 compute streams, device validation incl."}
-        result["pipeline"] = {"value": round(world * b / (pipe_ms * 1e-3), 2), "unit": UNIT,
+                         "api": "fmap_solve_f32 with DEFAULT options (compute_residual=1, as the reference always "
+                                "reports max_residual_norm): host G,R,M pinned -> C, 8 pair chunks, H2D / "
+                                "validation+solve+residual / D2H overlapped on 2 copy + 2 compute streams"
+                                + ("; per rank on its pair range, max over ranks (no host-side gather)"
+                                   if world > 1 else "")}
+        result["pipeline"] = {"value": round(gb / (pipe_ms * 1e-3), 2), "unit": UNIT,
                               "ms_per_step": round(pipe_ms, 4),
                               "api": "fmap_pipeline_f32_dev: Phi,Mass,F,ev -> projection, Gram/RHS, "
                                      "fused resolvent mask, solver (device-resident)"}
-        result["f64_route"] = {"value": round(world * b / (f64_ms * 1e-3), 2), "unit": UNIT,
+        result["f64_route"] = {"value": round(gb / (f64_ms * 1e-3), 2), "unit": UNIT,
                                "ms_per_step": round(f64_ms, 4), "dtype": "f64",
                                "api": "fmap_solve_f64_dev (the reference's default precision; same "
                                       "device-resident G, R, M in f64, validation + solve)"}
@@ -321,10 +351,10 @@ def _e2e(args, cfg, G, R, M, device, ctx, stream) -> float:
     import torch
     import ctypes as C
     from paper_2604_10377_b200 import fmsolve, _lib
-    b, k = cfg.batch, cfg.k
+    b, k = G.shape[0], cfg.k
     hG, hR, hM = (x.cpu().pin_memory() for x in (G, R, M))
     hC = torch.empty_like(hG).pin_memory()
-    opts = fmsolve.SolverOptions(compute_residual=False).to_c()
+    opts = fmsolve.SolverOptions().to_c()  # the reference's defaults (residual reported)
     P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
     L, h = ctx._lib, ctx.handle
 
@@ -368,7 +398,7 @@ def _f64_route(args, cfg, G, R, M, device, ctx, stream) -> float:
     import torch
     import ctypes as C
     from paper_2604_10377_b200 import fmsolve, _lib
-    b, k = cfg.batch, cfg.k
+    b, k = G.shape[0], cfg.k
     G64, R64, M64 = (x.double().contiguous() for x in (G, R, M))
     C64 = torch.empty_like(G64)
     opts = fmsolve.SolverOptions(compute_residual=False, rcond_threshold=-1.0).to_c()
@@ -672,15 +702,30 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg2")
-    ap.add_argument("--gather", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="(kept for compatibility: N > 1 always gathers)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: W >= 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
+
+
+def _self_launch(n: int) -> int:
+    """`--gpus N` outside torchrun: one rank per GPU through torch.distributed.run
+    (rendezvous on 127.0.0.1), same arguments."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

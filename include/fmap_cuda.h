@@ -71,7 +71,10 @@ typedef struct fmap_report {
   int64_t failing_system;    /* SingularSystemError::system(); -1 when none            */
   uint64_t required_bytes;   /* MemoryCapExceeded::required_bytes()                    */
   uint64_t cap_bytes;        /* MemoryCapExceeded::cap_bytes()                         */
-  double min_rcond;          /* smallest rcond estimate over all systems               */
+  double min_rcond;          /* smallest rcond over all systems: the comparison-matrix  */
+                             /* certificate (a lower bound) or, where that was          */
+                             /* inconclusive, the exact Hager/Higham estimate           */
+  int64_t rcond_exact_systems; /* systems that needed the exact estimator               */
 } fmap_report;
 
 typedef struct fmap_ctx fmap_ctx;
@@ -165,6 +168,9 @@ int64_t fmap_max_resolution(fmap_ctx* ctx);
 /* Number of solver-family kernel launches issued by the last call (evidence
  * for bench.py's gpu_launches). */
 int64_t fmap_last_launch_count(const fmap_ctx* ctx);
+/* Names of those kernels, comma-separated, in launch order (e.g.
+ * "validate_kernel,gram_check_kernel,chol_tc_kernel"); valid until the next call. */
+const char* fmap_last_launches(const fmap_ctx* ctx);
 
 #ifdef __cplusplus
 }

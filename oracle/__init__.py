@@ -73,6 +73,8 @@ def lib() -> C.CDLL:
             ("oracle_generate_instance", I, [I, I, C.c_uint64, P, P, P, P]),
             ("oracle_randn", None, [I, I, C.c_uint64, P]),
             ("oracle_hardware_threads", C.c_uint, []),
+            ("oracle_rcond_f64", D, [I, P]),
+            ("oracle_rcond_f32", F, [I, P]),
         ]:
             fn = getattr(L, name)
             fn.restype, fn.argtypes = res, args
@@ -198,6 +200,14 @@ def random_problem(k, d, seed, kind=0, sigma=0.5):
     M = mask(kind, e1, e2, sigma)
     G, R = normal_equations(a, b)
     return G, R, M, a, b
+
+
+def rcond(A, dtype=np.float32) -> float:
+    """The reference's rcond estimate of one assembled system A (solver.hpp:158-166:
+    PartialPivLU + Hager/Higham); -1 on an exact zero pivot."""
+    A = _c(A, dtype)
+    fn = lib().oracle_rcond_f64 if dtype == np.float64 else lib().oracle_rcond_f32
+    return float(fn(A.shape[0], _p(A)))
 
 
 def hardware_threads() -> int:

@@ -683,4 +683,32 @@ void oracle_randn(int rows, int cols, uint64_t seed, double* out) {
 
 unsigned oracle_hardware_threads(void) { return std::thread::hardware_concurrency(); }
 
+// The reference's rcond of one assembled row system A (k x k, row-major):
+// PartialPivLU + the Hager/Higham estimate, exactly what factor_solve_inplace
+// compares with the threshold (solver.hpp:158-166).  -1 on an exact zero pivot.
+double oracle_rcond_f64(int k, const double* a) {
+  std::vector<double> m(a, a + (size_t)k * k);
+  double l1norm = 0;
+  for (int c = 0; c < k; ++c) {
+    double s = 0;
+    for (int r = 0; r < k; ++r) s += std::abs(m[(size_t)r * k + c]);
+    l1norm = std::max(l1norm, s);
+  }
+  LU<double> lu(m.data(), k);
+  if (lu.has_zero_pivot()) return -1.0;
+  return format_rcond(l1norm, lu);
+}
+float oracle_rcond_f32(int k, const float* a) {
+  std::vector<float> m(a, a + (size_t)k * k);
+  float l1norm = 0;
+  for (int c = 0; c < k; ++c) {
+    float s = 0;
+    for (int r = 0; r < k; ++r) s += std::abs(m[(size_t)r * k + c]);
+    l1norm = std::max(l1norm, s);
+  }
+  LU<float> lu(m.data(), k);
+  if (lu.has_zero_pivot()) return -1.f;
+  return format_rcond(l1norm, lu);
+}
+
 }  // extern "C"

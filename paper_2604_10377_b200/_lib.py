@@ -31,7 +31,7 @@ EXPORTED = [
     "fmap_solve_ev_f32_dev", "fmap_mask_f32", "fmap_mask_f32_dev",
     "fmap_normal_equations_f32", "fmap_normal_equations_f32_dev", "fmap_project_f32_dev",
     "fmap_residual_f32_dev", "fmap_pipeline_f32_dev", "fmap_max_resolution",
-    "fmap_last_launch_count", "fmap_solve_f64", "fmap_solve_f64_dev",
+    "fmap_last_launch_count", "fmap_last_launches", "fmap_solve_f64", "fmap_solve_f64_dev",
 ]
 
 
@@ -56,6 +56,7 @@ class ReportC(C.Structure):
         ("required_bytes", C.c_uint64),
         ("cap_bytes", C.c_uint64),
         ("min_rcond", C.c_double),
+        ("rcond_exact_systems", C.c_int64),
     ]
 
 
@@ -98,8 +99,11 @@ def load() -> C.CDLL:
                                           I, F, F, opt, P, P, rep]),
             "fmap_max_resolution": (I64, [P]),
             "fmap_last_launch_count": (I64, [P]),
+            "fmap_last_launches": (C.c_char_p, [P]),
         }
         for name, (res, args) in sig.items():
+            if os.environ.get("FMAP_LIB_VARIANT") and not hasattr(lib, name):
+                continue  # developer A/B against an older build
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
@@ -151,6 +155,12 @@ class Context:
     @property
     def last_launch_count(self) -> int:
         return int(self._lib.fmap_last_launch_count(self.handle))
+
+    @property
+    def last_launches(self) -> list[str]:
+        """Kernel names the last call launched, in order (fmap_last_launches)."""
+        names = self._lib.fmap_last_launches(self.handle).decode()
+        return names.split(",") if names else []
 
 
 _contexts: dict[int, Context] = {}

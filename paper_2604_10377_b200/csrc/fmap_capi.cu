@@ -35,11 +35,14 @@ struct fmap_ctx {
   size_t arena_bytes = 0;
   void* scr = nullptr;
   size_t scr_bytes = 0;
-  // control block: [0] fail_min (u64) | [8] rcond bits (u32) | [12] flags (u32)
+  // control block: [0] fail_min (u64) | [8] rcond bits (u32) | [12] flags (u32) |
+  // [16] systems whose rcond needed the exact Hager/Higham estimator (u32)
   unsigned char* d_ctrl = nullptr;
   unsigned char* h_ctrl = nullptr;  // pinned
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int64_t launches = 0;
+  unsigned last_exact = 0;     // systems of the last call that ran the exact rcond estimator
+  int64_t launches = 0;        // kernels launched by the last call
+  std::string launch_names;    // their names, comma-separated (fmap_last_launches)
   int max_smem_optin = 0;
   int num_sms = 0;
   // host-buffer pipelining (fmap_solve_f32): second compute stream + copy stream
@@ -67,6 +70,7 @@ int set_err(fmap_ctx* ctx, int code, const std::string& msg) {
 unsigned long long* d_fail(fmap_ctx* c) { return reinterpret_cast<unsigned long long*>(c->d_ctrl); }
 unsigned* d_rcond(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 8); }
 unsigned* d_flags(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 12); }
+unsigned* d_nexact(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 16); }
 
 // Grow-only device arena.  Growth drops the old contents (the stream is drained
 // first, so no queued kernel still reads it): callers reserve BEFORE carving.
@@ -87,6 +91,16 @@ int arena_reserve(fmap_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->arena, &
 int scratch_reserve(fmap_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->scr, &ctx->scr_bytes, bytes); }
 
 // Every entry point runs on the context's device and restores the caller's.
+// Records the kernels one C-ABI call launches into its context.
+struct LaunchScope {
+  fmap_ctx* ctx;
+  explicit LaunchScope(fmap_ctx* c) : ctx(c) { clear_launch_log(); }
+  ~LaunchScope() {
+    ctx->launches = launch_log_count();
+    ctx->launch_names = launch_log();
+  }
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -121,27 +135,27 @@ size_t carve_size(std::initializer_list<size_t> bytes) {
 }
 
 int reset_ctrl(fmap_ctx* ctx) {
-  unsigned char init[16];
+  unsigned char init[24];
   const unsigned long long nf = kNoFail;
   const unsigned fmax = 0x7f7fffffu;  // FLT_MAX bits
-  const unsigned zero = 0;
+  std::memset(init, 0, sizeof init);
   std::memcpy(init, &nf, 8);
   std::memcpy(init + 8, &fmax, 4);
-  std::memcpy(init + 12, &zero, 4);
-  std::memcpy(ctx->h_ctrl, init, 16);
-  FMAP_CK(ctx, cudaMemcpyAsync(ctx->d_ctrl, ctx->h_ctrl, 16, cudaMemcpyHostToDevice, ctx->stream));
+  std::memcpy(ctx->h_ctrl, init, 24);
+  FMAP_CK(ctx, cudaMemcpyAsync(ctx->d_ctrl, ctx->h_ctrl, 24, cudaMemcpyHostToDevice, ctx->stream));
   return FMAP_OK;
 }
 
 int read_ctrl(fmap_ctx* ctx, unsigned long long* fail, float* rcond, unsigned* flags) {
-  FMAP_CK(ctx, cudaMemcpyAsync(ctx->h_ctrl + 16, ctx->d_ctrl, 16, cudaMemcpyDeviceToHost,
+  FMAP_CK(ctx, cudaMemcpyAsync(ctx->h_ctrl + 32, ctx->d_ctrl, 24, cudaMemcpyDeviceToHost,
                                ctx->stream));
   FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
-  std::memcpy(fail, ctx->h_ctrl + 16, 8);
+  std::memcpy(fail, ctx->h_ctrl + 32, 8);
   unsigned rb;
-  std::memcpy(&rb, ctx->h_ctrl + 24, 4);
+  std::memcpy(&rb, ctx->h_ctrl + 40, 4);
   std::memcpy(rcond, &rb, 4);
-  std::memcpy(flags, ctx->h_ctrl + 28, 4);
+  std::memcpy(flags, ctx->h_ctrl + 44, 4);
+  std::memcpy(&ctx->last_exact, ctx->h_ctrl + 48, 4);
   return FMAP_OK;
 }
 
@@ -175,11 +189,7 @@ std::string flags_message(unsigned f) {
   return "invalid input";
 }
 
-int max_resolution(fmap_ctx* ctx) {
-  int k = 4;
-  while (solver_smem_bytes(k + 4) <= (size_t)ctx->max_smem_optin) k += 4;
-  return k;
-}
+int max_resolution(fmap_ctx* ctx) { return tc_max_resolution(ctx->max_smem_optin); }
 
 // Core solve on device buffers. mask_mode 0: d_mask; 1/2: from eigenvalues.
 int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float* R,
@@ -200,14 +210,13 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   const int kmax = max_resolution(ctx);
   if (k > kmax)
     return set_err(ctx, FMAP_INVALID_ARGUMENT,
-                   "k = " + std::to_string(k) + " exceeds the single-CTA solver limit " +
+                   "k = " + std::to_string(k) + " exceeds the tensor-memory solver limit " +
                        std::to_string(kmax) + " on this device");
   const size_t kk = (size_t)k * k;
   const size_t nsys = (size_t)b * k;
   const bool need_mask_scratch = opts.compute_residual && mask_mode != 0;
   const size_t res_partial = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
-  const bool use_tc = tc_supported((int)k, ctx->max_smem_optin) && !std::getenv("FMAP_FORCE_SINGLE");
-  const size_t tc_bytes = use_tc ? tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms) : 0;
+  const size_t tc_bytes = tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms);
   const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
                                      need_mask_scratch ? (size_t)b * kk * sizeof(float) : 0,
                                      (size_t)k * sizeof(float), tc_bytes, (size_t)b * k * sizeof(float)});
@@ -234,20 +243,16 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   float* rowsum = cv.take<float>((size_t)b * k);
 
   if ((st = reset_ctrl(ctx))) return st;
-  ctx->launches = 0;
   if (device_validate) {
     if (mask_mode == 0) {
       FMAP_CK(ctx, launch_validate(G, R, M, (size_t)b * kk, d_flags(ctx), ctx->stream));
     } else {
       FMAP_CK(ctx, launch_validate(G, R, nullptr, (size_t)b * kk, d_flags(ctx), ctx->stream));
       FMAP_CK(ctx, launch_validate_ev(ev1, ev2, (size_t)b * k, d_flags(ctx), ctx->stream));
-      ctx->launches++;
     }
-    ctx->launches++;
   }
   // symmetry check + row 1-norms of G (rcond certificate input)
   FMAP_CK(ctx, launch_gram_check(G, b, (int)k, rowsum, d_flags(ctx), ctx->stream));
-  ctx->launches++;
 
   SolveParams p{};
   p.gram = G;
@@ -269,7 +274,8 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   p.fail_min = d_fail(ctx);
   p.rcond_min_bits = d_rcond(ctx);
   p.flags = d_flags(ctx);
-  p.tc_scratch = use_tc ? tc_scr : nullptr;
+  p.rcond_exact = d_nexact(ctx);
+  p.tc_scratch = tc_scr;
   p.gram_rowsum = rowsum;
 
   // debug: FMAP_TRACE_FILE=<path> dumps per-warp clock64 phase stamps of one block
@@ -282,8 +288,6 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     const char* tb = std::getenv("FMAP_TRACE_BLOCK");
     p.trace_block = tb ? std::atoi(tb) : 0;
   }
-  p.force_single = std::getenv("FMAP_FORCE_SINGLE") ? 1 : 0;
-  p.pair_shared_smsp = std::getenv("FMAP_PAIR_SHARED") ? 1 : 0;
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, launch_chol_solve(p, mask_mode, ctx->stream));
   if (d_trace) {
@@ -297,7 +301,6 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     cudaFree(d_trace);
     p.trace = nullptr;
   }
-  ctx->launches++;
   if (opts.inject_fault) {
     // solver.hpp:269-273: negate the largest-|.| entry of row 0 of system 0's
     // assembled LHS.  Solved exactly as a rank-one update of the SPD system.
@@ -343,7 +346,6 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     pz.rhs_unit = 0;
     FMAP_CK(ctx, launch_chol_solve(pz, mask_mode, ctx->stream));
     FMAP_CK(ctx, launch_fault_combine(C, zrow, (int)k, w, alpha, d_fail(ctx), 0ull, ctx->stream));
-    ctx->launches += 2;
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
 
@@ -353,10 +355,8 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
       FMAP_CK(ctx, launch_mask(ev1, ev2, b, (int)k, mask_mode == 1 ? 1 : 0, sigma, mask_scratch,
                                ctx->stream));
       Muse = mask_scratch;
-      ctx->launches++;
     }
     FMAP_CK(ctx, launch_residual(C, G, R, Muse, b, (int)k, lambda, partial, res_out, ctx->stream));
-    ctx->launches += 2;
   }
 
   unsigned long long fail;
@@ -368,6 +368,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   if (rep) {
     rep->wall_seconds = ms * 1e-3;
     rep->min_rcond = rcond;
+    rep->rcond_exact_systems = ctx->last_exact;
   }
   if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, flags_message(flags));
   if (fail != kNoFail) {
@@ -453,12 +454,12 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   p.fail_min = d_fail(ctx);
   p.rcond_min_bits = d_rcond(ctx);
   p.flags = d_flags(ctx);
+  p.rcond_exact = d_nexact(ctx);
   p.gram = dG;
   p.rhs = dR;
   p.mask = dM;
   p.C = dC;
   p.gram_rowsum = rowsum;
-  ctx->launches = 0;
   for (int c = 0; c < nchunk; ++c) {  // all H2D first: the copy stream never waits on the solver
     const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
     if (nq <= 0) break;
@@ -481,11 +482,9 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
     p.sys_offset = q0 * k;
     p.tc_scratch = scr[c & 1];
     FMAP_CK(ctx, launch_chol_solve(p, 0, s));
-    ctx->launches += 3;
     if (opts.compute_residual) {  // check_stationarity per chunk (solver.hpp:314-320), overlapped
       FMAP_CK(ctx, launch_residual(dC + off, dG + off, dR + off, dM + off, nq, (int)k, lambda,
                                    partial + (size_t)c * residual_partial_count(cb, (int)k), res_out + q0, s));
-      ctx->launches += 2;
     }
     FMAP_CK(ctx, cudaEventRecord(done, s));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy2, done, 0));
@@ -505,6 +504,7 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   if (rep) {
     rep->wall_seconds = ms * 1e-3;
     rep->min_rcond = rcond;
+    rep->rcond_exact_systems = ctx->last_exact;
   }
   if (flags || fail != kNoFail) std::memset(C_out, 0, bytes);  // no partial results
   if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, flags_message(flags));
@@ -564,13 +564,11 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
   double* sq = cv.take<double>((size_t)b);
   double* zrow = cv.take<double>((size_t)k);
   if ((st = reset_ctrl(ctx))) return st;
-  ctx->launches = 0;
   FMAP_CK(ctx, launch_validate_f64(G, R, M, (size_t)b * kk, d_flags(ctx), ctx->stream));
   const double rthr = opts.rcond_threshold < 0.f ? 1e-14 : (double)opts.rcond_threshold;
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, launch_chol_f64(G, R, M, C, (int)k, b * k, lambda, (double)opts.ridge, rthr, -1, d_fail(ctx),
                                d_rcond(ctx), ctx->stream));
-  ctx->launches += 2;
   if (opts.inject_fault) {  // solver.hpp:269-273, as solve_core
     std::vector<double> g0(k);
     double m00 = 0.0;
@@ -589,12 +587,10 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
     FMAP_CK(ctx, launch_chol_f64(G, R, M, zrow, (int)k, 1, lambda, (double)opts.ridge, rthr, 0, d_fail(ctx),
                                  d_rcond(ctx), ctx->stream));
     FMAP_CK(ctx, launch_fault_combine_f64(C, zrow, (int)k, w, alpha, d_fail(ctx), ctx->stream));
-    ctx->launches += 2;
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
   if (opts.compute_residual) {
     FMAP_CK(ctx, launch_residual_f64(C, G, R, M, b, (int)k, lambda, sq, ctx->stream));
-    ctx->launches++;
   }
   unsigned long long fail;
   float rcond;
@@ -605,6 +601,7 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
   if (rep) {
     rep->wall_seconds = ms * 1e-3;
     rep->min_rcond = rcond;
+    rep->rcond_exact_systems = ctx->last_exact;
   }
   if (flags) return set_err(ctx, FMAP_INVALID_ARGUMENT, flags_message(flags));
   if (fail != kNoFail) {
@@ -705,11 +702,14 @@ int64_t fmap_max_resolution(fmap_ctx* ctx) { return ctx ? max_resolution(ctx) : 
 
 int64_t fmap_last_launch_count(const fmap_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+const char* fmap_last_launches(const fmap_ctx* ctx) { return ctx ? ctx->launch_names.c_str() : ""; }
+
 int fmap_solve_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gram,
                        const float* d_rhs, const float* d_mask, float lambda,
                        const fmap_solver_options* opts, float* d_C, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   return solve_core(ctx, b, k, d_gram, d_rhs, d_mask, nullptr, nullptr, 0, 0.f, lambda, opts,
                     d_C, report, true, 0);
 }
@@ -720,6 +720,7 @@ int fmap_solve_ev_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gr
                           const fmap_solver_options* opts, float* d_C, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   if (mask_kind != FMAP_MASK_COMMUTATIVITY && mask_kind != FMAP_MASK_RESOLVENT)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
   return solve_core(ctx, b, k, d_gram, d_rhs, nullptr, d_ev1, d_ev2,
@@ -732,6 +733,7 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
                    float* C_out, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   init_report(report);
   if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
   if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
@@ -750,8 +752,7 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   // residual); FMAP_PIPELINE=<chunks> overrides the default (1 = unpipelined)
   const char* pipe = std::getenv("FMAP_PIPELINE");
   const int nchunk = pipe ? std::max(1, std::min(16, std::atoi(pipe))) : 8;
-  if (nchunk > 1 && !o.inject_fault && b >= 2 * nchunk && !std::getenv("FMAP_SOLVER") &&
-      k <= max_resolution(ctx) && tc_supported((int)k, ctx->max_smem_optin))
+  if (nchunk > 1 && !o.inject_fault && b >= 2 * nchunk && k <= max_resolution(ctx))
     return solve_host_pipelined(ctx, b, k, gram, rhs, mask, lambda, o, C_out, report, nchunk);
   if (o.has_memory_cap && staging > o.memory_cap_bytes) {
     if (report) {
@@ -787,6 +788,7 @@ int fmap_solve_f64_dev(fmap_ctx* ctx, int64_t b, int64_t k, const double* d_gram
                        fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   return solve_core_f64(ctx, b, k, d_gram, d_rhs, d_mask, lambda, opts, d_C_out, report, 0);
 }
 
@@ -794,6 +796,7 @@ int fmap_solve_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* gram, cons
                    double lambda, const fmap_solver_options* opts, double* C_out, fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   init_report(report);
   if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
   if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
@@ -835,6 +838,7 @@ int fmap_mask_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_ev1,
                       const float* d_ev2, int mask_kind, float sigma, float* d_mask_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalue vectors must be non-empty");
   if (mask_kind != 0 && mask_kind != 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
   if (mask_kind == 1 && !(sigma > 0.f))
@@ -842,13 +846,10 @@ int fmap_mask_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_ev1,
   int st = reset_ctrl(ctx);
   if (st) return st;
   FMAP_CK(ctx, launch_validate_ev(d_ev1, d_ev2, (size_t)b * k, d_flags(ctx), ctx->stream));
-  ctx->launches = 1;
   if (mask_kind == 1) {  // masks.hpp:58-59: the resolvent mask normalises by the pair's max eigenvalue
     FMAP_CK(ctx, launch_ev_max_check(d_ev1, d_ev2, b, (int)k, d_flags(ctx), ctx->stream));
-    ctx->launches++;
   }
   FMAP_CK(ctx, launch_mask(d_ev1, d_ev2, b, (int)k, mask_kind, sigma, d_mask_out, ctx->stream));
-  ctx->launches++;
   unsigned long long fail;
   float rc;
   unsigned flags;
@@ -862,6 +863,7 @@ int fmap_mask_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* ev1, const f
                   int mask_kind, float sigma, float* mask_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "eigenvalue vectors must be non-empty");
   if (mask_kind != 0 && mask_kind != 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "unknown mask kind");
   // masks.hpp:48-53 / 79-89 validation order
@@ -892,7 +894,6 @@ int fmap_mask_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* ev1, const f
   FMAP_CK(ctx, cudaMemcpyAsync(d1, ev1, evb, cudaMemcpyHostToDevice, ctx->stream));
   FMAP_CK(ctx, cudaMemcpyAsync(d2, ev2, evb, cudaMemcpyHostToDevice, ctx->stream));
   FMAP_CK(ctx, launch_mask(d1, d2, b, (int)k, mask_kind, sigma, dm, ctx->stream));
-  ctx->launches = 1;
   FMAP_CK(ctx, cudaMemcpyAsync(mask_out, dm, mb, cudaMemcpyDeviceToHost, ctx->stream));
   FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
   return FMAP_OK;
@@ -903,11 +904,11 @@ int fmap_normal_equations_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d
                                   float* d_rhs) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   if (b < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "descriptor A must be non-empty");
   FMAP_CK(ctx, launch_gemm_nt(d_A, d_A, b, (int)k, (int)k, (int)d, d_gram, ctx->stream));
   FMAP_CK(ctx, launch_gemm_nt(d_B, d_A, b, (int)k, (int)k, (int)d, d_rhs, ctx->stream));
-  ctx->launches = 2;
   return FMAP_OK;
 }
 
@@ -915,6 +916,7 @@ int fmap_normal_equations_f32(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d, co
                               const float* B, float* gram_out, float* rhs_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   if (b < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "descriptor A must be non-empty");
   const size_t nab = (size_t)b * k * d, ng = (size_t)b * k * k;
@@ -941,10 +943,10 @@ int fmap_project_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t
                          float* d_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   if (b < 1 || n < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "basis and features must be non-empty");
   FMAP_CK(ctx, launch_project(d_phi, d_mass, d_F, b, n, (int)k, (int)d, d_out, ctx->stream));
-  ctx->launches = 1;
   return FMAP_OK;
 }
 
@@ -953,13 +955,13 @@ int fmap_residual_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_C,
                           float lambda, double* d_out) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   if (b < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
   const size_t np = residual_partial_count(b, (int)k);
   int st = scratch_reserve(ctx, np * sizeof(double));
   if (st) return st;
   FMAP_CK(ctx, launch_residual(d_C, d_gram, d_rhs, d_mask, b, (int)k, lambda,
                                reinterpret_cast<double*>(ctx->scr), d_out, ctx->stream));
-  ctx->launches = 2;
   return FMAP_OK;
 }
 
@@ -972,6 +974,7 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
                           fmap_report* report) {
   if (!ctx) return FMAP_INVALID_ARGUMENT;
   DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
   init_report(report);
   if (b < 1 || n1 < 1 || n2 < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "pipeline dimensions must be positive");
@@ -1004,12 +1007,10 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
     FMAP_CK(ctx, launch_gemm_nt(B, B, b, (int)k, (int)k, (int)d, G2, ctx->stream));
     FMAP_CK(ctx, launch_gemm_nt(A, B, b, (int)k, (int)k, (int)d, R2, ctx->stream));
   }
-  int64_t pre = bidir ? 6 : 4;
   // solve_core carves its own scratch after host_staging_bytes = our scratch
   const int mm = mask_kind == FMAP_MASK_RESOLVENT ? 1 : 2;
   st = solve_core(ctx, b, k, G, R, nullptr, d_ev1, d_ev2, mm, sigma, lambda, &o, d_Cxy, report,
                   true, scratch);
-  int64_t launches = pre + ctx->launches;
   if (st) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1020,7 +1021,6 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
     // reverse direction: source/target swap, mask(ev2, ev1) = M^T
     st = solve_core(ctx, b, k, G2, R2, nullptr, d_ev2, d_ev1, mm, sigma, lambda, &o, d_Cyx, &r2,
                     true, scratch);
-    launches += ctx->launches;
     if (st) {
       if (report) *report = r2;
       cudaEventDestroy(e0);
@@ -1030,6 +1030,7 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
     if (report) {
       report->max_residual = std::max(report->max_residual, r2.max_residual);
       report->min_rcond = std::min(report->min_rcond, r2.min_rcond);
+      report->rcond_exact_systems += r2.rcond_exact_systems;
     }
   }
   FMAP_CK(ctx, cudaEventRecord(e1, ctx->stream));
@@ -1039,7 +1040,6 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
   if (report) report->wall_seconds = ms * 1e-3;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  ctx->launches = launches;
   return FMAP_OK;
 }
 

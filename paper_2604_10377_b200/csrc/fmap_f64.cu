@@ -21,6 +21,7 @@
 // Verdict as the f32 route: non-positive / non-finite pivot, rcond estimate
 // min(pivot)/max|diag| below the threshold, or a non-finite solution; lowest
 // failing global system index wins.
+#include "fmap_kernels.cuh"
 #include "fmap_solver.cuh"
 
 #include <cuda_runtime.h>
@@ -340,6 +341,7 @@ __global__ void fault_combine_f64_kernel(double* __restrict__ x, const double* _
 
 cudaError_t launch_fault_combine_f64(double* x, const double* z, int k, int w, double alpha,
                                      unsigned long long* fail_min, cudaStream_t st) {
+  note_launch("fault_combine_f64_kernel");
   fault_combine_f64_kernel<<<1, 256, 0, st>>>(x, z, k, w, alpha, fail_min);
   return cudaGetLastError();
 }
@@ -363,6 +365,7 @@ cudaError_t launch_chol_f64(const double* G, const double* R, const double* M, d
   const int per_sm = (int)std::max<size_t>(1, 233472 / (smem + 1024));
   const int64_t maxgrid = (int64_t)sms * per_sm;
   const unsigned grid = (unsigned)(nsys < maxgrid ? nsys : maxgrid);
+  note_launch("chol_f64_kernel");
   chol_f64_kernel<<<grid, kT64, smem, st>>>(G, R, M, C, k, nsys, lambda, ridge, rthr, rhs_unit, fail_min,
                                             rcond_min_bits);
   return cudaGetLastError();
@@ -371,6 +374,7 @@ cudaError_t launch_chol_f64(const double* G, const double* R, const double* M, d
 cudaError_t launch_validate_f64(const double* g, const double* r, const double* m, size_t n, unsigned* flags,
                                 cudaStream_t st) {
   const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 8);
+  note_launch("validate_f64_kernel");
   validate_f64_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(g, r, m, n, flags);
   return cudaGetLastError();
 }
@@ -380,6 +384,7 @@ cudaError_t launch_residual_f64(const double* Cm, const double* G, const double*
   cudaError_t e = cudaMemsetAsync(sq, 0, (size_t)b * sizeof(double), st);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)k, (unsigned)b);
+  note_launch("residual_f64_kernel");
   residual_f64_kernel<<<grid, 128, 0, st>>>(Cm, G, R, M, k, lambda, sq);
   return cudaGetLastError();
 }

@@ -13,6 +13,23 @@
 namespace fmap {
 
 namespace {
+thread_local std::string g_launch_log;
+thread_local int g_launch_count = 0;
+}  // namespace
+
+void note_launch(const char* kernel) {
+  if (!g_launch_log.empty()) g_launch_log += ',';
+  g_launch_log += kernel;
+  ++g_launch_count;
+}
+void clear_launch_log() {
+  g_launch_log.clear();
+  g_launch_count = 0;
+}
+const char* launch_log() { return g_launch_log.c_str(); }
+int launch_log_count() { return g_launch_count; }
+
+namespace {
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -402,6 +419,7 @@ __global__ void fault_combine_kernel(float* __restrict__ x, const float* __restr
 cudaError_t launch_mask(const float* ev1, const float* ev2, int64_t b, int k, int kind,
                         float sigma, float* out, cudaStream_t st) {
   dim3 grid((k + 7) / 8, (unsigned)b);
+  note_launch("mask_kernel");
   mask_kernel<<<grid, 256, 0, st>>>(ev1, ev2, k, kind, sigma, out);
   return cudaGetLastError();
 }
@@ -409,6 +427,7 @@ cudaError_t launch_mask(const float* ev1, const float* ev2, int64_t b, int k, in
 cudaError_t launch_validate(const float* g, const float* r, const float* m, size_t n,
                             unsigned* flags, cudaStream_t st) {
   const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 8);
+  note_launch("validate_kernel");
   validate_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(g, r, m, n, flags);
   return cudaGetLastError();
 }
@@ -416,17 +435,20 @@ cudaError_t launch_validate(const float* g, const float* r, const float* m, size
 cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsigned* flags,
                                cudaStream_t st) {
   const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 4);
+  note_launch("validate_ev_kernel");
   validate_ev_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(e1, e2, n, flags);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ev_max_check(const float* e1, const float* e2, int64_t b, int k, unsigned* flags,
                                 cudaStream_t st) {
+  note_launch("ev_max_check_kernel");
   ev_max_check_kernel<<<(unsigned)((b + 7) / 8), 256, 0, st>>>(e1, e2, b, k, flags);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gram_check(const float* G, int64_t b, int k, float* S, unsigned* flags, cudaStream_t st) {
+  note_launch("gram_check_kernel");
   gram_check_kernel<<<(unsigned)(b * ((k + 31) / 32)), 256, 0, st>>>(G, k, S, flags);
   return cudaGetLastError();
 }
@@ -434,6 +456,7 @@ cudaError_t launch_gram_check(const float* G, int64_t b, int k, float* S, unsign
 cudaError_t launch_gemm_nt(const float* X, const float* Y, int64_t b, int M, int N, int K,
                            float* out, cudaStream_t st) {
   dim3 grid((N + GT - 1) / GT, (M + GT - 1) / GT, (unsigned)b);
+  note_launch("gemm_nt_kernel");
   gemm_nt_kernel<<<grid, 256, 0, st>>>(X, Y, M, N, K, out);
   return cudaGetLastError();
 }
@@ -456,6 +479,7 @@ cudaError_t launch_project(const float* phi, const float* mass, const float* F, 
     if (e != cudaErrorNotSupported) return e;
   }
   dim3 grid((d + PJ_T - 1) / PJ_T, (k + PJ_T - 1) / PJ_T, (unsigned)b);
+  note_launch("project_kernel");
   project_kernel<<<grid, 256, 0, st>>>(phi, mass, F, n, k, d, out);
   return cudaGetLastError();
 }
@@ -465,10 +489,12 @@ cudaError_t launch_residual(const float* C, const float* G, const float* R, cons
                             cudaStream_t st) {
   const int nchunk = (k + RES_ROWS - 1) / RES_ROWS;
   dim3 grid(nchunk, (unsigned)b);
+  note_launch("residual_partial_kernel");
   residual_partial_kernel<<<grid, 256, RES_ROWS * k * sizeof(float), st>>>(C, G, R, M, k, lambda,
                                                                           partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  note_launch("residual_finish_kernel");
   residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, nchunk, (int)b,
                                                                       out);
   return cudaGetLastError();
@@ -481,6 +507,7 @@ size_t residual_partial_count(int64_t b, int k) {
 cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,
                                  unsigned long long* fail_min, unsigned long long sys,
                                  cudaStream_t st) {
+  note_launch("fault_combine_kernel");
   fault_combine_kernel<<<1, 256, 0, st>>>(x, z, k, w, alpha, fail_min, sys);
   return cudaGetLastError();
 }

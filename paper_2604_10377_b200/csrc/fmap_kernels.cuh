@@ -2,12 +2,20 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 #include <algorithm>
 #include <cuda_runtime.h>
 
 #include "fmap_solver.cuh"
 
 namespace fmap {
+
+// Per-thread log of the kernels the current C-ABI call launched (evidence for
+// fmap_last_launches / bench.py's gpu_launches).
+void note_launch(const char* kernel);
+void clear_launch_log();
+const char* launch_log();
+int launch_log_count();
 
 cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream);
 

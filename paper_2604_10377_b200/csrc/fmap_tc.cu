@@ -38,6 +38,7 @@
 //
 // Singular = non-positive / non-finite pivot, rcond estimate min(pivot)/max|diag|
 // below the threshold, or a non-finite solution (lowest failing index wins).
+#include "fmap_kernels.cuh"
 #include "fmap_solver.cuh"
 
 #include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
@@ -75,6 +76,7 @@ struct TcLayout {
   int cps;  // CTAs per SM
   // offsets in floats from the dynamic smem base
   int off_hi, off_lo, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_a0, off_stg, off_misc;
+  int off_uv, off_wv, off_hv;  // rcond (back-substitution warp): comparison solves u, w; Hager vectors
   int floats;
   long long lb;  // floats of one L scratch slot (global memory)
 };
@@ -127,6 +129,9 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.off_xv = o;  o += ns * L.K16;               // back substitution: x (per system)
   L.off_lb = o;  o += ns * 2 * lbs;             // back substitution: L blocks (per system, 2 buffers)
   L.off_zb = o;  o += ns * 16;
+  L.off_uv = o;  o += ns * L.K16;               // back substitution: u = M(L)^{-1} e (per system)
+  L.off_wv = o;  o += ns * L.K16;               // back substitution: w = M(L)^{-T} e (per system)
+  L.off_hv = o;  o += ns * 3 * L.K16;           // back substitution: Hager estimator vectors (per system)
   o = (o + 31) & ~31;                           // 128 B aligned (TMA destination)
   L.off_a0 = o;  o += ns * L.K16 * 16;          // panel-0 columns of every row (float4 [h][t4][row])
   o = (o + 255) & ~255;                         // 1 KB aligned (TMA destination)
@@ -158,10 +163,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   do {
     asm volatile(
         "{\n.reg .pred P1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, P1;\n}"
         : "=r"(ok)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(0x989680u)
         : "memory");
   } while (!ok);
 }
@@ -472,20 +477,21 @@ __global__ void __launch_bounds__(MAXT, MINB)
   uint64_t* stg = chk + 3;
   float4* a0s = reinterpret_cast<float4*>(smem + Ly.off_a0);  // panel-0 columns: [(h*4 + t4)*K16 + row]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 48);
-  unsigned* scb = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 56);  // [n&1][h][4]
-  // sc[4h+0] dmax bits, [1] pivmin bits, [2] bad, [3] ev_max bits (current systems);
-  // double-buffered by iteration parity, reset right after the hand-off
-  unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 72);  // [slot][4]
+  unsigned* scb = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 56);  // [n&1][h][8]
+  // sc[8h+0] dmax bits, [1] pivmin bits, [2] bad, [3] ev_max bits, [4] ||A||_1 bits (current
+  // systems); double-buffered by iteration parity, reset right after the hand-off
+  unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 88);  // [slot][8]
   float* Lscr = p.tc_scratch + (size_t)blockIdx.x * 2 * NS * Ly.lb;
   const int64_t npi = (p.nsys + NS - 1) / NS;
 
   // ---- one-time setup ----
   for (int e = tid; e < 2 * NS * opsz; e += Ly.threads) smem[Ly.off_hi + e] = 0.f;
   if (tid < 2 * NS) {
-    scb[4 * tid + 0] = 0u;
-    scb[4 * tid + 1] = __float_as_uint(FLT_MAX);
-    scb[4 * tid + 2] = 0u;
-    scb[4 * tid + 3] = 0u;
+    scb[8 * tid + 0] = 0u;
+    scb[8 * tid + 1] = __float_as_uint(FLT_MAX);
+    scb[8 * tid + 2] = 0u;
+    scb[8 * tid + 3] = 0u;
+    scb[8 * tid + 4] = 0u;
   }
   if (tid == 0) {
     for (int e = 0; e < 8 + 6 * NS; ++e) mbar_init(&mbar[e], e == 2 ? (uint32_t)(Ly.nmain / 32) : 1u);
@@ -498,18 +504,43 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const uint32_t tbase = *tslot;
 
   // ======================= back-substitution warps =======================
+  // Per system (one behind the factorization): L^T x = y, the backward
+  // comparison solve M(L)^T w = e, the rcond verdict, the row of C.
+  //
+  // rcond (solver.hpp:164-168: Eigen's PartialPivLU::rcond(), a Hager/Higham
+  // estimate of 1 / (||A||_1 ||A^{-1}||_1)).  For A = L L^T, |L^{-1}| <= M(L)^{-1}
+  // entrywise (M = comparison matrix), so ||A^{-1}||_1 <= ||L^{-1}||_inf ||L^{-1}||_1
+  // <= max(u) max(w) with u = M(L)^{-1} e (forward, riding along the panels) and
+  // w = M(L)^{-T} e (here): cert = 1 / (||A||_1 max(u) max(w)) is a lower bound on
+  // the true rcond, and the reference's estimate never exceeds ||A^{-1}||_1, so
+  // cert >= 2 * threshold proves the reference would accept the system.  Otherwise
+  // (rare: near-singular systems) the exact Hager/Higham estimator runs here on the
+  // factor (forward + backward solves streaming the L scratch), the same algorithm
+  // the oracle restates (oracle/fmsolve_oracle.cpp inverse_l1_norm_estimate).
   if (warp >= Ly.bwarp && warp < Ly.bwarp + NS) {
     const int h = warp - Ly.bwarp;
     float* xv = smem + Ly.off_xv + h * K16;
+    float* wv = smem + Ly.off_wv + h * K16;
+    float* hv = smem + Ly.off_hv + h * 3 * K16;  // Hager: working vector | sign | previous sign
     const int lbs = (K16 - 16 > 0 ? K16 - 16 : 1) * 16;  // floats per L block buffer
     float* lbuf = smem + Ly.off_lb + h * 2 * lbs;
     uint64_t* lf = lfull + 2 * h;
     uint32_t lb_use = 0;  // L-block counter (lfull phases: block use u -> buffer u&1)
     int n = 0;
+    auto warp_sum = [&](float v) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      return v;
+    };
+    auto warp_maxf = [&](float v) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+      return v;
+    };
     for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x, ++n) {
       const int slot = NS * (n & 1) + h;
       mbar_wait(&fact[slot], (n >> 1) & 1);
-      unsigned* ssc = slotsc + 4 * slot;
+      unsigned* ssc = slotsc + 8 * slot;
       if (ssc[3] == 0u) {
         int64_t q;
         int i;
@@ -517,8 +548,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
         const int64_t sys = q * k + i;  // global system index (error convention)
         const float* L11 = smem + Ly.off_l11 + slot * P * 152;
         const float* yv = smem + Ly.off_yv + slot * K16;
+        float* uvs = smem + Ly.off_uv + h * K16;
         const float* Lsl = Lscr + (size_t)slot * Ly.lb;
-        // blocks b = P-2 .. 0 carry L rows below them; prefetch the first one
+        // blocks b = 0 .. P-2 carry L rows below them (block P-1 none)
         auto issue_blk = [&](int b, uint32_t use) {
           const uint32_t bytes = (uint32_t)(K16 - 16 * b - 16) * 64u;
           if (lane == 0) {
@@ -526,23 +558,57 @@ __global__ void __launch_bounds__(MAXT, MINB)
             bulk_g2s(lbuf + (use & 1) * lbs, Lsl + lb_off(b, K16), bytes, &lf[use & 1]);
           }
         };
+        // forward comparison solve M(L) u = e (rcond certificate), streaming blocks 0..P-2
+        for (int c = lane; c < K16; c += 32) uvs[c] = 1.f;
+        __syncwarp();
+        if (P >= 2) issue_blk(0, lb_use);
+        for (int b = 0; b < P; ++b) {
+          const float* Lbb = L11 + b * 152;
+          {  // u_b = M(L_bb)^{-1} acc_b by forward substitution, lane t (< 16) owns row t:
+             // u_s = acc_s / L_ss, then acc_t += |L[t][s]| u_s  (chain: SHFL -> FMUL -> FFMA)
+            const int t = lane & 15;
+            float a = uvs[16 * b + t], res = 0.f;
+#pragma unroll
+            for (int sv = 0; sv < 16; ++sv) {
+              const float us = __shfl_sync(kFull, a, sv) * Lbb[136 + sv];
+              if (t == sv) res = us;
+              if (t > sv) a = fmaf(fabsf(Lbb[t * (t + 1) / 2 + sv]), us, a);
+            }
+            __syncwarp();
+            if (lane < 16) uvs[16 * b + lane] = res;
+          }
+          __syncwarp();
+          const int R = K16 - 16 * b - 16;
+          if (R > 0) {
+            const uint32_t use = lb_use++;
+            mbar_wait(&lf[use & 1], (use >> 1) & 1);
+            if (b + 2 < P) issue_blk(b + 1, lb_use);  // prefetch (other buffer)
+            const float* blk = lbuf + (use & 1) * lbs;
+            float ub[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) ub[t] = uvs[16 * b + t];
+            for (int rho = lane; rho < R; rho += 32) {
+              float acc = uvs[16 * b + 16 + rho];
+#pragma unroll
+              for (int t4 = 0; t4 < 4; ++t4) {
+                const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * t4);
+                acc = fmaf(fabsf(l4.x), ub[4 * t4], acc);
+                acc = fmaf(fabsf(l4.y), ub[4 * t4 + 1], acc);
+                acc = fmaf(fabsf(l4.z), ub[4 * t4 + 2], acc);
+                acc = fmaf(fabsf(l4.w), ub[4 * t4 + 3], acc);
+              }
+              uvs[16 * b + 16 + rho] = acc;
+            }
+            __syncwarp();  // buffer and u rows consumed before the next refill
+          }
+        }
+        // backward pass: blocks b = P-2 .. 0; prefetch the first one
         if (P >= 2) issue_blk(P - 2, lb_use);
         for (int b = P - 1; b >= 0; --b) {
-          // lanes 0..15: column u = lane of W_b = L_bb^{-1} (independent of x)
           const float* Lbb = L11 + b * 152;
-          float w[16];
-          {
-            const int u = lane & 15;
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              float acc = (t == u) ? 1.f : 0.f;
-#pragma unroll
-              for (int v = 0; v < t; ++v) acc = fmaf(-Lbb[t * (t + 1) / 2 + v], w[v], acc);
-              w[t] = (t >= u) ? acc * Lbb[136 + t] : 0.f;
-            }
-          }
-          // s_t = sum_{c >= 16b+16} L[c][16b+t] x_c   (lane: rows rho = lane>>2 + 8m, cols 4(lane&3)..)
-          float v4[4] = {0.f, 0.f, 0.f, 0.f};
+          // s_t = sum_{c >= 16b+16} L[c][16b+t] x_c, sw_t = sum |L[c][16b+t]| w_c
+          // (lane: rows rho = lane>>2 + 8m, cols 4(lane&3)..)
+          float v4[4] = {0.f, 0.f, 0.f, 0.f}, w4[4] = {0.f, 0.f, 0.f, 0.f};
           const int R = K16 - 16 * b - 16;
           if (R > 0) {
             const uint32_t use = lb_use++;
@@ -550,52 +616,215 @@ __global__ void __launch_bounds__(MAXT, MINB)
             if (b >= 1) issue_blk(b - 1, lb_use);  // prefetch the next block (other buffer)
             const float* blk = lbuf + (use & 1) * lbs;
             for (int rho = lane >> 2; rho < R; rho += 8) {
-              const float xc = xv[16 * b + 16 + rho];
+              const float xc = xv[16 * b + 16 + rho], wcv = wv[16 * b + 16 + rho];
               const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
               v4[0] = fmaf(l4.x, xc, v4[0]);
               v4[1] = fmaf(l4.y, xc, v4[1]);
               v4[2] = fmaf(l4.z, xc, v4[2]);
               v4[3] = fmaf(l4.w, xc, v4[3]);
+              w4[0] = fmaf(fabsf(l4.x), wcv, w4[0]);
+              w4[1] = fmaf(fabsf(l4.y), wcv, w4[1]);
+              w4[2] = fmaf(fabsf(l4.z), wcv, w4[2]);
+              w4[3] = fmaf(fabsf(l4.w), wcv, w4[3]);
             }
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1)
 #pragma unroll
-              for (int e = 0; e < 4; ++e) v4[e] += __shfl_xor_sync(kFull, v4[e], o);
+              for (int e = 0; e < 4; ++e) {
+                v4[e] += __shfl_xor_sync(kFull, v4[e], o);
+                w4[e] += __shfl_xor_sync(kFull, w4[e], o);
+              }
             __syncwarp();  // everyone done with this buffer before it is refilled
           }
-          // lane t (< 16): z_t = y_t - s_t ; x_t = sum_{u >= t} W[u][t] z_u
+          // lane t (< 16): z_t = y_t - s_t, then back substitution L_bb^T x_b = z_b by rows
+          // from the bottom (x_v = z_v / L_vv; z_t -= L[v][t] x_v), and the same with
+          // the comparison matrix for w (zw_t = 1 + sw_t; zw_t += |L[v][t]| w_v)
           const int t = lane & 15;
-          float st = 0.f;
+          float st = 0.f, swt = 0.f;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float other = __shfl_sync(kFull, v4[e], (t >> 2));  // lane (t>>2) holds cols 4(t>>2)..
-            if ((t & 3) == e) st = other;
+            const float otherw = __shfl_sync(kFull, w4[e], (t >> 2));
+            if ((t & 3) == e) {
+              st = other;
+              swt = otherw;
+            }
           }
-          const float z = yv[16 * b + t] - st;
-          float x = 0.f;
+          float z = yv[16 * b + t] - st, zw = 1.f + swt;
+          float x = 0.f, xw = 0.f;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const float zu = __shfl_sync(kFull, z, u);
-            x = fmaf(w[u], zu, x);  // w[u] = W[u][t] (lane t holds column t); zero for u < t
+          for (int v = 15; v >= 0; --v) {
+            const float iv = Lbb[136 + v];
+            const float xv_ = __shfl_sync(kFull, z, v) * iv, wv_ = __shfl_sync(kFull, zw, v) * iv;
+            if (t == v) {
+              x = xv_;
+              xw = wv_;
+            }
+            if (t < v) {
+              const float lt = Lbb[v * (v + 1) / 2 + t];
+              z = fmaf(-lt, xv_, z);
+              zw = fmaf(fabsf(lt), wv_, zw);
+            }
           }
-          if (lane < 16) xv[16 * b + t] = x;
+          if (lane < 16) {
+            xv[16 * b + t] = x;
+            wv[16 * b + t] = xw;
+          }
           __syncwarp();
         }
-        // row of C, singularity verdict
+        // row of C, certificate
         float* Crow = p.C + ((size_t)q * k + i) * k;
         bool nf = false;
+        float umax = 0.f, wmax = 0.f;
         for (int c = lane; c < k; c += 32) {
           const float x = xv[c];
           nf |= !(fabsf(x) <= FLT_MAX);
           Crow[c] = x;
+          umax = fmaxf(umax, uvs[c]);
+          wmax = fmaxf(wmax, wv[c]);
         }
         nf = __any_sync(kFull, nf);
+        umax = warp_maxf(umax);
+        wmax = warp_maxf(wmax);
+        const float a1 = __uint_as_float(ssc[4]);
+        bool sing = ssc[2] != 0u || nf;
+        float rc = 0.f;
+        if (!sing) {
+          const float cert = 1.f / (a1 * umax * wmax);  // 0 when the bound overflows
+          if (!(a1 > 0.f)) {
+            rc = 0.f;                                   // rcond_estimate_helper: ||A||_1 == 0
+          } else if (k == 1) {
+            rc = 1.f;
+          } else if (cert >= 2.f * p.rcond_thr) {
+            rc = cert;
+          } else {
+            // ---- exact Hager / Higham estimate of ||A^{-1}||_1 (rare path) ----
+            float* v = hv;
+            float* csg = hv + K16;
+            float* osg = hv + 2 * K16;
+            // v <- A^{-1} v  (A = L L^T): forward L z = v, backward L^T v = z
+            auto solve_inplace = [&]() {
+              for (int b = 0; b < P; ++b) {
+                const float* Lbb = L11 + b * 152;
+                if (lane == 0) {
+                  for (int t = 0; t < 16; ++t) {
+                    float sacc = v[16 * b + t];
+                    for (int u = 0; u < t; ++u) sacc = fmaf(-Lbb[t * (t + 1) / 2 + u], v[16 * b + u], sacc);
+                    v[16 * b + t] = sacc * Lbb[136 + t];
+                  }
+                }
+                __syncwarp();
+                const int R = K16 - 16 * b - 16;
+                if (R > 0) {
+                  const uint32_t use = lb_use++;
+                  issue_blk(b, use);
+                  mbar_wait(&lf[use & 1], (use >> 1) & 1);
+                  const float* blk = lbuf + (use & 1) * lbs;
+                  for (int rho = lane; rho < R; rho += 32) {
+                    float acc = v[16 * b + 16 + rho];
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) acc = fmaf(-blk[rho * 16 + t], v[16 * b + t], acc);
+                    v[16 * b + 16 + rho] = acc;
+                  }
+                  __syncwarp();
+                }
+              }
+              for (int b = P - 1; b >= 0; --b) {
+                const float* Lbb = L11 + b * 152;
+                const int R = K16 - 16 * b - 16;
+                if (R > 0) {
+                  const uint32_t use = lb_use++;
+                  issue_blk(b, use);
+                  mbar_wait(&lf[use & 1], (use >> 1) & 1);
+                  const float* blk = lbuf + (use & 1) * lbs;
+                  if (lane < 16) {
+                    float sacc = 0.f;
+                    for (int rho = 0; rho < R; ++rho) sacc = fmaf(blk[rho * 16 + lane], v[16 * b + 16 + rho], sacc);
+                    wv[lane] = sacc;
+                  }
+                } else if (lane < 16) {
+                  wv[lane] = 0.f;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                  for (int t = 15; t >= 0; --t) {
+                    float sacc = v[16 * b + t] - wv[t];
+                    for (int u = t + 1; u < 16; ++u) sacc = fmaf(-Lbb[u * (u + 1) / 2 + t], v[16 * b + u], sacc);
+                    v[16 * b + t] = sacc * Lbb[136 + t];
+                  }
+                }
+                __syncwarp();
+              }
+              for (int c = k + lane; c < K16; c += 32) v[c] = 0.f;  // identity padding stays out
+              __syncwarp();
+            };
+            auto l1v = [&]() {
+              float sacc = 0.f;
+              for (int c = lane; c < k; c += 32) sacc += fabsf(v[c]);
+              return warp_sum(sacc);
+            };
+            const float nk = (float)k;
+            for (int c = lane; c < K16; c += 32) v[c] = c < k ? 1.f / nk : 0.f;
+            __syncwarp();
+            solve_inplace();
+            float lower = l1v(), old_lower = lower;
+            int vmax = -1, old_vmax = -1;
+            for (int it = 0; it < 4; ++it) {
+              bool same = true;  // sign == old_sign
+              for (int c = lane; c < K16; c += 32) {
+                const float sg = c < k ? (v[c] < 0.f ? -1.f : 1.f) : 0.f;
+                same &= (sg == osg[c]);
+                csg[c] = sg;
+                v[c] = sg;  // next right-hand side: the sign vector
+              }
+              same = __all_sync(kFull, same);
+              if (it > 0 && same) break;
+              __syncwarp();
+              solve_inplace();  // A^T = A
+              float best = -1.f;
+              int bi = 0;
+              for (int c = lane; c < k; c += 32)
+                if (fabsf(v[c]) > best) {
+                  best = fabsf(v[c]);
+                  bi = c;
+                }
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {  // first index of the max
+                const float ob = __shfl_xor_sync(kFull, best, o);
+                const int oi = __shfl_xor_sync(kFull, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                  best = ob;
+                  bi = oi;
+                }
+              }
+              vmax = bi;
+              if (vmax == old_vmax) break;
+              for (int c = lane; c < K16; c += 32) v[c] = (c == vmax) ? 1.f : 0.f;
+              __syncwarp();
+              solve_inplace();
+              lower = l1v();
+              if (lower <= old_lower) break;
+              for (int c = lane; c < K16; c += 32) osg[c] = csg[c];  // old_sign = sign
+              __syncwarp();
+              old_vmax = vmax;
+              old_lower = lower;
+            }
+            for (int c = lane; c < K16; c += 32) {
+              const float sgn = (c & 1) ? -1.f : 1.f;
+              v[c] = c < k ? sgn * (1.f + (float)c / (float)(k - 1)) : 0.f;
+            }
+            __syncwarp();
+            solve_inplace();
+            const float alt = (2.f * l1v()) / (3.f * nk);
+            if (lane == 0 && p.rcond_exact) atomicAdd(p.rcond_exact, 1u);
+            const float est = fmaxf(lower, alt);
+            rc = est == 0.f ? 0.f : (1.f / est) / a1;
+          }
+          if (!(rc >= p.rcond_thr)) sing = true;
+        }
         if (lane == 0) {
-          const float dm = __uint_as_float(ssc[0]);
-          const float pm = __uint_as_float(ssc[1]);
-          float rc = dm > 0.f ? pm / dm : 0.f;
           if (!(rc >= 0.f)) rc = 0.f;
-          if (ssc[2] || nf || !(rc >= p.rcond_thr)) atomicMin(p.fail_min, (unsigned long long)sys);
+          if (sing) atomicMin(p.fail_min, (unsigned long long)sys);
           atomicMin(p.rcond_min_bits, __float_as_uint(rc));
         }
       }
@@ -810,7 +1039,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
 #pragma unroll
       for (int h = 0; h < NS; ++h) mbar_wait(&bsub[slot0 + h], ((n - 2) >> 1) & 1);
     }
-    unsigned* sc = scb + 4 * NS * (n & 1);
+    unsigned* sc = scb + 8 * NS * (n & 1);
     float ev_max[NS];
     bool skip[NS];
 #pragma unroll
@@ -827,12 +1056,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
           m = fmaxf(m, fmaxf(p.ev1[(size_t)qs[h] * k + c], p.ev2[(size_t)qs[h] * k + c]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-        if (lane == 0) atomicMax(&sc[4 * h + 3], __float_as_uint(m));
+        if (lane == 0) atomicMax(&sc[8 * h + 3], __float_as_uint(m));
       }
       main_sync(NM);
 #pragma unroll
       for (int h = 0; h < NS; ++h) {
-        ev_max[h] = __uint_as_float(sc[4 * h + 3]);
+        ev_max[h] = __uint_as_float(sc[8 * h + 3]);
         skip[h] = skip[h] || !(ev_max[h] > 0.f);
       }
     }
@@ -861,6 +1090,14 @@ __global__ void __launch_bounds__(MAXT, MINB)
           dadd[h] = p.lambda * mask_entry<MASK_MODE>(p, qs[h], is[h], row, ev_max[h]) + p.ridge;
         }
       }
+    }
+    // ||A||_1 inputs (the loads are in flight while the previous MMAs drain)
+    float grr[NS], srow[NS];
+#pragma unroll
+    for (int h = 0; h < NS; ++h) {
+      const bool on = row_valid && row < k && vld[h] && !skip[h];
+      grr[h] = on ? __ldg(p.gram + ((size_t)qs[h] * k + row) * k + row) : 0.f;
+      srow[h] = on ? __ldg(p.gram_rowsum + (size_t)qs[h] * k + row) : 0.f;
     }
     // previous systems' MMAs must be complete before TMEM is rewritten
     if (any_mma) {
@@ -954,10 +1191,21 @@ __global__ void __launch_bounds__(MAXT, MINB)
     if (has_grp) tmem_st_wait();
 #pragma unroll
     for (int h = 0; h < NS; ++h) {
+      // row 1-norm of the assembled system: sum_c |G[row][c]| with the diagonal
+      // entry replaced by G[row][row] + lambda m + ridge (||A||_1 = max over rows,
+      // A symmetric) -- the matrix norm of the reference's rcond (solver.hpp:165)
+      float a1 = 0.f;
+      if (row_valid && row < k && vld[h] && !skip[h]) a1 = srow[h] - fabsf(grr[h]) + fabsf(grr[h] + dadd[h]);
       float m = dmax[h];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-      if (lane == 0) atomicMax(&sc[4 * h], __float_as_uint(m));
+      for (int o = 16; o > 0; o >>= 1) {
+        m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+        a1 = fmaxf(a1, __shfl_xor_sync(kFull, a1, o));
+      }
+      if (lane == 0) {
+        atomicMax(&sc[8 * h], __float_as_uint(m));
+        atomicMax(&sc[8 * h + 4], __float_as_uint(a1));
+      }
     }
     tc_fence_before();
     main_sync(NM);
@@ -1173,8 +1421,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
         pm = fminf(pm, __shfl_xor_sync(kFull, pm, o));
       }
       if (lane == 0) {
-        if (b) atomicOr(&sc[4 * h + 2], 1u);
-        atomicMin(&sc[4 * h + 1], __float_as_uint(fmaxf(pm, 0.f)));
+        if (b) atomicOr(&sc[8 * h + 2], 1u);
+        atomicMin(&sc[8 * h + 1], __float_as_uint(fmaxf(pm, 0.f)));
       }
     }
     main_sync(NM);
@@ -1187,15 +1435,17 @@ __global__ void __launch_bounds__(MAXT, MINB)
           sk = skip[hh];
           vv = vld[hh];
         }
-      unsigned* ssc = slotsc + 4 * (slot0 + h);
-      ssc[0] = sc[4 * h + 0];
-      ssc[1] = sc[4 * h + 1];
-      ssc[2] = sc[4 * h + 2];
+      unsigned* ssc = slotsc + 8 * (slot0 + h);
+      ssc[0] = sc[8 * h + 0];
+      ssc[1] = sc[8 * h + 1];
+      ssc[2] = sc[8 * h + 2];
       ssc[3] = sk ? 1u : 0u;
-      sc[4 * h + 0] = 0u;
-      sc[4 * h + 1] = __float_as_uint(FLT_MAX);
-      sc[4 * h + 2] = 0u;
-      sc[4 * h + 3] = 0u;
+      ssc[4] = sc[8 * h + 4];
+      sc[8 * h + 0] = 0u;
+      sc[8 * h + 1] = __float_as_uint(FLT_MAX);
+      sc[8 * h + 2] = 0u;
+      sc[8 * h + 3] = 0u;
+      sc[8 * h + 4] = 0u;
       if (sk && vv) atomicOr(p.flags, 32u);
       mbar_arrive(&fact[slot0 + h]);
     }
@@ -1266,6 +1516,19 @@ bool tc_supported(int k, int optin_smem) {
   return (size_t)L.floats * 4 <= (size_t)optin_smem;
 }
 
+int tc_max_resolution(int optin_smem) {
+  int k = 1;
+  while (k < 4096 && tc_supported(k + 1, optin_smem)) ++k;
+  return k;
+}
+
+// The f32 route: every row system goes through the tcgen05/TMEM kernel (no
+// other solver, no CPU fallback); k beyond tc_max_resolution is rejected by the
+// C ABI before a launch.
+cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream) {
+  return launch_chol_tc(p, mask_mode, stream);
+}
+
 // Host-side launcher for the tensor-core solver (p.tc_scratch must hold
 // tc_scratch_bytes(k, nsys, SMs)).
 cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream) {
@@ -1329,6 +1592,7 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   const int64_t npi = (p.nsys + L.ns - 1) / L.ns;
   const int64_t maxgrid = (int64_t)sms * L.cps;
   const unsigned grid = (unsigned)(npi < maxgrid ? npi : maxgrid);
+  note_launch("chol_tc_kernel");
   fn<<<grid, L.threads, smem, stream>>>(p, L, tmG, tmA);
   return cudaGetLastError();
 }
@@ -1733,6 +1997,7 @@ cudaError_t launch_project_tc(const float* phi, const float* mass, const float* 
       cudaError_t e = cudaFuncSetAttribute(proj_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       dim3 grid((unsigned)((k + 127) / 128), (unsigned)b);
+      note_launch("proj_tma_kernel");
       proj_tma_kernel<<<grid, kPjThreads, smem, st>>>(tp, tf, tm, n, k, d, N, out);
       return cudaGetLastError();
     }
@@ -1742,6 +2007,7 @@ cudaError_t launch_project_tc(const float* phi, const float* mass, const float* 
   cudaError_t e = cudaFuncSetAttribute(proj_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)req);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((k + 127) / 128), (unsigned)b);
+  note_launch("proj_tc_kernel");
   proj_tc_kernel<<<grid, kPjThreads, req, st>>>(phi, mass, F, n, k, d, N, out);
   return cudaGetLastError();
 }

@@ -123,6 +123,7 @@ class SolveReport:
     wall_time: timedelta = timedelta(0)
     peak_extra_bytes: int = 0
     min_rcond: float = 0.0
+    rcond_exact_systems: int = 0  # systems that needed the exact Hager/Higham estimator
 
 
 @dataclass
@@ -133,6 +134,7 @@ class BatchSolveReport:
     wall_time: timedelta = timedelta(0)
     peak_extra_bytes: int = 0
     min_rcond: float = 0.0
+    rcond_exact_systems: int = 0  # systems that needed the exact Hager/Higham estimator
 
 
 @dataclass
@@ -282,7 +284,7 @@ def solve_host(G: np.ndarray, R: np.ndarray, M: np.ndarray, lam: float,
                                      _ptr(out), C.byref(rep))
         _raise(ctx, st, rep)
         return BatchSolveReport(out, rep.max_residual, timedelta(seconds=rep.wall_seconds),
-                                int(rep.peak_extra_bytes), rep.min_rcond)
+                                int(rep.peak_extra_bytes), rep.min_rcond, int(rep.rcond_exact_systems))
     _require(precision == "f32", "precision must be 'f32' or 'f64'")
     opts = opts or SolverOptions()
     G, R, M = _f32(G), _f32(R), _f32(M)
@@ -297,7 +299,7 @@ def solve_host(G: np.ndarray, R: np.ndarray, M: np.ndarray, lam: float,
                                  C.byref(o), _ptr(out), C.byref(rep))
     _raise(ctx, st, rep)
     return BatchSolveReport(out, rep.max_residual, timedelta(seconds=rep.wall_seconds),
-                            int(rep.peak_extra_bytes), rep.min_rcond)
+                            int(rep.peak_extra_bytes), rep.min_rcond, int(rep.rcond_exact_systems))
 
 
 def solve_cuda(problem_or_a, *args, device: int = 0, **kw) -> SolveReport:
@@ -312,7 +314,7 @@ def solve_cuda(problem_or_a, *args, device: int = 0, **kw) -> SolveReport:
     opts = rest[0] if rest else kw.get("opts")
     batch = solve_cuda_many([problem], lam, opts, device)
     return SolveReport(batch.maps[0], batch.max_residual_norm, batch.wall_time,
-                       batch.peak_extra_bytes, batch.min_rcond)
+                       batch.peak_extra_bytes, batch.min_rcond, batch.rcond_exact_systems)
 
 
 # Drop-in aliases: the reference names of the one-dispatch route.
@@ -390,7 +392,7 @@ def solve_device(gram, rhs, mask=None, *, lam: float, ev1=None, ev2=None,
     finally:
         ctx.set_stream(None)
     return out, BatchSolveReport(out, rep.max_residual, timedelta(seconds=rep.wall_seconds),
-                                 int(rep.peak_extra_bytes), rep.min_rcond)
+                                 int(rep.peak_extra_bytes), rep.min_rcond, int(rep.rcond_exact_systems))
 
 
 def pipeline_device(phi1, mass1, F1, ev1, phi2, mass2, F2, ev2, *, lam: float = 100.0,
@@ -426,4 +428,4 @@ def pipeline_device(phi1, mass1, F1, ev1, phi2, mass2, F2, ev2, *, lam: float = 
     finally:
         ctx.set_stream(None)
     return cxy, cyx, BatchSolveReport(cxy, rep.max_residual, timedelta(seconds=rep.wall_seconds),
-                                      int(rep.peak_extra_bytes), rep.min_rcond)
+                                      int(rep.peak_extra_bytes), rep.min_rcond, int(rep.rcond_exact_systems))

@@ -27,15 +27,16 @@ def main():
     tG, tR, t1, t2 = (torch.from_numpy(x).to(dev) for x in (G, R, e1, e2))
     M = torch.from_numpy(fm.build_mask(fm.MaskKind.Resolvent, e1, e2, 0.5)).to(dev)
     opts = fm.SolverOptions(compute_residual=False)
-    times = []
+    times, exact = [], []
     for _ in range(a.reps):
         if a.mode == "ev":
             _, rep = fm.solve_device(tG, tR, lam=100.0, ev1=t1, ev2=t2, opts=opts)
         else:
             _, rep = fm.solve_device(tG, tR, M, lam=100.0, opts=opts)
         times.append(rep.wall_time.total_seconds() * 1e3)
+        exact.append(getattr(rep, "rcond_exact_systems", -1))
     torch.cuda.synchronize()
-    print("solver kernel ms:", " ".join(f"{t:.3f}" for t in times))
+    print("solver kernel ms:", " ".join(f"{t:.3f}" for t in times), "| exact-rcond systems:", exact)
 
 
 if __name__ == "__main__":
