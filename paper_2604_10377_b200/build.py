@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libfmap_cuda.so"
-SOURCES = ["fmap_tc.cu", "fmap_f64.cu", "fmap_kernels.cu", "fmap_capi.cu"]
+SOURCES = ["fmap_tc.cu", "fmap_gram.cu", "fmap_f64.cu", "fmap_kernels.cu", "fmap_capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -39,7 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir = PKG / "_build"
     objdir.mkdir(exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-I", str(ROOT / "include"), "-Xptxas", "-v"]
+              "-I", str(ROOT / "include"), "-Xptxas", "-v",
+              *os.environ.get("FMAP_NVCC_FLAGS", "").split()]  # e.g. -DFMAP_TC_TRACE (phase stamps)
     def compile_one(src: str) -> str:
         obj = objdir / (Path(src).stem + ".o")
         if not force and not _stale(obj, [CSRC / src, *CSRC.glob("*.cuh"), ROOT / "include" / "fmap_cuda.h"]):

@@ -47,7 +47,7 @@ struct fmap_ctx {
   int num_sms = 0;
   // host-buffer pipelining (fmap_solve_f32): second compute stream + copy stream
   cudaStream_t comp2 = nullptr, copy = nullptr, copy2 = nullptr;  // 2nd compute, H2D, D2H
-  cudaEvent_t cev[36] = {};  // start | done | per chunk: H2D done, solve done (x 16 chunks) | H2D join
+  cudaEvent_t cev[37] = {};  // start | done | per chunk: H2D done, solve done (x 16 chunks) | H2D join | compute join
 };
 
 namespace {
@@ -407,7 +407,7 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   const int64_t cb = (b + nchunk - 1) / nchunk;  // pairs per chunk
   const int64_t csys = cb * k;
   const size_t tcb = tc_scratch_bytes((int)k, csys, ctx->num_sms);
-  const size_t npart = opts.compute_residual ? residual_partial_count(cb, (int)k) * nchunk : 0;
+  const size_t npart = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
   const size_t staging = carve_size({bytes, bytes, bytes, bytes, tcb, tcb, (size_t)b * k * sizeof(float),
                                      npart * sizeof(double), opts.compute_residual ? (size_t)b * sizeof(double) : 0});
   if (rep) rep->peak_extra_bytes = staging;
@@ -482,16 +482,21 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
     p.sys_offset = q0 * k;
     p.tc_scratch = scr[c & 1];
     FMAP_CK(ctx, launch_chol_solve(p, 0, s));
-    if (opts.compute_residual) {  // check_stationarity per chunk (solver.hpp:314-320), overlapped
-      FMAP_CK(ctx, launch_residual(dC + off, dG + off, dR + off, dM + off, nq, (int)k, lambda,
-                                   partial + (size_t)c * residual_partial_count(cb, (int)k), res_out + q0, s));
-    }
     FMAP_CK(ctx, cudaEventRecord(done, s));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy2, done, 0));
     FMAP_CK(ctx, cudaMemcpyAsync(C_out + off, dC + off, nb, cudaMemcpyDeviceToHost, ctx->copy2));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[3 + 2 * nchunk], ctx->copy));  // all H2D done (stream join)
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[3 + 2 * nchunk], 0));
+  if (opts.compute_residual) {
+    // check_stationarity (solver.hpp:314-320) once over the whole batch on the
+    // tensor cores after every chunk's solve (a residual kernel cannot share an SM
+    // with a running solver chunk: both need tensor memory), overlapping the last
+    // chunk's D2H
+    FMAP_CK(ctx, cudaEventRecord(ctx->cev[36], comp[1]));
+    FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[36], 0));
+    FMAP_CK(ctx, launch_residual(dC, dG, dR, dM, b, (int)k, lambda, partial, res_out, ctx->stream));
+  }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[1], ctx->copy2));
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[1], 0));
   FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
@@ -538,15 +543,13 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
   if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
   if (!(lambda >= 0.0)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "lambda must be non-negative");
   if (!G || !R || !M || !C) return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
-  if (chol_f64_smem_bytes((int)k) > (size_t)ctx->max_smem_optin) {
-    int kmax = 1;
-    while (chol_f64_smem_bytes(kmax + 1) <= (size_t)ctx->max_smem_optin) ++kmax;
+  constexpr int64_t kF64Max = 512;  // rows beyond shared memory spill to an L2-resident scratch
+  if (k > kF64Max)
     return set_err(ctx, FMAP_INVALID_ARGUMENT,
-                   "k = " + std::to_string(k) + " exceeds the f64 route's single-CTA limit " + std::to_string(kmax) +
-                       " on this device");
-  }
+                   "k = " + std::to_string(k) + " exceeds the f64 route's limit " + std::to_string(kF64Max));
   const size_t kk = (size_t)k * k;
-  const size_t scratch = carve_size({(size_t)b * sizeof(double), (size_t)k * sizeof(double)});
+  const size_t spill = chol_f64_spill_doubles((int)k, (size_t)ctx->max_smem_optin, ctx->num_sms);
+  const size_t scratch = carve_size({(size_t)b * sizeof(double), (size_t)k * sizeof(double), spill * sizeof(double)});
   const uint64_t required = (uint64_t)scratch + host_staging_bytes;
   if (rep) rep->peak_extra_bytes = required;
   if (opts.has_memory_cap && required > opts.memory_cap_bytes) {
@@ -563,12 +566,13 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
   Carve cv{reinterpret_cast<char*>(ctx->scr)};
   double* sq = cv.take<double>((size_t)b);
   double* zrow = cv.take<double>((size_t)k);
+  double* dspill = spill ? cv.take<double>(spill) : nullptr;
   if ((st = reset_ctrl(ctx))) return st;
   FMAP_CK(ctx, launch_validate_f64(G, R, M, (size_t)b * kk, d_flags(ctx), ctx->stream));
   const double rthr = opts.rcond_threshold < 0.f ? 1e-14 : (double)opts.rcond_threshold;
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, launch_chol_f64(G, R, M, C, (int)k, b * k, lambda, (double)opts.ridge, rthr, -1, d_fail(ctx),
-                               d_rcond(ctx), ctx->stream));
+                               d_rcond(ctx), d_nexact(ctx), dspill, ctx->stream));
   if (opts.inject_fault) {  // solver.hpp:269-273, as solve_core
     std::vector<double> g0(k);
     double m00 = 0.0;
@@ -585,7 +589,7 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
       }
     const double alpha = -2.0 * g0[w];
     FMAP_CK(ctx, launch_chol_f64(G, R, M, zrow, (int)k, 1, lambda, (double)opts.ridge, rthr, 0, d_fail(ctx),
-                                 d_rcond(ctx), ctx->stream));
+                                 d_rcond(ctx), d_nexact(ctx), dspill, ctx->stream));
     FMAP_CK(ctx, launch_fault_combine_f64(C, zrow, (int)k, w, alpha, d_fail(ctx), ctx->stream));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
@@ -619,6 +623,23 @@ int solve_core_f64(fmap_ctx* ctx, int64_t b, int64_t k, const double* G, const d
   }
   ctx->last_error.clear();
   return FMAP_OK;
+}
+
+// normal_equations (solver.hpp:95-103) for up to 4 products on the tensor cores
+// (fmap_gram.cu); the FP32 SIMT GEMM serves shapes the tcgen05 kernel does not
+// (k > 304, or more than 65535 pairs) and FMAP_GRAM=simt.
+cudaError_t normal_products(int n, const float* const* X, const float* const* Y, float* const* out, const int* sym,
+                            int64_t b, int k, int d, cudaStream_t st) {
+  const char* sel = std::getenv("FMAP_GRAM");
+  if (!(sel && sel[0] == 's')) {
+    const cudaError_t e = launch_gram_tc(n, X, Y, out, sym, b, k, d, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  for (int i = 0; i < n; ++i) {
+    const cudaError_t e = launch_gemm_nt(X[i], Y[i], b, k, k, d, out[i], st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 bool host_finite(const float* p, size_t n) {
@@ -907,8 +928,11 @@ int fmap_normal_equations_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, int64_t d
   LaunchScope ls(ctx);
   if (b < 1 || k < 1 || d < 1)
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "descriptor A must be non-empty");
-  FMAP_CK(ctx, launch_gemm_nt(d_A, d_A, b, (int)k, (int)k, (int)d, d_gram, ctx->stream));
-  FMAP_CK(ctx, launch_gemm_nt(d_B, d_A, b, (int)k, (int)k, (int)d, d_rhs, ctx->stream));
+  const float* X[2] = {d_A, d_B};
+  const float* Y[2] = {d_A, d_A};
+  float* O[2] = {d_gram, d_rhs};
+  const int sym[2] = {1, 0};
+  FMAP_CK(ctx, normal_products(2, X, Y, O, sym, b, (int)k, (int)d, ctx->stream));
   return FMAP_OK;
 }
 
@@ -1001,11 +1025,12 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
   FMAP_CK(ctx, cudaEventRecord(e0, ctx->stream));
   FMAP_CK(ctx, launch_project(d_phi1, d_mass1, d_F1, b, n1, (int)k, (int)d, A, ctx->stream));
   FMAP_CK(ctx, launch_project(d_phi2, d_mass2, d_F2, b, n2, (int)k, (int)d, B, ctx->stream));
-  FMAP_CK(ctx, launch_gemm_nt(A, A, b, (int)k, (int)k, (int)d, G, ctx->stream));
-  FMAP_CK(ctx, launch_gemm_nt(B, A, b, (int)k, (int)k, (int)d, R, ctx->stream));
-  if (bidir) {
-    FMAP_CK(ctx, launch_gemm_nt(B, B, b, (int)k, (int)k, (int)d, G2, ctx->stream));
-    FMAP_CK(ctx, launch_gemm_nt(A, B, b, (int)k, (int)k, (int)d, R2, ctx->stream));
+  {  // G = A A^T, R = B A^T (and G2 = B B^T, R2 = A B^T): one tcgen05 launch
+    const float* X[4] = {A, B, B, A};
+    const float* Y[4] = {A, A, B, B};
+    float* O[4] = {G, R, G2, R2};
+    const int sym[4] = {1, 0, 1, 0};
+    FMAP_CK(ctx, normal_products(bidir ? 4 : 2, X, Y, O, sym, b, (int)k, (int)d, ctx->stream));
   }
   // solve_core carves its own scratch after host_staging_bytes = our scratch
   const int mm = mask_kind == FMAP_MASK_RESOLVENT ? 1 : 2;

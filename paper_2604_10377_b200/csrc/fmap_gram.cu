@@ -1,0 +1,243 @@
+// Normal equations on the 5th-generation tensor cores (north_star stage 1):
+//   G_q = A_q A_q^T,  R_q = B_q A_q^T      (replaces normal_equations,
+//   /root/reference/proj/include/fmsolve/solver.hpp:95-103, batched)
+// and, for the bidirectional pipeline, G2 = B B^T, R2 = A B^T.
+//
+// One CTA per (128-row tile of the output, pair, product).  D[m][n] =
+// sum_t X[m][t] Y[n][t] with X, Y row-major k x d: both operands are K-major in
+// memory, so each 16-column K stage is loaded with coalesced float4 reads,
+// split into TF32 hi/lo parts (3xTF32: hi*hi + hi*lo + lo*hi; 1xTF32 misses the
+// 1e-4 bar) and stored in the no-swizzle core-matrix layout;
+// thread 0 issues the tcgen05.mma (M = 128, N <= 256 per instruction, K = 8)
+// into a TMEM accumulator while the 128 threads stage the next K stage (two
+// buffers, mbarrier hand-off).  Symmetric products (G) compute the lower
+// triangle's block row only (N = rows up to the tile's end) and mirror it, so G
+// is exactly symmetric.  Work: 2 k^2 d flops per product (tensor-bound, tiny
+// next to the solver); bytes 4 (2 k d + k^2) per product.
+#include "fmap_kernels.cuh"
+#include "tc_ptx.cuh"
+
+#include <cstdlib>
+
+namespace fmap {
+
+namespace {
+
+using namespace ptx;
+
+constexpr int kGK = 16;        // K (= d) elements per stage
+constexpr int kGThreads = 128;  // one thread per output row of the tile
+constexpr int kGMaxN = 320;     // k <= 304 (solver limit) -> N <= 304 padded to 16
+
+struct GramJob {
+  const float* X;
+  const float* Y;
+  float* out;
+  int sym;
+  // residual mode (partial != nullptr): no `out`; per row r of pair q,
+  // partial[q k + r] = sum_c (D[r][c] + lambda M[r][c] X[r][c] - R[r][c])^2  (fp64)
+  const float* M;
+  const float* R;
+  float lambda;
+  double* partial;
+};
+
+struct GramArgs {
+  GramJob job[4];
+  int k, d;
+  int ys;          // floats of one Y operand copy (round16(k) x 16)
+  uint32_t tcols;  // TMEM columns allocated (256, or 512 when k > 256)
+};
+
+__device__ __forceinline__ uint32_t idesc_tf32_pos(int N) {  // D += A*B (no negation), M = 128
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ int core_idx(int r, int t) {  // element (r, t < 16) of a [rows x 16] operand
+  return (r >> 3) * 128 + (t >> 2) * 32 + (r & 7) * 4 + (t & 3);
+}
+
+// Stage rows [r0, r0 + nrows) x K columns [k0, k0 + 16) of a row-major (rows x d)
+// matrix into hi / lo operand buffers; rows >= rlim and columns >= d are zero.
+__device__ __forceinline__ void stage_rows(const float* __restrict__ M, int r0, int nrows, int rlim, int d, int k0,
+                                           float* hi, float* lo, int tid) {
+  const bool vec = (d & 3) == 0;
+  for (int e = tid; e < nrows * 4; e += kGThreads) {
+    const int r = e >> 2, t4 = e & 3;
+    const int gr = r0 + r, gc = k0 + 4 * t4;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (gr < rlim) {
+      const float* src = M + (size_t)gr * d + gc;
+      if (vec && gc + 4 <= d) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+        v[0] = x.x;
+        v[1] = x.y;
+        v[2] = x.z;
+        v[3] = x.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = gc + u < d ? __ldg(src + u) : 0.f;
+      }
+    }
+    float h[4], l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) split_tf32(v[u], h[u], l[u]);
+    const int o = core_idx(r, 4 * t4);
+    *reinterpret_cast<float4*>(hi + o) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(lo + o) = make_float4(l[0], l[1], l[2], l[3]);
+  }
+}
+
+__global__ void __launch_bounds__(kGThreads, 1) gram_tc_kernel(GramArgs a) {
+  extern __shared__ __align__(1024) float smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const GramJob jb = a.job[blockIdx.z];
+  const int q = blockIdx.y, m0 = blockIdx.x * 128, k = a.k, d = a.d;
+  if (m0 >= k) return;
+  const float* Xq = jb.X + (size_t)q * k * d;
+  const float* Yq = jb.Y + (size_t)q * k * d;
+  float* Oq = jb.partial ? nullptr : jb.out + (size_t)q * k * k;
+  const int mrows = min(128, k - m0);
+  const int Nreal = jb.sym ? min(k, m0 + 128) : k;  // symmetric: lower block row only
+  const int N = (Nreal + 15) & ~15;
+  const int xs = 128 * kGK, ys = a.ys;               // floats per operand copy
+  const int bufsz = 2 * xs + 2 * ys;                  // Xhi | Xlo | Yhi | Ylo
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * bufsz);  // [0..1] empty, [2] done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, a.tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const int nst = (d + kGK - 1) / kGK;
+  for (int st = 0; st < nst; ++st) {
+    const int buf = st & 1;
+    float* B = smem + buf * bufsz;
+    if (st >= 2) {  // the MMAs that read this buffer (stage st-2) are done
+      mbar_wait(&bar[buf], ((st - 2) >> 1) & 1);
+    }
+    stage_rows(Xq, m0, 128, k, d, st * kGK, B, B + xs, tid);
+    stage_rows(Yq, 0, N, Nreal, d, st * kGK, B + 2 * xs, B + 2 * xs + ys, tid);
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t xh = su32(B), xl = su32(B + xs), yh = su32(B + 2 * xs), yl = su32(B + 2 * xs + ys);
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t ko = (uint32_t)ks * 256u;
+        for (int n0 = 0; n0 < N; n0 += 256) {
+          const int nn = min(256, N - n0);
+          const uint32_t id = idesc_tf32_pos(nn);
+          const uint32_t yo = (uint32_t)(n0 >> 3) * 512u;
+          const uint32_t acc0 = (st > 0 || ks > 0) ? 1u : 0u;
+          mma_tf32(tbase + (uint32_t)n0, sdesc(xh + ko), sdesc(yh + yo + ko), id, acc0);
+          mma_tf32(tbase + (uint32_t)n0, sdesc(xh + ko), sdesc(yl + yo + ko), id, 1u);
+          mma_tf32(tbase + (uint32_t)n0, sdesc(xl + ko), sdesc(yh + yo + ko), id, 1u);
+        }
+      }
+      mma_commit(&bar[buf]);
+      if (st == nst - 1) mma_commit(&bar[2]);
+    }
+  }
+  mbar_wait(&bar[2], 0);
+  tc_fence_after();
+  // epilogue: warp w reads TMEM lanes 32w.. (rows m0 + 32w + lane)
+  const int r = m0 + 32 * warp + lane;
+  const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
+  if (jb.partial) {  // check_stationarity (solver.hpp:116-128): C G + lambda M.*C - R, squared, per row
+    const bool live = 32 * warp + lane < mrows;
+    const size_t ro = ((size_t)q * k + (live ? r : 0)) * k;
+    double acc = 0.0;
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      float v[16];
+      tmem_ld16(tl + (uint32_t)c0, v);
+      if (live) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const int c = c0 + t;
+          if (c < k) {
+            const float e = v[t] + jb.lambda * (__ldg(jb.M + ro + c) * __ldg(Xq + (size_t)r * d + c)) -
+                            __ldg(jb.R + ro + c);
+            acc += (double)e * (double)e;
+          }
+        }
+      }
+    }
+    if (live) jb.partial[(size_t)q * k + r] = acc;
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tbase, a.tcols);
+    return;
+  }
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tmem_ld16(tl + (uint32_t)c0, v);
+    if (32 * warp + lane < mrows) {
+      float* orow = Oq + (size_t)r * k;
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int c = c0 + t;
+        if (c < Nreal && (!jb.sym || c <= r)) {
+          orow[c] = v[t];
+          if (jb.sym && c < r) Oq[(size_t)c * k + r] = v[t];  // mirror: G exactly symmetric
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, a.tcols);
+}
+
+}  // namespace
+
+// two stages of X hi/lo (128 x 16) and Y hi/lo (round16(k) x 16) + barriers:
+// 86 KB at k = 200, so two CTAs share an SM (TMEM 256 columns each)
+size_t gram_tc_smem_bytes(int k) { return (size_t)(2 * (2 * 128 * kGK + 2 * ((k + 15) & ~15) * kGK)) * 4 + 64; }
+
+// nprod products (X_i Y_i^T -> out_i, sym_i) over b pairs, k x d operands.
+cudaError_t launch_gram_tc(int nprod, const float* const* X, const float* const* Y, float* const* out,
+                           const int* sym, int64_t b, int k, int d, cudaStream_t st) {
+  if (nprod < 1 || nprod > 4 || k < 1 || d < 1 || b < 1) return cudaErrorInvalidValue;
+  if (k > kGMaxN - 16 || b > 65535) return cudaErrorNotSupported;
+  GramArgs a{};
+  for (int i = 0; i < nprod; ++i) a.job[i] = GramJob{X[i], Y[i], out[i], sym[i], nullptr, nullptr, 0.f, nullptr};
+  a.k = k;
+  a.d = d;
+  a.ys = ((k + 15) & ~15) * kGK;
+  a.tcols = ((k + 15) & ~15) <= 256 ? 256u : 512u;
+  const size_t smem = gram_tc_smem_bytes(k);
+  cudaError_t e = cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  note_launch("gram_tc_kernel");
+  gram_tc_kernel<<<dim3((unsigned)((k + 127) / 128), (unsigned)b, (unsigned)nprod), kGThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Residual partials on the tensor cores: partial[q k + r] for C G (k x k, d = k).
+cudaError_t launch_residual_tc(const float* C, const float* G, const float* R, const float* M, int64_t b, int k,
+                               float lambda, double* partial, cudaStream_t st) {
+  if (k < 1 || b < 1) return cudaErrorInvalidValue;
+  if (k > kGMaxN - 16 || b > 65535 || std::getenv("FMAP_RESIDUAL_SIMT")) return cudaErrorNotSupported;
+  GramArgs a{};
+  a.job[0] = GramJob{C, G, nullptr, 0, M, R, lambda, partial};
+  a.k = k;
+  a.d = k;
+  a.ys = ((k + 15) & ~15) * kGK;
+  a.tcols = ((k + 15) & ~15) <= 256 ? 256u : 512u;
+  const size_t smem = gram_tc_smem_bytes(k);
+  cudaError_t e = cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  note_launch("gram_tc_kernel(residual)");
+  gram_tc_kernel<<<dim3((unsigned)((k + 127) / 128), (unsigned)b, 1), kGThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace fmap

@@ -487,21 +487,25 @@ cudaError_t launch_project(const float* phi, const float* mass, const float* F, 
 cudaError_t launch_residual(const float* C, const float* G, const float* R, const float* M,
                             int64_t b, int k, float lambda, double* partial, double* out,
                             cudaStream_t st) {
-  const int nchunk = (k + RES_ROWS - 1) / RES_ROWS;
-  dim3 grid(nchunk, (unsigned)b);
-  note_launch("residual_partial_kernel");
-  residual_partial_kernel<<<grid, 256, RES_ROWS * k * sizeof(float), st>>>(C, G, R, M, k, lambda,
-                                                                          partial);
-  cudaError_t e = cudaGetLastError();
+  // C G on the tensor cores (3xTF32) with the mask / rhs terms and the squares in
+  // the epilogue (per-row fp64 partials); FP32 SIMT kernel for shapes it does not serve
+  int nchunk = k;
+  cudaError_t e = launch_residual_tc(C, G, R, M, b, k, lambda, partial, st);
+  if (e == cudaErrorNotSupported) {
+    nchunk = (k + RES_ROWS - 1) / RES_ROWS;
+    dim3 grid(nchunk, (unsigned)b);
+    note_launch("residual_partial_kernel");
+    residual_partial_kernel<<<grid, 256, RES_ROWS * k * sizeof(float), st>>>(C, G, R, M, k, lambda, partial);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return e;
   note_launch("residual_finish_kernel");
-  residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, nchunk, (int)b,
-                                                                      out);
+  residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, nchunk, (int)b, out);
   return cudaGetLastError();
 }
 
 size_t residual_partial_count(int64_t b, int k) {
-  return (size_t)b * ((k + RES_ROWS - 1) / RES_ROWS);
+  return (size_t)b * k;  // per-row partials (tensor-core path); >= the SIMT kernel's b * ceil(k / 8)
 }
 
 cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,

@@ -28,6 +28,12 @@ cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsig
 cudaError_t launch_ev_max_check(const float* e1, const float* e2, int64_t b, int k, unsigned* flags,
                                 cudaStream_t st);
 cudaError_t launch_gram_check(const float* G, int64_t b, int k, float* S, unsigned* flags, cudaStream_t st);
+// tcgen05 3xTF32 normal equations (fmap_gram.cu): nprod <= 4 products
+// out_i[q] = X_i[q] Y_i[q]^T (k x d operands), sym_i = 1 for X_i == Y_i (mirrored).
+cudaError_t launch_gram_tc(int nprod, const float* const* X, const float* const* Y, float* const* out,
+                           const int* sym, int64_t b, int k, int d, cudaStream_t st);
+cudaError_t launch_residual_tc(const float* C, const float* G, const float* R, const float* M, int64_t b, int k,
+                               float lambda, double* partial, cudaStream_t st);
 cudaError_t launch_gemm_nt(const float* X, const float* Y, int64_t b, int M, int N, int K,
                            float* out, cudaStream_t st);
 cudaError_t launch_project(const float* phi, const float* mass, const float* F, int64_t b,

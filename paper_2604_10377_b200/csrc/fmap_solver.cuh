@@ -51,10 +51,11 @@ cudaError_t launch_project_tc(const float* phi, const float* mass, const float* 
 cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream);
 
 // f64 route (fmap_f64.cu)
-size_t chol_f64_smem_bytes(int k);
+size_t chol_f64_smem_bytes(int k, size_t optin);
+size_t chol_f64_spill_doubles(int k, size_t optin, int num_sms);
 cudaError_t launch_chol_f64(const double* G, const double* R, const double* M, double* C, int k, int64_t nsys,
                             double lambda, double ridge, double rthr, int rhs_unit, unsigned long long* fail_min,
-                            unsigned* rcond_min_bits, cudaStream_t st);
+                            unsigned* rcond_min_bits, unsigned* rcond_exact, double* spill, cudaStream_t st);
 cudaError_t launch_validate_f64(const double* g, const double* r, const double* m, size_t n, unsigned* flags,
                                 cudaStream_t st);
 cudaError_t launch_residual_f64(const double* Cm, const double* G, const double* R, const double* M, int64_t b,

@@ -40,6 +40,7 @@
 // below the threshold, or a non-finite solution (lowest failing index wins).
 #include "fmap_kernels.cuh"
 #include "fmap_solver.cuh"
+#include "tc_ptx.cuh"
 
 #include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
@@ -146,181 +147,7 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   return L;
 }
 
-// ---------------------------------------------------------------------------
-// PTX wrappers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  const uint32_t a = su32(b);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n.reg .pred P1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
-        "selp.u32 %0, 1, 0, P1;\n}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity), "r"(0x989680u)
-        : "memory");
-  } while (!ok);
-}
-
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(slot)),
-               "r"(ncols)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
-               : "memory");
-}
-
-// 32 lanes x 16 consecutive 32-bit columns (lane = this warp's TMEM lane quarter).
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-      "[%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
-                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
-                 "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-               :
-               : "memory");
-#pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
-}
-
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16};" ::"r"(taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15]))
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// Shared-memory matrix descriptor, K-major, no swizzle: core matrices of 8 rows x
-// 16 B; LBO = distance between the two K-adjacent core matrices (128 B),
-// SBO = distance between 8-row groups (512 B).  Version field = 1 (sm_100).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128u >> 4) << 16) |
-         ((uint64_t)(512u >> 4) << 32) | (1ull << 46);
-}
-
-// Instruction descriptor: D f32, A/B tf32, K-major, A negated (D += -A*B), M=128.
-__device__ __forceinline__ uint32_t idesc_tf32(int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 13) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t acc = 1u) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(dtmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   su32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes)
-               : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(bar))
-      : "memory");
-}
-// 3-D / 2-D tensor TMA loads (box from the tensor map) into shared memory.
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
-      : "memory");
-}
-// 4-D tensor TMA load (box from the tensor map) into shared memory.
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-      "[%6];" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
-      : "memory");
-}
-// Shared-memory descriptor with explicit leading / stride byte offsets (no swizzle).
-__device__ __forceinline__ uint64_t sdesc_ls(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
-// shared memory (128 rows x 32 B, core-matrix layout) -> TMEM lanes 0..127, 8 columns
-__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t desc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
-}
-// Named barrier over the main (factorization) warps only.
-__device__ __forceinline__ void main_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
-
-__device__ __forceinline__ float rsqrt_fast(float x) {
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// x = hi + lo with hi = round-to-nearest TF32; lo is exact in fp32 and the tensor
-// core reads it as TF32 (truncated): |x - hi - tf32(lo)| <= 2^-21 |x|.
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  lo = x - hi;
-}
+using namespace ptx;
 
 // float index of element (r, t) (t < 16) in an operand buffer
 __device__ __forceinline__ int opnd_idx(int r, int t) {
@@ -397,10 +224,18 @@ __device__ __forceinline__ void trsm_row(const float* __restrict__ LT, const flo
 }
 
 // Debug phase trace (FMAP_TRACE_FILE): clock64 stamps of one CTA's second system.
+// Compiled in only with -DFMAP_TC_TRACE (tools/trace_panel.py), so the product
+// kernel carries no stamp code.
+#ifdef FMAP_TC_TRACE
 #define TC_TRACE(cond, slot)                                                              \
   do {                                                                                    \
     if (p.trace && tr_on && (cond)) p.trace[(slot)] = clock64();                          \
   } while (0)
+#else
+#define TC_TRACE(cond, slot) \
+  do {                       \
+  } while (0)
+#endif
 
 // Launch-local system number sl -> (pair q, row i).  A full batch is walked pair-
 // interleaved (consecutive sl hit different pairs), so the CTAs running at the
@@ -893,7 +728,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
               }
       };
       uint32_t gm = 0, n_chk = 0, n_cpd = 0, n_a0 = 0;
-      for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x) {
+      int nmi = 0;
+      for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x, ++nmi) {
+        const bool tr_on = blockIdx.x == (unsigned)p.trace_block && nmi == 1;
         const int64_t pi2 = pi + gridDim.x;
         const bool pf = Ly.tma && pi2 < npi;
         int64_t qn[NS];
@@ -907,6 +744,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         bool cpd_pending = false;
         for (int pp = 0; pp < P; ++pp, ++gm) {
           mbar_wait(opsready, gm & 1);
+          TC_TRACE(pp < 16, 800 + pp);
           mbar_arrive(ysync);
           tc_fence_after();
           const int r0 = 16 * pp + 16;
@@ -916,6 +754,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
             for (int gg = 0; gg < kMaxGroups; ++gg)
               if (gg < Ly.G && Ly.hi[gg] > r0) mma3(h, Ly.lo[gg], Ly.base[gg], r0, 16);
           mma_commit(&mbar[0]);
+          TC_TRACE(pp < 16, 820 + pp);
           // next pair: panel-0 columns (a0s is free: every main warp is past panel 0)
           // and chunk pp into the tile (free once the previous chunk's copies are done)
           if (pf && pp == 0) {
@@ -949,6 +788,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
               }
             }
           mma_commit(&mbar[1]);
+          TC_TRACE(pp < 16, 840 + pp);
           if (pf && pp >= 1) {  // chunk pp of the current pair was read at this panel's top
             mbar_wait(chk, n_chk & 1);
             ++n_chk;
@@ -1284,6 +1124,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
       for (int gg = 0; gg < kMaxGroups; ++gg)
         if (gg < Ly.G && j >= Ly.lo[gg] && j < Ly.hi[gg]) dwarp = 4 * gg + ((j - Ly.lo[gg]) >> 5);
       if (warp == dwarp) {
+        TC_TRACE(lane == 0 && pp < 16, 900 + 4 * pp + 1);
         const bool upper = ((j - glo) & 31) != 0;         // diagonal rows in lanes 16..31
         const bool own = (lane >= 16) == upper;           // this lane holds a diagonal row
         const int hs = own ? 0 : NS - 1;                  // system factored by this lane
@@ -1318,6 +1159,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         };
         if constexpr (NS == 1) {
           diag_emit(a[0], own);
+          TC_TRACE(lane == 0 && pp < 16, 900 + 4 * pp + 2);
           // the other half-warp's rows were clobbered by the factorization: reload
           if (pp == 0) {
             load_a0(0, a[0]);
@@ -1340,6 +1182,14 @@ __global__ void __launch_bounds__(MAXT, MINB)
         TC_TRACE(row == j, 3 + 4 * pp);
       }
       main_sync(NM);
+      TC_TRACE(tid == 0 && pp < 16, 1100 + pp);
+#ifdef FMAP_TC_TRACE
+      if (lane == 0 && warp < 8 && pp < 12 && p.trace && tr_on) {  // barrier release as seen by each warp
+        volatile float sink = LTb[0];
+        (void)sink;
+        p.trace[1400 + 8 * pp + warp] = clock64();
+      }
+#endif
       // c. TRSM rows >= j+16 ; augmented row -> y for this panel
       float l[NS][16];
       const bool trsm = active && row >= j + 16;
@@ -1358,6 +1208,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
           for (int t = 0; t < 16; ++t) yv[j + t] = l[h][t];
         }
       }
+      TC_TRACE(tid == 0 && pp < 16, 1120 + pp);
+      TC_TRACE(lane == 0 && pp < 12 && warp < 8, 1200 + 8 * pp + warp);
       // d. store L21: scratch (back substitution), operand hi/lo
       if (trsm) {
 #pragma unroll
@@ -1369,6 +1221,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
             __stcg(dst + c4, make_float4(l[h][4 * c4], l[h][4 * c4 + 1], l[h][4 * c4 + 2], l[h][4 * c4 + 3]));
         }
         if (pp > 0) mbar_wait(&mbar[1], (g - 1) & 1);  // previous REST MMA done reading
+        TC_TRACE(lane == 0 && pp < 12 && warp < 8, 1300 + 8 * pp + warp);
 #pragma unroll
         for (int h = 0; h < NS; ++h) {
           float* hp = opnd_hi + h * opsz + opnd_idx(row, 0);
@@ -1387,7 +1240,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
       fence_async_smem();
       tc_fence_before();  // this panel's TMEM reads precede the MMA warp's copies into chunk pp
       __syncwarp();
-      if (lane == 0) mbar_arrive(opsready);  // operands of this panel stored
+      if (lane == 0) {
+        TC_TRACE(pp < 12 && warp < 8, 700 + 8 * pp + warp);
+        mbar_arrive(opsready);  // operands of this panel stored
+      }
       any_mma = true;
 #pragma unroll
       for (int h = 0; h < NS; ++h)

@@ -20,7 +20,8 @@ def _problems(oracle, b, k, d, seed, kind=1):
     return np.stack(Gs), np.stack(Rs), np.stack(Ms)
 
 
-@pytest.mark.parametrize("k,b", [(1, 3), (5, 3), (16, 3), (40, 3), (100, 2), (200, 1), (234, 1)])
+@pytest.mark.parametrize("k,b", [(1, 3), (5, 3), (16, 3), (40, 3), (100, 2), (200, 1), (234, 1), (240, 2),
+                                 (300, 2)])
 def test_f64_route_matches_reference_batched_f64(fm, oracle, k, b):
     G, R, M = _problems(oracle, b, k, 2 * k if k < 128 else 256, 500 + k, kind=0 if k == 1 else 1)
     lam = 100.0
@@ -63,7 +64,7 @@ def test_f64_validation_and_limits(fm, oracle):
         fm.solve_host(G, nan, M, 1.0, precision="f64")
     with pytest.raises(fm.InvalidArgument):
         fm.solve_host(G, R, M, -1.0, precision="f64")
-    k = 240  # beyond the single-CTA f64 limit (packed triangle in shared memory)
+    k = 513  # beyond the f64 route's limit (rows past shared memory spill to L2 up to k = 512)
     z = np.zeros((1, k, k))
     with pytest.raises(fm.InvalidArgument, match="f64 route"):
         fm.solve_host(z + np.eye(k), z, z, 1.0, precision="f64")
@@ -80,3 +81,26 @@ def test_f64_fault_hook_matches_reference_fault(fm, oracle):
     ref = oracle.solve(G, R, M, 100.0, route="batched", dtype=np.float64, threads=0, inject_fault=True).maps
     assert np.abs(faulted - clean).max() > 1e-6
     assert np.abs(faulted - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("k", [24, 240])
+def test_f64_rcond_verdict_matches_reference(fm, oracle, k):
+    # solver.hpp:164-168 in f64 (threshold 1e-14 by default): thresholds placed on
+    # both sides of the reference's estimate force the exact Hager/Higham path;
+    # the verdict and the estimate must agree (k = 240 runs the spilled kernel)
+    rng = np.random.default_rng(k)
+    Q, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    G = (Q * np.logspace(0, -6, k)) @ Q.T
+    G = 0.5 * (G + G.T)
+    R = rng.standard_normal((k, k))
+    M = np.zeros((k, k))
+    r0 = oracle.rcond(G, np.float64)
+    ok = fm.solve_host(G[None], R[None], M[None], 0.0, fm.SolverOptions(rcond_threshold=r0 / 1.5), precision="f64")
+    assert 0.95 <= ok.min_rcond / r0 <= 1.05
+    assert ok.rcond_exact_systems == k
+    with pytest.raises(fm.SingularSystemError) as ei:
+        fm.solve_host(G[None], R[None], M[None], 0.0, fm.SolverOptions(rcond_threshold=r0 * 1.5), precision="f64")
+    assert ei.value.system() == 0
+    # the default threshold (1e-14) accepts it
+    out = fm.solve_host(G[None], R[None], M[None], 0.0, precision="f64")
+    assert out.min_rcond >= 1e-14
