@@ -144,6 +144,25 @@ int fmap_project_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t
                          const float* d_phi, const float* d_mass, const float* d_F,
                          float* d_out);
 
+/* Replaces project_to_spectral<Scalar>(basis, features, opts) (spectral.hpp:47-93)
+ * for b bases at once: A[q] = pinv(Phi[q]) F[q] (k x d), Phi [b][n][k], F [b][n][d].
+ * Decisions as the reference: n < k or cond(Phi) > condition_threshold (the
+ * reference default is 1e10) take the rank-revealing path, where a basis of
+ * numerical rank < k (threshold eps * min(n, k) * sigma_max) is an error:
+ * FMAP_RANK_DEFICIENT (RankDeficientError), report->failing_system = the lowest
+ * such shape, rank_out[q] (optional, b entries) = every shape's detected rank.
+ * Computed in f64 on the device (one-sided Jacobi SVD per shape); the f32 entry
+ * widens its inputs on the device and rounds A back. */
+int fmap_project_pinv_f64(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d, const double* phi,
+                          const double* F, double condition_threshold, double* A_out, int64_t* rank_out,
+                          fmap_report* report);
+int fmap_project_pinv_f64_dev(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d, const double* d_phi,
+                              const double* d_F, double condition_threshold, double* d_A, int64_t* rank_out,
+                              fmap_report* report);
+int fmap_project_pinv_f32(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d, const float* phi,
+                          const float* F, float condition_threshold, float* A_out, int64_t* rank_out,
+                          fmap_report* report);
+
 /* check_stationarity (solver.hpp:116-128) per pair: out[q] =
  * ||C G + lambda M.*C - R||_F, fp32 products, fp64 accumulation. */
 int fmap_residual_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_C,

@@ -21,7 +21,7 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 LIB = HERE / "_build" / "liboracle.so"
 
-OK, INVALID_ARGUMENT, SINGULAR, MEMORY_CAP = 0, 1, 2, 3
+OK, INVALID_ARGUMENT, SINGULAR, MEMORY_CAP, RANK_DEFICIENT = 0, 1, 2, 3, 5
 
 
 class Opts(C.Structure):
@@ -74,6 +74,7 @@ def lib() -> C.CDLL:
             ("oracle_randn", None, [I, I, C.c_uint64, P]),
             ("oracle_hardware_threads", C.c_uint, []),
             ("oracle_rcond_f64", D, [I, P]),
+            ("oracle_project_pinv", I, [I64, I, I, P, P, D, P, C.POINTER(C.c_int), C.c_char_p]),
             ("oracle_rcond_f32", F, [I, P]),
         ]:
             fn = getattr(L, name)
@@ -208,6 +209,26 @@ def rcond(A, dtype=np.float32) -> float:
     A = _c(A, dtype)
     fn = lib().oracle_rcond_f64 if dtype == np.float64 else lib().oracle_rcond_f32
     return float(fn(A.shape[0], _p(A)))
+
+
+def project_pinv(basis, features, condition_threshold=1e10):
+    """project_to_spectral (spectral.hpp:47-93) in double: pinv(basis) @ features.
+    Raises OracleError(RANK_DEFICIENT) with .rank / .expected on a rank-deficient basis."""
+    B, F = _c(basis, np.float64), _c(features, np.float64)
+    n, k = B.shape
+    d = F.shape[1]
+    out = np.zeros((k, d))
+    rank = C.c_int(0)
+    msg = C.create_string_buffer(256)
+    st = lib().oracle_project_pinv(n, k, d, _p(B), _p(F), condition_threshold, _p(out), C.byref(rank), msg)
+    if st != OK:
+        r = Report()
+        r.message = msg.value
+        r.failing_system = -1
+        err = OracleError(st, r)
+        err.rank, err.expected = rank.value, k
+        raise err
+    return out
 
 
 def hardware_threads() -> int:

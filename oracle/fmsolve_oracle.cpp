@@ -45,7 +45,7 @@
 
 namespace {
 
-enum Status { OK = 0, INVALID_ARGUMENT = 1, SINGULAR = 2, MEMORY_CAP = 3 };
+enum Status { OK = 0, INVALID_ARGUMENT = 1, SINGULAR = 2, MEMORY_CAP = 3, RANK_DEFICIENT = 5 };
 
 struct InvalidArgument : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -623,6 +623,177 @@ int oracle_project_mass(int64_t n, int k, int d, const double* phi, const double
       double* o = out + (size_t)i * d;
       for (int t = 0; t < d; ++t) o[t] += p * row[t];
     }
+  }
+  return OK;
+}
+
+// project_to_spectral (spectral.hpp:47-93) restated in double: pinv(basis) * F.
+// Normal equations when well conditioned (eigenvalues of B^T B by cyclic Jacobi,
+// cond = sqrt(ev_max / ev_min) <= threshold, then Cholesky); otherwise the
+// complete orthogonal decomposition's role is played by Householder QR with
+// column pivoting (the factor Eigen's COD is built on): rank = #{|R_ii| >
+// eps * min(n,k) * |R_00|} (Eigen's default ColPivHouseholderQR threshold);
+// rank < k -> RANK_DEFICIENT (rank in *rank_out); full rank -> least squares.
+// basis: n x k, features: n x d (row-major); out: k x d.  Returns 0 / 1 / 5.
+int oracle_project_pinv(int64_t n, int k, int d, const double* basis, const double* F, double cond_thr,
+                        double* out, int* rank_out, char* msg) {
+  auto fail = [&](int code, const std::string& m) {
+    if (msg) std::snprintf(msg, 256, "%s", m.c_str());
+    return code;
+  };
+  if (n < 1 || k < 1) return fail(INVALID_ARGUMENT, "basis must be non-empty");
+  if (d < 1) return fail(INVALID_ARGUMENT, "features must be non-empty");
+  for (size_t e = 0; e < (size_t)n * k; ++e)
+    if (!std::isfinite(basis[e])) return fail(INVALID_ARGUMENT, "basis contains non-finite entries");
+  for (size_t e = 0; e < (size_t)n * d; ++e)
+    if (!std::isfinite(F[e])) return fail(INVALID_ARGUMENT, "features contains non-finite entries");
+  if (rank_out) *rank_out = k;
+  auto rank_revealing = [&]() -> int {
+    // Householder QR with column pivoting of the n x k basis (column-major copy)
+    std::vector<double> a((size_t)n * k);
+    for (int64_t v = 0; v < n; ++v)
+      for (int j = 0; j < k; ++j) a[(size_t)j * n + v] = basis[(size_t)v * k + j];
+    std::vector<int> perm(k);
+    for (int j = 0; j < k; ++j) perm[j] = j;
+    std::vector<double> cn(k), tau(k, 0.0);
+    for (int j = 0; j < k; ++j) {
+      double s2 = 0;
+      for (int64_t v = 0; v < n; ++v) s2 += a[(size_t)j * n + v] * a[(size_t)j * n + v];
+      cn[j] = s2;
+    }
+    const int m = (int)std::min<int64_t>(n, k);
+    for (int i = 0; i < m; ++i) {
+      int best = i;
+      for (int j = i + 1; j < k; ++j)
+        if (cn[j] > cn[best]) best = j;
+      if (best != i) {
+        for (int64_t v = 0; v < n; ++v) std::swap(a[(size_t)i * n + v], a[(size_t)best * n + v]);
+        std::swap(cn[i], cn[best]);
+        std::swap(perm[i], perm[best]);
+      }
+      double* col = a.data() + (size_t)i * n;
+      double nrm = 0;
+      for (int64_t v = i; v < n; ++v) nrm += col[v] * col[v];
+      nrm = std::sqrt(nrm);
+      if (nrm == 0.0) continue;
+      const double alpha = col[i] > 0 ? -nrm : nrm;
+      const double v0 = col[i] - alpha;
+      for (int64_t v = i + 1; v < n; ++v) col[v] /= v0;
+      tau[i] = -v0 / alpha;
+      col[i] = alpha;
+      for (int j = i + 1; j < k; ++j) {
+        double* cj = a.data() + (size_t)j * n;
+        double w = cj[i];
+        for (int64_t v = i + 1; v < n; ++v) w += col[v] * cj[v];
+        w *= tau[i];
+        cj[i] -= w;
+        for (int64_t v = i + 1; v < n; ++v) cj[v] -= w * col[v];
+        double s2 = 0;
+        for (int64_t v = i + 1; v < n; ++v) s2 += cj[v] * cj[v];
+        cn[j] = s2;
+      }
+    }
+    const double r00 = m > 0 ? std::abs(a[0]) : 0.0;
+    const double thr = std::numeric_limits<double>::epsilon() * (double)m * r00;
+    int rank = 0;
+    for (int i = 0; i < m; ++i)
+      if (std::abs(a[(size_t)i * n + i]) > thr) ++rank;
+    if (rank_out) *rank_out = rank;
+    if (rank < k)
+      return fail(RANK_DEFICIENT, "basis is rank deficient: rank " + std::to_string(rank) + " < " +
+                                      std::to_string(k) + " columns");
+    // full rank: x = P R^{-1} (Q^T F)
+    std::vector<double> qf((size_t)n * d);
+    for (int64_t v = 0; v < n; ++v)
+      for (int t = 0; t < d; ++t) qf[(size_t)t * n + v] = F[(size_t)v * d + t];
+    for (int i = 0; i < k; ++i) {
+      const double* col = a.data() + (size_t)i * n;
+      for (int t = 0; t < d; ++t) {
+        double* f = qf.data() + (size_t)t * n;
+        double w = f[i];
+        for (int64_t v = i + 1; v < n; ++v) w += col[v] * f[v];
+        w *= tau[i];
+        f[i] -= w;
+        for (int64_t v = i + 1; v < n; ++v) f[v] -= w * col[v];
+      }
+    }
+    for (int t = 0; t < d; ++t) {
+      std::vector<double> z(k);
+      for (int i = k - 1; i >= 0; --i) {
+        double sacc = qf[(size_t)t * n + i];
+        for (int j = i + 1; j < k; ++j) sacc -= a[(size_t)j * n + i] * z[j];
+        z[i] = sacc / a[(size_t)i * n + i];
+      }
+      for (int i = 0; i < k; ++i) out[(size_t)perm[i] * d + t] = z[i];
+    }
+    return OK;
+  };
+  if (n < k) return rank_revealing();
+  // gram = B^T B and its eigenvalues (cyclic Jacobi)
+  std::vector<double> g((size_t)k * k, 0.0);
+  for (int64_t v = 0; v < n; ++v)
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) g[(size_t)i * k + j] += basis[(size_t)v * k + i] * basis[(size_t)v * k + j];
+  std::vector<double> e(g);
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0;
+    for (int i = 0; i < k; ++i)
+      for (int j = i + 1; j < k; ++j) off += e[(size_t)i * k + j] * e[(size_t)i * k + j];
+    if (off < 1e-30) break;
+    for (int p2 = 0; p2 < k; ++p2)
+      for (int q2 = p2 + 1; q2 < k; ++q2) {
+        const double apq = e[(size_t)p2 * k + q2];
+        if (apq == 0.0) continue;
+        const double app = e[(size_t)p2 * k + p2], aqq = e[(size_t)q2 * k + q2];
+        const double theta = (aqq - app) / (2 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1));
+        const double c = 1 / std::sqrt(t * t + 1), sn = t * c;
+        for (int r = 0; r < k; ++r) {
+          const double arp = e[(size_t)r * k + p2], arq = e[(size_t)r * k + q2];
+          e[(size_t)r * k + p2] = c * arp - sn * arq;
+          e[(size_t)r * k + q2] = sn * arp + c * arq;
+        }
+        for (int r = 0; r < k; ++r) {
+          const double apr = e[(size_t)p2 * k + r], aqr = e[(size_t)q2 * k + r];
+          e[(size_t)p2 * k + r] = c * apr - sn * aqr;
+          e[(size_t)q2 * k + r] = sn * apr + c * aqr;
+        }
+      }
+  }
+  double ev_min = e[0], ev_max = e[0];
+  for (int i = 1; i < k; ++i) {
+    ev_min = std::min(ev_min, e[(size_t)i * k + i]);
+    ev_max = std::max(ev_max, e[(size_t)i * k + i]);
+  }
+  if (!(ev_min > 0.0 && std::sqrt(ev_max / ev_min) <= cond_thr)) return rank_revealing();
+  // LLT of the gram, then solve gram * X = B^T F
+  std::vector<double> l(g);
+  for (int j = 0; j < k; ++j) {
+    double dj = l[(size_t)j * k + j];
+    for (int t = 0; t < j; ++t) dj -= l[(size_t)j * k + t] * l[(size_t)j * k + t];
+    if (!(dj > 0.0)) return rank_revealing();
+    dj = std::sqrt(dj);
+    l[(size_t)j * k + j] = dj;
+    for (int i = j + 1; i < k; ++i) {
+      double v = l[(size_t)i * k + j];
+      for (int t = 0; t < j; ++t) v -= l[(size_t)i * k + t] * l[(size_t)j * k + t];
+      l[(size_t)i * k + j] = v / dj;
+    }
+  }
+  for (int t = 0; t < d; ++t) {
+    std::vector<double> z(k);
+    for (int i = 0; i < k; ++i) {
+      double sacc = 0;
+      for (int64_t v = 0; v < n; ++v) sacc += basis[(size_t)v * k + i] * F[(size_t)v * d + t];
+      for (int j = 0; j < i; ++j) sacc -= l[(size_t)i * k + j] * z[j];
+      z[i] = sacc / l[(size_t)i * k + i];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double sacc = z[i];
+      for (int j = i + 1; j < k; ++j) sacc -= l[(size_t)j * k + i] * z[j];
+      z[i] = sacc / l[(size_t)i * k + i];
+    }
+    for (int i = 0; i < k; ++i) out[(size_t)i * d + t] = z[i];
   }
   return OK;
 }

@@ -25,6 +25,7 @@ from .fmsolve import (  # noqa: F401
     mask_resolvent,
     normal_equations,
     pipeline_device,
+    project_to_spectral,
     solve_batched,
     solve_batched_many,
     solve_cuda,

@@ -32,6 +32,7 @@ EXPORTED = [
     "fmap_normal_equations_f32", "fmap_normal_equations_f32_dev", "fmap_project_f32_dev",
     "fmap_residual_f32_dev", "fmap_pipeline_f32_dev", "fmap_max_resolution",
     "fmap_last_launch_count", "fmap_last_launches", "fmap_solve_f64", "fmap_solve_f64_dev",
+    "fmap_project_pinv_f64", "fmap_project_pinv_f64_dev", "fmap_project_pinv_f32",
 ]
 
 
@@ -100,6 +101,9 @@ def load() -> C.CDLL:
             "fmap_max_resolution": (I64, [P]),
             "fmap_last_launch_count": (I64, [P]),
             "fmap_last_launches": (C.c_char_p, [P]),
+            "fmap_project_pinv_f64": (I, [P, I64, I64, I64, I64, P, P, C.c_double, P, P, rep]),
+            "fmap_project_pinv_f64_dev": (I, [P, I64, I64, I64, I64, P, P, C.c_double, P, P, rep]),
+            "fmap_project_pinv_f32": (I, [P, I64, I64, I64, I64, P, P, F, P, P, rep]),
         }
         for name, (res, args) in sig.items():
             if os.environ.get("FMAP_LIB_VARIANT") and not hasattr(lib, name):

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libfmap_cuda.so"
-SOURCES = ["fmap_tc.cu", "fmap_gram.cu", "fmap_f64.cu", "fmap_kernels.cu", "fmap_capi.cu"]
+SOURCES = ["fmap_tc.cu", "fmap_gram.cu", "fmap_f64.cu", "fmap_pinv.cu", "fmap_kernels.cu", "fmap_capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

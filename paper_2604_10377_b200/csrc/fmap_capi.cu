@@ -214,7 +214,10 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
                        std::to_string(kmax) + " on this device");
   const size_t kk = (size_t)k * k;
   const size_t nsys = (size_t)b * k;
-  const bool need_mask_scratch = opts.compute_residual && mask_mode != 0;
+  // check_stationarity inside the solver (its own warp) unless the fault hook
+  // rewrites a row after the solve
+  const bool res_in_kernel = opts.compute_residual && !opts.inject_fault && tc_inkernel_residual((int)k);
+  const bool need_mask_scratch = opts.compute_residual && mask_mode != 0 && !res_in_kernel;
   const size_t res_partial = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
   const size_t tc_bytes = tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms);
   const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
@@ -277,6 +280,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   p.rcond_exact = d_nexact(ctx);
   p.tc_scratch = tc_scr;
   p.gram_rowsum = rowsum;
+  p.res_partial = res_in_kernel ? partial : nullptr;
 
   // debug: FMAP_TRACE_FILE=<path> dumps per-warp clock64 phase stamps of one block
   const char* trace_file = std::getenv("FMAP_TRACE_FILE");
@@ -341,6 +345,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
       }
     const float alpha = -2.f * g0[w];
     SolveParams pz = p;
+    pz.res_partial = nullptr;
     pz.C = zrow;  // system 0 writes its row at offset 0
     pz.nsys = 1;
     pz.rhs_unit = 0;
@@ -349,7 +354,9 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
 
-  if (opts.compute_residual) {
+  if (res_in_kernel) {
+    FMAP_CK(ctx, launch_residual_finish(partial, b, (int)k, res_out, ctx->stream));
+  } else if (opts.compute_residual) {
     const float* Muse = M;
     if (mask_mode != 0) {
       FMAP_CK(ctx, launch_mask(ev1, ev2, b, (int)k, mask_mode == 1 ? 1 : 0, sigma, mask_scratch,
@@ -460,6 +467,8 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   p.mask = dM;
   p.C = dC;
   p.gram_rowsum = rowsum;
+  const bool res_in_kernel = opts.compute_residual && tc_inkernel_residual((int)k);
+  p.res_partial = res_in_kernel ? partial : nullptr;
   for (int c = 0; c < nchunk; ++c) {  // all H2D first: the copy stream never waits on the solver
     const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
     if (nq <= 0) break;
@@ -495,7 +504,10 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
     // chunk's D2H
     FMAP_CK(ctx, cudaEventRecord(ctx->cev[36], comp[1]));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[36], 0));
-    FMAP_CK(ctx, launch_residual(dC, dG, dR, dM, b, (int)k, lambda, partial, res_out, ctx->stream));
+    if (res_in_kernel)  // the per-system partials came out of the solver chunks
+      FMAP_CK(ctx, launch_residual_finish(partial, b, (int)k, res_out, ctx->stream));
+    else
+      FMAP_CK(ctx, launch_residual(dC, dG, dR, dM, b, (int)k, lambda, partial, res_out, ctx->stream));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[1], ctx->copy2));
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[1], 0));
@@ -642,6 +654,52 @@ cudaError_t normal_products(int n, const float* const* X, const float* const* Y,
   return cudaSuccess;
 }
 
+// project_to_spectral (spectral.hpp:47-93) on device f64 buffers; `convert`
+// = inputs were fp32 and have been widened into the staging arena already.
+int project_pinv_core(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d, const double* phi,
+                      const double* F, double cond_thr, double* A, int64_t* rank_out, fmap_report* rep) {
+  init_report(rep);
+  if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no bases to project onto");
+  if (n < 1 || k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "basis must be non-empty");
+  if (d < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "features must be non-empty");
+  if (b > 65535) return set_err(ctx, FMAP_INVALID_ARGUMENT, "at most 65535 shapes per call");
+  if (!phi || !F || !A) return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
+  const size_t work = pinv_work_doubles(b, n, (int)k, (int)d);
+  const size_t scratch = carve_size({work * sizeof(double), (size_t)b * sizeof(int)});
+  int st = scratch_reserve(ctx, scratch);
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->scr)};
+  double* dwork = cv.take<double>(work);
+  int* drank = cv.take<int>((size_t)b);
+  if ((st = reset_ctrl(ctx))) return st;
+  FMAP_CK(ctx, launch_finite_f64(phi, (size_t)b * n * k, 1u, d_flags(ctx), ctx->stream));
+  FMAP_CK(ctx, launch_finite_f64(F, (size_t)b * n * d, 2u, d_flags(ctx), ctx->stream));
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  FMAP_CK(ctx, launch_pinv(phi, F, b, n, (int)k, (int)d, cond_thr, dwork, A, drank, d_fail(ctx), ctx->stream));
+  FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  unsigned long long fail;
+  float rc;
+  unsigned flags;
+  if ((st = read_ctrl(ctx, &fail, &rc, &flags))) return st;
+  if (flags & 1u) return set_err(ctx, FMAP_INVALID_ARGUMENT, "basis contains non-finite entries");
+  if (flags & 2u) return set_err(ctx, FMAP_INVALID_ARGUMENT, "features contains non-finite entries");
+  float ms = 0.f;
+  FMAP_CK(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (rep) rep->wall_seconds = ms * 1e-3;
+  std::vector<int> ranks((size_t)b);
+  FMAP_CK(ctx, cudaMemcpy(ranks.data(), drank, (size_t)b * sizeof(int), cudaMemcpyDeviceToHost));
+  if (rank_out)
+    for (int64_t q = 0; q < b; ++q) rank_out[q] = ranks[(size_t)q];
+  if (fail != kNoFail) {
+    if (rep) rep->failing_system = (int64_t)fail;
+    return set_err(ctx, FMAP_RANK_DEFICIENT,
+                   "basis is rank deficient: rank " + std::to_string(ranks[(size_t)fail]) + " < " +
+                       std::to_string(k) + " columns (shape " + std::to_string(fail) + ")");
+  }
+  ctx->last_error.clear();
+  return FMAP_OK;
+}
+
 bool host_finite(const float* p, size_t n) {
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) return false;
@@ -724,6 +782,70 @@ int64_t fmap_max_resolution(fmap_ctx* ctx) { return ctx ? max_resolution(ctx) : 
 int64_t fmap_last_launch_count(const fmap_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 const char* fmap_last_launches(const fmap_ctx* ctx) { return ctx ? ctx->launch_names.c_str() : ""; }
+
+int fmap_project_pinv_f64_dev(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d, const double* d_phi,
+                              const double* d_F, double condition_threshold, double* d_A, int64_t* rank_out,
+                              fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
+  return project_pinv_core(ctx, b, n, k, d, d_phi, d_F, condition_threshold, d_A, rank_out, report);
+}
+
+int fmap_project_pinv_f64(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d, const double* phi,
+                          const double* F, double condition_threshold, double* A_out, int64_t* rank_out,
+                          fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
+  init_report(report);
+  if (b < 1 || n < 1 || k < 1 || d < 1 || !phi || !F || !A_out)
+    return project_pinv_core(ctx, b, n, k, d, phi, F, condition_threshold, A_out, rank_out, report);
+  const size_t np = (size_t)b * n * k, nf = (size_t)b * n * d, na = (size_t)b * k * d;
+  int st = arena_reserve(ctx, carve_size({np * 8, nf * 8, na * 8}));
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  double* dP = cv.take<double>(np);
+  double* dF = cv.take<double>(nf);
+  double* dA = cv.take<double>(na);
+  FMAP_CK(ctx, cudaMemcpyAsync(dP, phi, np * 8, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(dF, F, nf * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = project_pinv_core(ctx, b, n, k, d, dP, dF, condition_threshold, dA, rank_out, report))) return st;
+  FMAP_CK(ctx, cudaMemcpyAsync(A_out, dA, na * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMAP_OK;
+}
+
+int fmap_project_pinv_f32(fmap_ctx* ctx, int64_t b, int64_t n, int64_t k, int64_t d, const float* phi,
+                          const float* F, float condition_threshold, float* A_out, int64_t* rank_out,
+                          fmap_report* report) {
+  if (!ctx) return FMAP_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->device);
+  LaunchScope ls(ctx);
+  init_report(report);
+  if (b < 1 || n < 1 || k < 1 || d < 1 || !phi || !F || !A_out)
+    return project_pinv_core(ctx, b, n, k, d, nullptr, nullptr, condition_threshold, nullptr, rank_out, report);
+  const size_t np = (size_t)b * n * k, nf = (size_t)b * n * d, na = (size_t)b * k * d;
+  int st = arena_reserve(ctx, carve_size({np * 4, nf * 4, na * 4, np * 8, nf * 8, na * 8}));
+  if (st) return st;
+  Carve cv{reinterpret_cast<char*>(ctx->arena)};
+  float* sP = cv.take<float>(np);
+  float* sF = cv.take<float>(nf);
+  float* sA = cv.take<float>(na);
+  double* dP = cv.take<double>(np);
+  double* dF = cv.take<double>(nf);
+  double* dA = cv.take<double>(na);
+  FMAP_CK(ctx, cudaMemcpyAsync(sP, phi, np * 4, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(sF, F, nf * 4, cudaMemcpyHostToDevice, ctx->stream));
+  FMAP_CK(ctx, launch_convert_f32_f64(sP, dP, np, ctx->stream));
+  FMAP_CK(ctx, launch_convert_f32_f64(sF, dF, nf, ctx->stream));
+  if ((st = project_pinv_core(ctx, b, n, k, d, dP, dF, (double)condition_threshold, dA, rank_out, report)))
+    return st;
+  FMAP_CK(ctx, launch_convert_f64_f32(dA, sA, na, ctx->stream));
+  FMAP_CK(ctx, cudaMemcpyAsync(A_out, sA, na * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return FMAP_OK;
+}
 
 int fmap_solve_f32_dev(fmap_ctx* ctx, int64_t b, int64_t k, const float* d_gram,
                        const float* d_rhs, const float* d_mask, float lambda,

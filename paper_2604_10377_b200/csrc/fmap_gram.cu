@@ -155,16 +155,35 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc_kernel(GramArgs a) {
     const bool live = 32 * warp + lane < mrows;
     const size_t ro = ((size_t)q * k + (live ? r : 0)) * k;
     double acc = 0.0;
+    const bool vec = (k & 3) == 0;
     for (int c0 = 0; c0 < N; c0 += 16) {
       float v[16];
       tmem_ld16(tl + (uint32_t)c0, v);
       if (live) {
+        float mv[16], xv[16], rv[16];
+        if (vec && c0 + 16 <= k) {  // 64 contiguous bytes of the row per array (float4 loads)
+#pragma unroll
+          for (int t4 = 0; t4 < 4; ++t4) {
+            const float4 m4 = __ldg(reinterpret_cast<const float4*>(jb.M + ro + c0) + t4);
+            const float4 x4 = __ldg(reinterpret_cast<const float4*>(Xq + (size_t)r * d + c0) + t4);
+            const float4 r4 = __ldg(reinterpret_cast<const float4*>(jb.R + ro + c0) + t4);
+            mv[4 * t4] = m4.x, mv[4 * t4 + 1] = m4.y, mv[4 * t4 + 2] = m4.z, mv[4 * t4 + 3] = m4.w;
+            xv[4 * t4] = x4.x, xv[4 * t4 + 1] = x4.y, xv[4 * t4 + 2] = x4.z, xv[4 * t4 + 3] = x4.w;
+            rv[4 * t4] = r4.x, rv[4 * t4 + 1] = r4.y, rv[4 * t4 + 2] = r4.z, rv[4 * t4 + 3] = r4.w;
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int c = c0 + t;
+            mv[t] = c < k ? __ldg(jb.M + ro + c) : 0.f;
+            xv[t] = c < k ? __ldg(Xq + (size_t)r * d + c) : 0.f;
+            rv[t] = c < k ? __ldg(jb.R + ro + c) : 0.f;
+          }
+        }
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          const int c = c0 + t;
-          if (c < k) {
-            const float e = v[t] + jb.lambda * (__ldg(jb.M + ro + c) * __ldg(Xq + (size_t)r * d + c)) -
-                            __ldg(jb.R + ro + c);
+          if (c0 + t < k) {
+            const float e = v[t] + jb.lambda * (mv[t] * xv[t]) - rv[t];
             acc += (double)e * (double)e;
           }
         }

@@ -504,6 +504,12 @@ cudaError_t launch_residual(const float* C, const float* G, const float* R, cons
   return cudaGetLastError();
 }
 
+cudaError_t launch_residual_finish(const double* partial, int64_t b, int k, double* out, cudaStream_t st) {
+  note_launch("residual_finish_kernel");
+  residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, k, (int)b, out);
+  return cudaGetLastError();
+}
+
 size_t residual_partial_count(int64_t b, int k) {
   return (size_t)b * k;  // per-row partials (tensor-core path); >= the SIMT kernel's b * ceil(k / 8)
 }

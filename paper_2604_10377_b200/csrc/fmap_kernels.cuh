@@ -34,6 +34,13 @@ cudaError_t launch_gram_tc(int nprod, const float* const* X, const float* const*
                            const int* sym, int64_t b, int k, int d, cudaStream_t st);
 cudaError_t launch_residual_tc(const float* C, const float* G, const float* R, const float* M, int64_t b, int k,
                                float lambda, double* partial, cudaStream_t st);
+// Euclidean pinv projection (fmap_pinv.cu), f64
+size_t pinv_work_doubles(int64_t b, int64_t n, int k, int d);
+cudaError_t launch_pinv(const double* phi, const double* F, int64_t b, int64_t n, int k, int d, double cond_thr,
+                        double* work, double* out, int* rank_out, unsigned long long* fail_min, cudaStream_t st);
+cudaError_t launch_convert_f32_f64(const float* x, double* y, size_t n, cudaStream_t st);
+cudaError_t launch_convert_f64_f32(const double* x, float* y, size_t n, cudaStream_t st);
+cudaError_t launch_finite_f64(const double* x, size_t n, unsigned bit, unsigned* flags, cudaStream_t st);
 cudaError_t launch_gemm_nt(const float* X, const float* Y, int64_t b, int M, int N, int K,
                            float* out, cudaStream_t st);
 cudaError_t launch_project(const float* phi, const float* mass, const float* F, int64_t b,
@@ -42,6 +49,8 @@ cudaError_t launch_residual(const float* C, const float* G, const float* R, cons
                             int64_t b, int k, float lambda, double* partial, double* out,
                             cudaStream_t st);
 size_t residual_partial_count(int64_t b, int k);
+// per-pair sqrt(sum of the k per-system partials) (in-kernel check_stationarity)
+cudaError_t launch_residual_finish(const double* partial, int64_t b, int k, double* out, cudaStream_t st);
 cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,
                                  unsigned long long* fail_min, unsigned long long sys,
                                  cudaStream_t st);

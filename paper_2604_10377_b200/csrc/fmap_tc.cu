@@ -71,6 +71,7 @@ struct TcLayout {
   int ns;  // systems factored in lockstep per CTA (same row -> same thread)
   int tma; // next pair's G staged by TMA + tcgen05.cp during the current pair's panels
   int nmain, bwarp, mwarp, threads, aug_tid;
+  int rwarp;  // check_stationarity warp (one system behind the back substitution), -1 when absent
   int tcols1;     // TMEM columns of one system
   int tmem_cols;  // allocated (ns * tcols1, power of two)
   int Rop;  // operand buffer rows
@@ -78,6 +79,7 @@ struct TcLayout {
   // offsets in floats from the dynamic smem base
   int off_hi, off_lo, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_a0, off_stg, off_misc;
   int off_uv, off_wv, off_hv;  // rcond (back-substitution warp): comparison solves u, w; Hager vectors
+  int off_xr;                  // residual warp: x of the last two systems [2][K16] + valid flags
   int floats;
   long long lb;  // floats of one L scratch slot (global memory)
 };
@@ -119,6 +121,8 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.bwarp = L.nmain / 32;      // back-substitution warps bwarp .. bwarp+ns-1 (one per system)
   L.mwarp = L.bwarp + ns;      // MMA-issue warp
   L.threads = L.nmain + 32 * ns + 32;
+  L.rwarp = (ns == 1 && L.threads + 32 <= 384) ? L.mwarp + 1 : -1;
+  if (L.rwarp >= 0) L.threads += 32;
   L.Rop = L.K16 > kTL ? L.K16 : kTL;
   const int lbs = (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;
   int o = 0;
@@ -137,6 +141,7 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.off_a0 = o;  o += ns * L.K16 * 16;          // panel-0 columns of every row (float4 [h][t4][row])
   o = (o + 255) & ~255;                         // 1 KB aligned (TMA destination)
   L.off_stg = o; o += ns * L.G * 4 * kTL * 4;   // one G chunk of every (system, group): [h][g][u][128 rows][4]
+  L.off_xr = o;  o += 2 * L.K16 + 32;
   L.off_misc = o; o += 128;
   L.floats = o;
   L.lb = (lb_off(L.P, L.K16) + 31) & ~31ll;
@@ -310,6 +315,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
   uint64_t* cpd = chk + 1;
   uint64_t* a0f = chk + 2;
   uint64_t* stg = chk + 3;
+  uint64_t* rready = chk + 4;  // [2] back-substitution warp -> residual warp (x of a system landed)
+  uint64_t* rfree = chk + 6;   // [2] residual warp -> back-substitution warp (slot consumed)
+  float* xres = smem + Ly.off_xr;                                   // [2][K16]
+  int* xres_ok = reinterpret_cast<int*>(smem + Ly.off_xr + 2 * K16);  // [2]
   float4* a0s = reinterpret_cast<float4*>(smem + Ly.off_a0);  // panel-0 columns: [(h*4 + t4)*K16 + row]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 48);
   unsigned* scb = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 56);  // [n&1][h][8]
@@ -329,7 +338,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
     scb[8 * tid + 4] = 0u;
   }
   if (tid == 0) {
-    for (int e = 0; e < 8 + 6 * NS; ++e) mbar_init(&mbar[e], e == 2 ? (uint32_t)(Ly.nmain / 32) : 1u);
+    const int nbar = 8 + 6 * NS + (Ly.rwarp >= 0 ? 4 : 0);  // + rready[2], rfree[2]
+    for (int e = 0; e < nbar; ++e) mbar_init(&mbar[e], e == 2 ? (uint32_t)(Ly.nmain / 32) : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, (uint32_t)Ly.tmem_cols);
@@ -663,8 +673,71 @@ __global__ void __launch_bounds__(MAXT, MINB)
           atomicMin(p.rcond_min_bits, __float_as_uint(rc));
         }
       }
+      if (Ly.rwarp >= 0 && p.res_partial) {  // hand x to the check_stationarity warp
+        const int rs = n & 1;
+        if (n >= 2) mbar_wait(&rfree[rs], ((n - 2) >> 1) & 1);
+        const bool ok = ssc[3] == 0u && p.rhs_unit < 0;
+        if (ok)
+          for (int c = lane; c < K16; c += 32) xres[rs * K16 + c] = xv[c];
+        if (lane == 0) xres_ok[rs] = ok ? 1 : 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rready[rs]);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bsub[slot]);
+    }
+    return;
+  }
+
+  // ======================= check_stationarity warp =======================
+  // solver.hpp:116-128 per system, one behind the back substitution:
+  // e_r = sum_c x_c G[c][r] + lambda m_i(r) x_r - R[i][r] (row i of C G +
+  // lambda M.*C - R; fp32 products, lanes over r so the G reads coalesce),
+  // res_partial[q k + i] = sum_r e_r^2 in fp64; residual_finish sums each pair.
+  if (warp == Ly.rwarp) {
+    if (!p.res_partial) return;
+    int n = 0;
+    for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x, ++n) {
+      const int rs = n & 1;
+      mbar_wait(&rready[rs], (n >> 1) & 1);
+      if (xres_ok[rs]) {
+        int64_t q;
+        int i;
+        sys_of(p, pi, q, i);
+        const float* x = xres + rs * K16;
+        const float* Gq = p.gram + (size_t)q * k * k;
+        float evm = 0.f;
+        if constexpr (MASK_MODE == 1) {
+          for (int c = lane; c < k; c += 32)
+            evm = fmaxf(evm, fmaxf(p.ev1[(size_t)q * k + c], p.ev2[(size_t)q * k + c]));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) evm = fmaxf(evm, __shfl_xor_sync(kFull, evm, o));
+        }
+        double acc = 0.0;
+        for (int r0 = 0; r0 < k; r0 += 32) {
+          const int r = r0 + lane;
+          if (r < k) {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            int c = 0;
+            for (; c + 4 <= k; c += 4) {
+              s0 = fmaf(x[c], __ldg(Gq + (size_t)c * k + r), s0);
+              s1 = fmaf(x[c + 1], __ldg(Gq + (size_t)(c + 1) * k + r), s1);
+              s2 = fmaf(x[c + 2], __ldg(Gq + (size_t)(c + 2) * k + r), s2);
+              s3 = fmaf(x[c + 3], __ldg(Gq + (size_t)(c + 3) * k + r), s3);
+            }
+            for (; c < k; ++c) s0 = fmaf(x[c], __ldg(Gq + (size_t)c * k + r), s0);
+            const float sg = (s0 + s1) + (s2 + s3);
+            const float m = mask_entry<MASK_MODE>(p, q, i, r, evm);
+            const float e = sg + p.lambda * (m * x[r]) - __ldg(p.rhs + ((size_t)q * k + i) * k + r);
+            acc += (double)e * (double)e;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (lane == 0) p.res_partial[(size_t)q * k + i] = acc;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rfree[rs]);
     }
     return;
   }
@@ -1365,6 +1438,9 @@ size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms) {
   return (size_t)grid * 2 * L.ns * (size_t)L.lb * sizeof(float);
 }
 
+// check_stationarity runs inside the solver (its own warp) for this k
+bool tc_inkernel_residual(int k) { return make_layout(k, tc_ns_override()).rwarp >= 0; }
+
 bool tc_supported(int k, int optin_smem) {
   if (k < 1) return false;
   const TcLayout L = make_layout(k, tc_ns_override());
@@ -1430,11 +1506,11 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
         default: fn = chol_tc_kernel<2, 2, 384, 1>; break;
       }
     }
-  } else if (L.cps >= 2 && L.threads <= 288) {  // two CTAs per SM
+  } else if (L.cps >= 2 && L.threads <= 320) {  // two CTAs per SM
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 1, 288, 2>; break;
-      case 1: fn = chol_tc_kernel<1, 1, 288, 2>; break;
-      default: fn = chol_tc_kernel<2, 1, 288, 2>; break;
+      case 0: fn = chol_tc_kernel<0, 1, 320, 2>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 320, 2>; break;
+      default: fn = chol_tc_kernel<2, 1, 320, 2>; break;
     }
   } else {
     switch (mask_mode) {

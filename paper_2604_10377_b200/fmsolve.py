@@ -322,6 +322,40 @@ solve_batched_many = solve_cuda_many
 solve_batched = solve_cuda
 
 
+def project_to_spectral(basis, features, condition_threshold: float = 1e10, device: int = 0,
+                        precision: str = "f64") -> np.ndarray:
+    """spectral.hpp:47-93 on the GPU: pinv(basis) @ features for one basis [n, k]
+    or a batch [b, n, k] (features [.., n, d]).  Raises RankDeficientError
+    (rank(), expected()) like the reference; InvalidArgument on bad input."""
+    B = np.asarray(basis)
+    Fm = np.asarray(features)
+    single = B.ndim == 2
+    if single:
+        B, Fm = B[None], Fm[None]
+    _require(B.ndim == 3 and B.shape[1] >= 1 and B.shape[2] >= 1, "basis must be non-empty")
+    _require(Fm.ndim == 3 and Fm.shape[2] >= 1 and Fm.shape[1] >= 1, "features must be non-empty")
+    if Fm.shape[1] != B.shape[1]:
+        raise InvalidArgument(f"feature row count ({Fm.shape[1]}) does not match basis vertex count ({B.shape[1]})")
+    _require(Fm.shape[0] == B.shape[0], "one feature matrix per basis")
+    b, n, k = B.shape
+    d = Fm.shape[2]
+    dt = np.float64 if precision == "f64" else np.float32
+    B = np.ascontiguousarray(B, dtype=dt)
+    Fm = np.ascontiguousarray(Fm, dtype=dt)
+    out = np.zeros((b, k, d), dt)
+    ranks = np.zeros(b, np.int64)
+    ctx = _ctx(device)
+    rep = _lib.ReportC()
+    fn = ctx._lib.fmap_project_pinv_f64 if precision == "f64" else ctx._lib.fmap_project_pinv_f32
+    st = fn(ctx.handle, b, n, k, d, _ptr(B), _ptr(Fm), float(condition_threshold), _ptr(out), _ptr(ranks),
+            C.byref(rep))
+    if st == _lib.FMAP_RANK_DEFICIENT:
+        q = int(rep.failing_system)
+        raise RankDeficientError(int(ranks[q]), k, ctx.last_error())
+    _raise(ctx, st, rep)
+    return out[0] if single else out
+
+
 def check_stationarity(c, a, b, mask, lam: float, device: int = 0) -> float:
     """solver.hpp:116-128: ||C AA^T + lambda (M .* C) - BA^T||_F (GPU, fp64 accumulation)."""
     import torch  # device plumbing only
