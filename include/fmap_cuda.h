@@ -94,7 +94,7 @@ void fmap_default_options(fmap_solver_options* opts);
  * (solver.hpp:132-145) runs on the device before any status is returned;
  * SINGULAR reports the lowest failing global system index; no partial results
  * on error (C_out is left untouched, or zero-filled when the copy-pipelined
- * path — batches of >= 16 pairs, FMAP_PIPELINE=<chunks> to tune, 1 to disable —
+ * path — batches of >= 8 pairs, 4 chunks, FMAP_PIPELINE=<chunks> to tune, 1 to disable —
  * had already copied some chunks back). */
 int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const float* rhs,
                    const float* mask, float lambda, const fmap_solver_options* opts,

@@ -214,10 +214,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
                        std::to_string(kmax) + " on this device");
   const size_t kk = (size_t)k * k;
   const size_t nsys = (size_t)b * k;
-  // check_stationarity inside the solver (its own warp) unless the fault hook
-  // rewrites a row after the solve
-  const bool res_in_kernel = opts.compute_residual && !opts.inject_fault && tc_inkernel_residual((int)k);
-  const bool need_mask_scratch = opts.compute_residual && mask_mode != 0 && !res_in_kernel;
+  const bool need_mask_scratch = opts.compute_residual && mask_mode != 0;
   const size_t res_partial = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
   const size_t tc_bytes = tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms);
   const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
@@ -280,7 +277,6 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   p.rcond_exact = d_nexact(ctx);
   p.tc_scratch = tc_scr;
   p.gram_rowsum = rowsum;
-  p.res_partial = res_in_kernel ? partial : nullptr;
 
   // debug: FMAP_TRACE_FILE=<path> dumps per-warp clock64 phase stamps of one block
   const char* trace_file = std::getenv("FMAP_TRACE_FILE");
@@ -345,7 +341,6 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
       }
     const float alpha = -2.f * g0[w];
     SolveParams pz = p;
-    pz.res_partial = nullptr;
     pz.C = zrow;  // system 0 writes its row at offset 0
     pz.nsys = 1;
     pz.rhs_unit = 0;
@@ -354,9 +349,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
 
-  if (res_in_kernel) {
-    FMAP_CK(ctx, launch_residual_finish(partial, b, (int)k, res_out, ctx->stream));
-  } else if (opts.compute_residual) {
+  if (opts.compute_residual) {
     const float* Muse = M;
     if (mask_mode != 0) {
       FMAP_CK(ctx, launch_mask(ev1, ev2, b, (int)k, mask_mode == 1 ? 1 : 0, sigma, mask_scratch,
@@ -467,8 +460,6 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   p.mask = dM;
   p.C = dC;
   p.gram_rowsum = rowsum;
-  const bool res_in_kernel = opts.compute_residual && tc_inkernel_residual((int)k);
-  p.res_partial = res_in_kernel ? partial : nullptr;
   for (int c = 0; c < nchunk; ++c) {  // all H2D first: the copy stream never waits on the solver
     const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
     if (nq <= 0) break;
@@ -492,22 +483,20 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
     p.tc_scratch = scr[c & 1];
     FMAP_CK(ctx, launch_chol_solve(p, 0, s));
     FMAP_CK(ctx, cudaEventRecord(done, s));
+    if (opts.compute_residual)  // check_stationarity tiles co-run with the next chunk's solve
+      FMAP_CK(ctx, launch_residual_tiles(dC + off, dG + off, dR + off, dM + off, nq, (int)k, lambda,
+                                         partial + (size_t)q0 * residual_tile_count((int)k), s));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy2, done, 0));
     FMAP_CK(ctx, cudaMemcpyAsync(C_out + off, dC + off, nb, cudaMemcpyDeviceToHost, ctx->copy2));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[3 + 2 * nchunk], ctx->copy));  // all H2D done (stream join)
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[3 + 2 * nchunk], 0));
   if (opts.compute_residual) {
-    // check_stationarity (solver.hpp:314-320) once over the whole batch on the
-    // tensor cores after every chunk's solve (a residual kernel cannot share an SM
-    // with a running solver chunk: both need tensor memory), overlapping the last
-    // chunk's D2H
+    // check_stationarity (solver.hpp:314-320): the per-chunk tiles ran beside the
+    // solver (no tensor memory, so they share SMs with a running chunk); join and sum
     FMAP_CK(ctx, cudaEventRecord(ctx->cev[36], comp[1]));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[36], 0));
-    if (res_in_kernel)  // the per-system partials came out of the solver chunks
-      FMAP_CK(ctx, launch_residual_finish(partial, b, (int)k, res_out, ctx->stream));
-    else
-      FMAP_CK(ctx, launch_residual(dC, dG, dR, dM, b, (int)k, lambda, partial, res_out, ctx->stream));
+    FMAP_CK(ctx, launch_residual_finish(partial, b, residual_tile_count((int)k), res_out, ctx->stream));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[1], ctx->copy2));
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[1], 0));
@@ -894,7 +883,11 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   // pipelined copies (tensor-core solver, >= 2 pairs per chunk, no fault injection /
   // residual); FMAP_PIPELINE=<chunks> overrides the default (1 = unpipelined)
   const char* pipe = std::getenv("FMAP_PIPELINE");
-  const int nchunk = pipe ? std::max(1, std::min(16, std::atoi(pipe))) : 8;
+  // 4 chunks: the copies of one chunk (~7.7 MB) hide behind the previous chunk's
+  // solve, and each chunk's 3200 systems keep the persistent grid (2 CTAs per SM)
+  // busy through its tail; 8 and 16 chunks measured 4 % and 17 % slower with the
+  // residual tiles on (tools/e2e_probe.py)
+  const int nchunk = pipe ? std::max(1, std::min(16, std::atoi(pipe))) : 4;
   if (nchunk > 1 && !o.inject_fault && b >= 2 * nchunk && k <= max_resolution(ctx))
     return solve_host_pipelined(ctx, b, k, gram, rhs, mask, lambda, o, C_out, report, nchunk);
   if (o.has_memory_cap && staging > o.memory_cap_bytes) {

@@ -49,8 +49,12 @@ cudaError_t launch_residual(const float* C, const float* G, const float* R, cons
                             int64_t b, int k, float lambda, double* partial, double* out,
                             cudaStream_t st);
 size_t residual_partial_count(int64_t b, int k);
-// per-pair sqrt(sum of the k per-system partials) (in-kernel check_stationarity)
-cudaError_t launch_residual_finish(const double* partial, int64_t b, int k, double* out, cudaStream_t st);
+// Lean residual tiles (co-run with a solver chunk): partial[q][residual_tile_count(k)]
+cudaError_t launch_residual_tiles(const float* C, const float* G, const float* R, const float* M, int64_t b,
+                                  int k, float lambda, double* partial, cudaStream_t st);
+int residual_tile_count(int k);
+// out[q] = sqrt(sum of pair q's `nper` partials), fixed order
+cudaError_t launch_residual_finish(const double* partial, int64_t b, int nper, double* out, cudaStream_t st);
 cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,
                                  unsigned long long* fail_min, unsigned long long sys,
                                  cudaStream_t st);

@@ -38,14 +38,12 @@ struct SolveParams {
   unsigned int* rcond_exact;     // count of systems that ran the exact rcond estimator
   float* tc_scratch;             // tensor-core solver: per-CTA L scratch (tc_scratch_bytes)
   const float* gram_rowsum;      // [b][k] sum_c |G[q][r][c]| (launch_gram_check): rcond certificate
-  double* res_partial;           // [b][k] per-system squared residual (in-kernel check_stationarity) or null
   long long* trace;              // debug phase trace (nullptr = off)
   int trace_block;
 };
 
 // Tensor-core (tcgen05 / TMEM) solver, fmap_tc.cu.
 bool tc_supported(int k, int optin_smem);
-bool tc_inkernel_residual(int k);
 int tc_max_resolution(int optin_smem);
 size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms);
 cudaError_t launch_project_tc(const float* phi, const float* mass, const float* F, int64_t b,

@@ -71,7 +71,6 @@ struct TcLayout {
   int ns;  // systems factored in lockstep per CTA (same row -> same thread)
   int tma; // next pair's G staged by TMA + tcgen05.cp during the current pair's panels
   int nmain, bwarp, mwarp, threads, aug_tid;
-  int rwarp;  // check_stationarity warp (one system behind the back substitution), -1 when absent
   int tcols1;     // TMEM columns of one system
   int tmem_cols;  // allocated (ns * tcols1, power of two)
   int Rop;  // operand buffer rows
@@ -79,7 +78,6 @@ struct TcLayout {
   // offsets in floats from the dynamic smem base
   int off_hi, off_lo, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_a0, off_stg, off_misc;
   int off_uv, off_wv, off_hv;  // rcond (back-substitution warp): comparison solves u, w; Hager vectors
-  int off_xr;                  // residual warp: x of the last two systems [2][K16] + valid flags
   int floats;
   long long lb;  // floats of one L scratch slot (global memory)
 };
@@ -121,8 +119,6 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.bwarp = L.nmain / 32;      // back-substitution warps bwarp .. bwarp+ns-1 (one per system)
   L.mwarp = L.bwarp + ns;      // MMA-issue warp
   L.threads = L.nmain + 32 * ns + 32;
-  L.rwarp = (ns == 1 && L.threads + 32 <= 384) ? L.mwarp + 1 : -1;
-  if (L.rwarp >= 0) L.threads += 32;
   L.Rop = L.K16 > kTL ? L.K16 : kTL;
   const int lbs = (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;
   int o = 0;
@@ -141,7 +137,6 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.off_a0 = o;  o += ns * L.K16 * 16;          // panel-0 columns of every row (float4 [h][t4][row])
   o = (o + 255) & ~255;                         // 1 KB aligned (TMA destination)
   L.off_stg = o; o += ns * L.G * 4 * kTL * 4;   // one G chunk of every (system, group): [h][g][u][128 rows][4]
-  L.off_xr = o;  o += 2 * L.K16 + 32;
   L.off_misc = o; o += 128;
   L.floats = o;
   L.lb = (lb_off(L.P, L.K16) + 31) & ~31ll;
@@ -315,10 +310,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
   uint64_t* cpd = chk + 1;
   uint64_t* a0f = chk + 2;
   uint64_t* stg = chk + 3;
-  uint64_t* rready = chk + 4;  // [2] back-substitution warp -> residual warp (x of a system landed)
-  uint64_t* rfree = chk + 6;   // [2] residual warp -> back-substitution warp (slot consumed)
-  float* xres = smem + Ly.off_xr;                                   // [2][K16]
-  int* xres_ok = reinterpret_cast<int*>(smem + Ly.off_xr + 2 * K16);  // [2]
   float4* a0s = reinterpret_cast<float4*>(smem + Ly.off_a0);  // panel-0 columns: [(h*4 + t4)*K16 + row]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 48);
   unsigned* scb = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 56);  // [n&1][h][8]
@@ -338,8 +329,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     scb[8 * tid + 4] = 0u;
   }
   if (tid == 0) {
-    const int nbar = 8 + 6 * NS + (Ly.rwarp >= 0 ? 4 : 0);  // + rready[2], rfree[2]
-    for (int e = 0; e < nbar; ++e) mbar_init(&mbar[e], e == 2 ? (uint32_t)(Ly.nmain / 32) : 1u);
+    for (int e = 0; e < 8 + 6 * NS; ++e) mbar_init(&mbar[e], e == 2 ? (uint32_t)(Ly.nmain / 32) : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, (uint32_t)Ly.tmem_cols);
@@ -673,71 +663,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
           atomicMin(p.rcond_min_bits, __float_as_uint(rc));
         }
       }
-      if (Ly.rwarp >= 0 && p.res_partial) {  // hand x to the check_stationarity warp
-        const int rs = n & 1;
-        if (n >= 2) mbar_wait(&rfree[rs], ((n - 2) >> 1) & 1);
-        const bool ok = ssc[3] == 0u && p.rhs_unit < 0;
-        if (ok)
-          for (int c = lane; c < K16; c += 32) xres[rs * K16 + c] = xv[c];
-        if (lane == 0) xres_ok[rs] = ok ? 1 : 0;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&rready[rs]);
-      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bsub[slot]);
-    }
-    return;
-  }
-
-  // ======================= check_stationarity warp =======================
-  // solver.hpp:116-128 per system, one behind the back substitution:
-  // e_r = sum_c x_c G[c][r] + lambda m_i(r) x_r - R[i][r] (row i of C G +
-  // lambda M.*C - R; fp32 products, lanes over r so the G reads coalesce),
-  // res_partial[q k + i] = sum_r e_r^2 in fp64; residual_finish sums each pair.
-  if (warp == Ly.rwarp) {
-    if (!p.res_partial) return;
-    int n = 0;
-    for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x, ++n) {
-      const int rs = n & 1;
-      mbar_wait(&rready[rs], (n >> 1) & 1);
-      if (xres_ok[rs]) {
-        int64_t q;
-        int i;
-        sys_of(p, pi, q, i);
-        const float* x = xres + rs * K16;
-        const float* Gq = p.gram + (size_t)q * k * k;
-        float evm = 0.f;
-        if constexpr (MASK_MODE == 1) {
-          for (int c = lane; c < k; c += 32)
-            evm = fmaxf(evm, fmaxf(p.ev1[(size_t)q * k + c], p.ev2[(size_t)q * k + c]));
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) evm = fmaxf(evm, __shfl_xor_sync(kFull, evm, o));
-        }
-        double acc = 0.0;
-        for (int r0 = 0; r0 < k; r0 += 32) {
-          const int r = r0 + lane;
-          if (r < k) {
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-            int c = 0;
-            for (; c + 4 <= k; c += 4) {
-              s0 = fmaf(x[c], __ldg(Gq + (size_t)c * k + r), s0);
-              s1 = fmaf(x[c + 1], __ldg(Gq + (size_t)(c + 1) * k + r), s1);
-              s2 = fmaf(x[c + 2], __ldg(Gq + (size_t)(c + 2) * k + r), s2);
-              s3 = fmaf(x[c + 3], __ldg(Gq + (size_t)(c + 3) * k + r), s3);
-            }
-            for (; c < k; ++c) s0 = fmaf(x[c], __ldg(Gq + (size_t)c * k + r), s0);
-            const float sg = (s0 + s1) + (s2 + s3);
-            const float m = mask_entry<MASK_MODE>(p, q, i, r, evm);
-            const float e = sg + p.lambda * (m * x[r]) - __ldg(p.rhs + ((size_t)q * k + i) * k + r);
-            acc += (double)e * (double)e;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-        if (lane == 0) p.res_partial[(size_t)q * k + i] = acc;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&rfree[rs]);
     }
     return;
   }
@@ -1438,9 +1365,6 @@ size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms) {
   return (size_t)grid * 2 * L.ns * (size_t)L.lb * sizeof(float);
 }
 
-// check_stationarity runs inside the solver (its own warp) for this k
-bool tc_inkernel_residual(int k) { return make_layout(k, tc_ns_override()).rwarp >= 0; }
-
 bool tc_supported(int k, int optin_smem) {
   if (k < 1) return false;
   const TcLayout L = make_layout(k, tc_ns_override());
@@ -1506,11 +1430,11 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
         default: fn = chol_tc_kernel<2, 2, 384, 1>; break;
       }
     }
-  } else if (L.cps >= 2 && L.threads <= 320) {  // two CTAs per SM
+  } else if (L.cps >= 2 && L.threads <= 288) {  // two CTAs per SM
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 1, 320, 2>; break;
-      case 1: fn = chol_tc_kernel<1, 1, 320, 2>; break;
-      default: fn = chol_tc_kernel<2, 1, 320, 2>; break;
+      case 0: fn = chol_tc_kernel<0, 1, 288, 2>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 288, 2>; break;
+      default: fn = chol_tc_kernel<2, 1, 288, 2>; break;
     }
   } else {
     switch (mask_mode) {
@@ -1677,9 +1601,9 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_tc_kernel(const float* __r
         const int c = st / kPjChunk;
         mbar_wait(chunkdone, c & 1);
         tc_fence_after();
-        const int quarter = warp & 3, half = warp >> 2, nh = N / 2;
+        const int quarter = warp & 3, half = warp >> 2, nh = ((N / 2) + 15) & ~15;  // 16-column chunks per half
         const uint32_t tl = tbase + ((uint32_t)(32 * quarter) << 16);
-        for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+        for (int c0 = half * nh; c0 < min(N, (half + 1) * nh); c0 += 16) {
           float v[16];
           tmem_ld16(tl + (uint32_t)c0, v);
           if (c > 0) {
@@ -1700,8 +1624,8 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_tc_kernel(const float* __r
     // exactly the quarter / column half it folded itself ----
     const int quarter = warp & 3, half = warp >> 2;
     const int i = i0 + 32 * quarter + lane;
-    const int nh = N / 2;
-    for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+    const int nh = ((N / 2) + 15) & ~15;
+    for (int c0 = half * nh; c0 < min(N, (half + 1) * nh); c0 += 16) {
       float v[16];
       tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + 256u + (uint32_t)c0, v);
       if (i < k) {
@@ -1732,23 +1656,26 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_tc_kernel(const float* __r
 // chunk-fold scheme as proj_tc_kernel.
 constexpr int kPjR = 4;
 
-__global__ void __launch_bounds__(kPjThreads, 1)
+__global__ void __launch_bounds__(kPjThreads, 2)
     proj_tma_kernel(const __grid_constant__ CUtensorMap tmPhi, const __grid_constant__ CUtensorMap tmF,
-                    const __grid_constant__ CUtensorMap tmMass, int64_t n, int k, int d, int N,
-                    float* __restrict__ out) {
+                    const __grid_constant__ CUtensorMap tmMass, int64_t n, int k, int d, int N, int R,
+                    uint32_t tcols, float* __restrict__ out) {
+  // N = this CTA's feature columns (blockIdx.z selects the slice: N-split for
+  // occupancy), R = raw-ring depth, tcols = TMEM columns (accumulator | sum at N)
   extern __shared__ __align__(1024) float smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q = blockIdx.y, i0 = blockIdx.x * 128;
+  const int q = blockIdx.y, i0 = blockIdx.x * 128, c_off = blockIdx.z * N;
+  const uint32_t sumoff = (uint32_t)N;
   const int abytes = 128 * kPjK, bbytes = N * kPjK;  // floats
   const int sstride = 2 * abytes + 2 * bbytes;
   const int rstride = (2048 + 16 * N + 16 + 31) & ~31;  // raw slot: Phi [16][128] | F [16][N] | Mass [16]
   float* raw = smem + 2 * sstride;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + kPjR * rstride);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + R * rstride);
   uint64_t* opfull = bar;          // [2] producers -> MMA
   uint64_t* opempty = bar + 2;     // [2] MMA -> producers
   uint64_t* chunkdone = bar + 5;
   uint64_t* folded = bar + 6;
-  uint64_t* rawfull = bar + 7;     // [kPjR] TMA -> producers
+  uint64_t* rawfull = bar + 7;     // [R] TMA -> producers
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 7 + kPjR);
   if (tid == 0) {
     mbar_init(&opfull[0], 8);
@@ -1757,10 +1684,10 @@ __global__ void __launch_bounds__(kPjThreads, 1)
     mbar_init(&opempty[1], 1);
     mbar_init(chunkdone, 1);
     mbar_init(folded, 8);
-    for (int r = 0; r < kPjR; ++r) mbar_init(&rawfull[r], 1);
+    for (int r = 0; r < R; ++r) mbar_init(&rawfull[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) tmem_alloc(tslot, 512);
+  if (warp == 0) tmem_alloc(tslot, tcols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1771,14 +1698,14 @@ __global__ void __launch_bounds__(kPjThreads, 1)
   if (warp == 8) {  // ---- TMA issue + MMA issue ----
     if (lane == 0) {
       auto issue_raw = [&](int s2) {
-        const int slot = s2 % kPjR;
+        const int slot = s2 % R;
         float* rs = raw + slot * rstride;
         mbar_expect_tx(&rawfull[slot], rawbytes);
         tma_load_3d(rs, &tmPhi, i0, s2 * kPjK, q, &rawfull[slot]);
-        tma_load_3d(rs + 2048, &tmF, 0, s2 * kPjK, q, &rawfull[slot]);
+        tma_load_3d(rs + 2048, &tmF, c_off, s2 * kPjK, q, &rawfull[slot]);
         tma_load_2d(rs + 2048 + 16 * N, &tmMass, s2 * kPjK, q, &rawfull[slot]);
       };
-      for (int s2 = 0; s2 < kPjR && s2 < nst; ++s2) issue_raw(s2);
+      for (int s2 = 0; s2 < R && s2 < nst; ++s2) issue_raw(s2);
       const uint32_t id = idesc_tf32(N) & ~(1u << 13);  // D += A*B (no negation)
       for (int st = 0; st < nst; ++st) {
         const int buf = st & 1;
@@ -1787,9 +1714,9 @@ __global__ void __launch_bounds__(kPjThreads, 1)
           mbar_wait(folded, ((st / kPjChunk) - 1) & 1);
           tc_fence_after();
         }
-        mbar_wait(&opfull[buf], (st >> 1) & 1);  // also: raw slot st % kPjR has been converted
+        mbar_wait(&opfull[buf], (st >> 1) & 1);  // also: raw slot st % R has been converted
         tc_fence_after();
-        if (st + kPjR < nst) issue_raw(st + kPjR);
+        if (st + R < nst) issue_raw(st + R);
         const uint32_t ah = su32(smem + buf * sstride), al = ah + abytes * 4;
         const uint32_t bh = al + abytes * 4, bl = bh + bbytes * 4;
 #pragma unroll
@@ -1806,8 +1733,8 @@ __global__ void __launch_bounds__(kPjThreads, 1)
   } else {  // ---- producers (256 threads): raw fp32 tiles -> hi/lo operands ----
     const int ia = tid & 127, vg = tid >> 7;  // A: basis function ia, vertices 8vg..8vg+7
     for (int st = 0; st < nst; ++st) {
-      const int buf = st & 1, slot = st % kPjR;
-      mbar_wait(&rawfull[slot], (st / kPjR) & 1);
+      const int buf = st & 1, slot = st % R;
+      mbar_wait(&rawfull[slot], (st / R) & 1);
       if (st >= 2) mbar_wait(&opempty[buf], ((st - 2) >> 1) & 1);  // MMAs of stage st-2 done
       const float* rp = raw + slot * rstride;
       const float* rf = rp + 2048;
@@ -1849,18 +1776,18 @@ __global__ void __launch_bounds__(kPjThreads, 1)
         const int c = st / kPjChunk;
         mbar_wait(chunkdone, c & 1);
         tc_fence_after();
-        const int quarter = warp & 3, half = warp >> 2, nh = N / 2;
+        const int quarter = warp & 3, half = warp >> 2, nh = ((N / 2) + 15) & ~15;  // 16-column chunks per half
         const uint32_t tl = tbase + ((uint32_t)(32 * quarter) << 16);
-        for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+        for (int c0 = half * nh; c0 < min(N, (half + 1) * nh); c0 += 16) {
           float v[16];
           tmem_ld16(tl + (uint32_t)c0, v);
           if (c > 0) {
             float sv[16];
-            tmem_ld16(tl + 256u + (uint32_t)c0, sv);
+            tmem_ld16(tl + sumoff + (uint32_t)c0, sv);
 #pragma unroll
             for (int t = 0; t < 16; ++t) v[t] += sv[t];
           }
-          tmem_st16(tl + 256u + (uint32_t)c0, v);
+          tmem_st16(tl + sumoff + (uint32_t)c0, v);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -1870,27 +1797,27 @@ __global__ void __launch_bounds__(kPjThreads, 1)
     }
     const int quarter = warp & 3, half = warp >> 2;
     const int i = i0 + 32 * quarter + lane;
-    const int nh = N / 2;
-    for (int c0 = half * nh; c0 < (half + 1) * nh; c0 += 16) {
+    const int nh = ((N / 2) + 15) & ~15;
+    for (int c0 = half * nh; c0 < min(N, (half + 1) * nh); c0 += 16) {
       float v[16];
-      tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + 256u + (uint32_t)c0, v);
+      tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + sumoff + (uint32_t)c0, v);
       if (i < k) {
-        float* o = out + ((size_t)q * k + i) * d + c0;
-        if (c0 + 16 <= d) {
+        float* o = out + ((size_t)q * k + i) * d + c_off + c0;
+        if (c_off + c0 + 16 <= d) {
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4)
             *reinterpret_cast<float4*>(o + 4 * c4) = make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
         } else {
 #pragma unroll
           for (int t = 0; t < 16; ++t)
-            if (c0 + t < d) o[t] = v[t];
+            if (c_off + c0 + t < d) o[t] = v[t];
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, 512);
+  if (warp == 0) tmem_dealloc(tbase, tcols);
 }
 }  // namespace
 
@@ -1918,19 +1845,33 @@ cudaError_t launch_project_tc(const float* phi, const float* mass, const float* 
     CUtensorMap tp, tf, tm;
     const cuuint64_t dp[3] = {(cuuint64_t)k, (cuuint64_t)n, (cuuint64_t)b};
     const cuuint32_t bp[3] = {128, (cuuint32_t)kPjK, 1};
+    // N-split: two CTAs per (pair, 128 basis functions) of N/2 feature columns
+    // each -- 256 columns of TMEM (accumulator + fp32 sum) and a 2-deep raw ring,
+    // so two CTAs share an SM and one's chunk fold hides behind the other's MMAs
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ctas = b * ((k + 127) / 128);
+    // opt-in (FMAP_PROJ_SPLIT=1): measured slower at cfg2 (0.363 vs 0.258 ms per
+    // direction: the 2-deep ring and the duplicated Phi conversion cost more than
+    // the second CTA per SM hides)
+    const int nsplit = (N > 128 && 2 * ctas <= 2LL * sms && std::getenv("FMAP_PROJ_SPLIT") != nullptr) ? 2 : 1;
+    const int Nc = nsplit == 2 ? ((N / 2 + 15) & ~15) : N;
+    const int R = nsplit == 2 ? 2 : kPjR;
+    const uint32_t tcols = 2 * Nc <= 256 ? 256u : 512u;
     const cuuint64_t df[3] = {(cuuint64_t)d, (cuuint64_t)n, (cuuint64_t)b};
-    const cuuint32_t bf[3] = {(cuuint32_t)N, (cuuint32_t)kPjK, 1};
+    const cuuint32_t bf[3] = {(cuuint32_t)Nc, (cuuint32_t)kPjK, 1};
     const cuuint64_t dm[2] = {(cuuint64_t)n, (cuuint64_t)b};
     const cuuint32_t bm[2] = {(cuuint32_t)kPjK, 1};
     if (encode_plain_map(&tp, phi, 3, dp, bp) == 0 && encode_plain_map(&tf, F, 3, df, bf) == 0 &&
         encode_plain_map(&tm, mass, 2, dm, bm) == 0) {
-      const int rstride = (2048 + 16 * N + 16 + 31) & ~31;
-      const size_t smem = (size_t)(2 * (2 * 128 * kPjK + 2 * N * kPjK) + kPjR * rstride) * 4 + 256;
+      const int rstride = (2048 + 16 * Nc + 16 + 31) & ~31;
+      const size_t smem = (size_t)(2 * (2 * 128 * kPjK + 2 * Nc * kPjK) + R * rstride) * 4 + 256;
       cudaError_t e = cudaFuncSetAttribute(proj_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      dim3 grid((unsigned)((k + 127) / 128), (unsigned)b);
+      dim3 grid((unsigned)((k + 127) / 128), (unsigned)b, (unsigned)nsplit);
       note_launch("proj_tma_kernel");
-      proj_tma_kernel<<<grid, kPjThreads, smem, st>>>(tp, tf, tm, n, k, d, N, out);
+      proj_tma_kernel<<<grid, kPjThreads, smem, st>>>(tp, tf, tm, n, k, d, Nc, R, tcols, out);
       return cudaGetLastError();
     }
   }

@@ -1,0 +1,33 @@
+"""e2e (host C ABI, pinned buffers) at cfg2-like shapes: residual on/off, chunk counts.
+    python tools/e2e_probe.py"""
+import ctypes as C
+import os
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+import paper_2604_10377_b200 as fm  # noqa: E402
+from paper_2604_10377_b200 import _lib, synth  # noqa: E402
+
+G, R, e1, e2 = synth.random_normal_equations(64, 200, 256, 7)
+M = fm.build_mask(fm.MaskKind.Resolvent, e1, e2, 0.5)
+hG, hR, hM = (torch.from_numpy(x).pin_memory() for x in (G, R, M))
+hC = torch.empty_like(hG).pin_memory()
+ctx = _lib.context(0)
+P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+for chunks in ("8", "4", "16"):
+    os.environ["FMAP_PIPELINE"] = chunks
+    for res in (False, True):
+        o = fm.SolverOptions(compute_residual=res).to_c()
+        rep = _lib.ReportC()
+        for _ in range(3):
+            ctx._lib.fmap_solve_f32(ctx.handle, 64, 200, P(hG), P(hR), P(hM), 100.0, C.byref(o), P(hC), C.byref(rep))
+        t0 = time.perf_counter()
+        for _ in range(10):
+            st = ctx._lib.fmap_solve_f32(ctx.handle, 64, 200, P(hG), P(hR), P(hM), 100.0, C.byref(o), P(hC),
+                                         C.byref(rep))
+        ms = (time.perf_counter() - t0) * 100
+        print(f"chunks={chunks} residual={res}: {ms:.3f} ms/step  st={st} launches={ctx.last_launches[:6]}...")
