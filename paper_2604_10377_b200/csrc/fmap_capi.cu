@@ -288,6 +288,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     const char* tb = std::getenv("FMAP_TRACE_BLOCK");
     p.trace_block = tb ? std::atoi(tb) : 0;
   }
+  if (const char* dbg = std::getenv("FMAP_DEBUG")) p.debug = std::atoi(dbg);  // timing experiments only
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   FMAP_CK(ctx, launch_chol_solve(p, mask_mode, ctx->stream));
   if (d_trace) {

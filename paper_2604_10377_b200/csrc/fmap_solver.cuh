@@ -40,6 +40,7 @@ struct SolveParams {
   const float* gram_rowsum;      // [b][k] sum_c |G[q][r][c]| (launch_gram_check): rcond certificate
   long long* trace;              // debug phase trace (nullptr = off)
   int trace_block;
+  int debug;                     // timing experiments only (FMAP_DEBUG): bit 0 = skip the back substitution
 };
 
 // Tensor-core (tcgen05 / TMEM) solver, fmap_tc.cu.

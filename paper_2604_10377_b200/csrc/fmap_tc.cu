@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
       const int slot = NS * (n & 1) + h;
       mbar_wait(&fact[slot], (n >> 1) & 1);
       unsigned* ssc = slotsc + 8 * slot;
-      if (ssc[3] == 0u) {
+      if (ssc[3] == 0u && !(p.debug & 1)) {
         int64_t q;
         int i;
         sys_of(p, NS * pi + h, q, i);
