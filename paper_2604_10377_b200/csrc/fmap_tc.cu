@@ -115,24 +115,23 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.tmem_cols = ns * c;
   const int ntop = L.hi[L.G - 1] - L.lo[L.G - 1];
   L.aug_tid = kTL * (L.G - 1) + ntop;
-  L.nmain = 32 * (4 * (L.G - 1) + (ntop + 1 + 31) / 32);
-  L.bwarp = L.nmain / 32;      // back-substitution warps bwarp .. bwarp+ns-1 (one per system)
-  L.mwarp = L.bwarp + ns;      // MMA-issue warp
-  L.threads = L.nmain + 32 * ns + 32;
+  L.nmain = 32 * (4 * (L.G - 1) + (ntop + 31) / 32);
+  L.bwarp = -1;                // back substitution: chol_backsub_kernel (own launch)
+  L.mwarp = L.nmain / 32;      // MMA-issue warp
+  L.threads = L.nmain + 32;
   L.Rop = L.K16 > kTL ? L.K16 : kTL;
-  const int lbs = (L.K16 - 16 > 0 ? L.K16 - 16 : 1) * 16;
   int o = 0;
   L.off_hi = o;  o += ns * L.Rop * 16;          // per system
   L.off_lo = o;  o += ns * L.Rop * 16;
   L.off_lt = o;  o += ns * (256 + 16);          // per system: diagonal block (transposed) + 1/L_tt
-  L.off_l11 = o; o += 2 * ns * L.P * 152;       // per slot: packed lower L_bb (+ 1/L_tt) of every block
-  L.off_yv = o;  o += 2 * ns * L.K16;           // per slot: y = L^{-1} r
-  L.off_xv = o;  o += ns * L.K16;               // back substitution: x (per system)
-  L.off_lb = o;  o += ns * 2 * lbs;             // back substitution: L blocks (per system, 2 buffers)
-  L.off_zb = o;  o += ns * 16;
-  L.off_uv = o;  o += ns * L.K16;               // back substitution: u = M(L)^{-1} e (per system)
-  L.off_wv = o;  o += ns * L.K16;               // back substitution: w = M(L)^{-T} e (per system)
-  L.off_hv = o;  o += ns * 3 * L.K16;           // back substitution: Hager estimator vectors (per system)
+  L.off_l11 = o;                                // (packed L_bb: per-system global store)
+  L.off_yv = o;                                 // (y = L^{-1} r: chol_backsub_kernel's forward pass)
+  L.off_xv = o;                                 // (back substitution: chol_backsub_kernel)
+  L.off_lb = o;
+  L.off_zb = o;
+  L.off_uv = o;
+  L.off_wv = o;
+  L.off_hv = o;
   o = (o + 31) & ~31;                           // 128 B aligned (TMA destination)
   L.off_a0 = o;  o += ns * L.K16 * 16;          // panel-0 columns of every row (float4 [h][t4][row])
   o = (o + 255) & ~255;                         // 1 KB aligned (TMA destination)
@@ -295,7 +294,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
   float* opnd_hi = smem + Ly.off_hi;  // system h: + h*opsz
   float* opnd_lo = smem + Ly.off_lo;
   float* LTb = smem + Ly.off_lt;  // system h: LT = LTb + 272h, LT[t][c] = L[c][t]; inv = LT + 256
-  float* zb = smem + Ly.off_zb;   // system h: + 16h
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + Ly.off_misc);
   // mbar[0] LA, [1] REST, [2] opsready (one arrival per main warp), [3] ysync,
   // [4 + s] fact (slot s), [4 + 2NS + s] bsub, [4 + 4NS + 2h + u] lfull (B warp h, buffer u),
@@ -316,7 +314,11 @@ __global__ void __launch_bounds__(MAXT, MINB)
   // sc[8h+0] dmax bits, [1] pivmin bits, [2] bad, [3] ev_max bits, [4] ||A||_1 bits (current
   // systems); double-buffered by iteration parity, reset right after the hand-off
   unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 88);  // [slot][8]
-  float* Lscr = p.tc_scratch + (size_t)blockIdx.x * 2 * NS * Ly.lb;
+  // per-system store for chol_backsub_kernel (launch-local system sl): L21 blocks,
+  // packed diagonal blocks (+ 1/L_tt), status words
+  float* Lst = p.tc_scratch;
+  float* L11st = Lst + (size_t)p.nsys * Ly.lb;
+  unsigned* stst = reinterpret_cast<unsigned*>(L11st + (size_t)p.nsys * P * 152);
   const int64_t npi = (p.nsys + NS - 1) / NS;
 
   // ---- one-time setup ----
@@ -337,337 +339,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-
-  // ======================= back-substitution warps =======================
-  // Per system (one behind the factorization): L^T x = y, the backward
-  // comparison solve M(L)^T w = e, the rcond verdict, the row of C.
-  //
-  // rcond (solver.hpp:164-168: Eigen's PartialPivLU::rcond(), a Hager/Higham
-  // estimate of 1 / (||A||_1 ||A^{-1}||_1)).  For A = L L^T, |L^{-1}| <= M(L)^{-1}
-  // entrywise (M = comparison matrix), so ||A^{-1}||_1 <= ||L^{-1}||_inf ||L^{-1}||_1
-  // <= max(u) max(w) with u = M(L)^{-1} e (forward, riding along the panels) and
-  // w = M(L)^{-T} e (here): cert = 1 / (||A||_1 max(u) max(w)) is a lower bound on
-  // the true rcond, and the reference's estimate never exceeds ||A^{-1}||_1, so
-  // cert >= 2 * threshold proves the reference would accept the system.  Otherwise
-  // (rare: near-singular systems) the exact Hager/Higham estimator runs here on the
-  // factor (forward + backward solves streaming the L scratch), the same algorithm
-  // the oracle restates (oracle/fmsolve_oracle.cpp inverse_l1_norm_estimate).
-  if (warp >= Ly.bwarp && warp < Ly.bwarp + NS) {
-    const int h = warp - Ly.bwarp;
-    float* xv = smem + Ly.off_xv + h * K16;
-    float* wv = smem + Ly.off_wv + h * K16;
-    float* hv = smem + Ly.off_hv + h * 3 * K16;  // Hager: working vector | sign | previous sign
-    const int lbs = (K16 - 16 > 0 ? K16 - 16 : 1) * 16;  // floats per L block buffer
-    float* lbuf = smem + Ly.off_lb + h * 2 * lbs;
-    uint64_t* lf = lfull + 2 * h;
-    uint32_t lb_use = 0;  // L-block counter (lfull phases: block use u -> buffer u&1)
-    int n = 0;
-    auto warp_sum = [&](float v) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-      return v;
-    };
-    auto warp_maxf = [&](float v) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
-      return v;
-    };
-    for (int64_t pi = blockIdx.x; pi < npi; pi += gridDim.x, ++n) {
-      const int slot = NS * (n & 1) + h;
-      mbar_wait(&fact[slot], (n >> 1) & 1);
-      unsigned* ssc = slotsc + 8 * slot;
-      if (ssc[3] == 0u && !(p.debug & 1)) {
-        int64_t q;
-        int i;
-        sys_of(p, NS * pi + h, q, i);
-        const int64_t sys = q * k + i;  // global system index (error convention)
-        const float* L11 = smem + Ly.off_l11 + slot * P * 152;
-        const float* yv = smem + Ly.off_yv + slot * K16;
-        float* uvs = smem + Ly.off_uv + h * K16;
-        const float* Lsl = Lscr + (size_t)slot * Ly.lb;
-        // blocks b = 0 .. P-2 carry L rows below them (block P-1 none)
-        auto issue_blk = [&](int b, uint32_t use) {
-          const uint32_t bytes = (uint32_t)(K16 - 16 * b - 16) * 64u;
-          if (lane == 0) {
-            mbar_expect_tx(&lf[use & 1], bytes);
-            bulk_g2s(lbuf + (use & 1) * lbs, Lsl + lb_off(b, K16), bytes, &lf[use & 1]);
-          }
-        };
-        // forward comparison solve M(L) u = e (rcond certificate), streaming blocks 0..P-2
-        for (int c = lane; c < K16; c += 32) uvs[c] = 1.f;
-        __syncwarp();
-        if (P >= 2) issue_blk(0, lb_use);
-        for (int b = 0; b < P; ++b) {
-          const float* Lbb = L11 + b * 152;
-          {  // u_b = M(L_bb)^{-1} acc_b by forward substitution, lane t (< 16) owns row t:
-             // u_s = acc_s / L_ss, then acc_t += |L[t][s]| u_s  (chain: SHFL -> FMUL -> FFMA)
-            const int t = lane & 15;
-            float a = uvs[16 * b + t], res = 0.f;
-#pragma unroll
-            for (int sv = 0; sv < 16; ++sv) {
-              const float us = __shfl_sync(kFull, a, sv) * Lbb[136 + sv];
-              if (t == sv) res = us;
-              if (t > sv) a = fmaf(fabsf(Lbb[t * (t + 1) / 2 + sv]), us, a);
-            }
-            __syncwarp();
-            if (lane < 16) uvs[16 * b + lane] = res;
-          }
-          __syncwarp();
-          const int R = K16 - 16 * b - 16;
-          if (R > 0) {
-            const uint32_t use = lb_use++;
-            mbar_wait(&lf[use & 1], (use >> 1) & 1);
-            if (b + 2 < P) issue_blk(b + 1, lb_use);  // prefetch (other buffer)
-            const float* blk = lbuf + (use & 1) * lbs;
-            float ub[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) ub[t] = uvs[16 * b + t];
-            for (int rho = lane; rho < R; rho += 32) {
-              float acc = uvs[16 * b + 16 + rho];
-#pragma unroll
-              for (int t4 = 0; t4 < 4; ++t4) {
-                const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * t4);
-                acc = fmaf(fabsf(l4.x), ub[4 * t4], acc);
-                acc = fmaf(fabsf(l4.y), ub[4 * t4 + 1], acc);
-                acc = fmaf(fabsf(l4.z), ub[4 * t4 + 2], acc);
-                acc = fmaf(fabsf(l4.w), ub[4 * t4 + 3], acc);
-              }
-              uvs[16 * b + 16 + rho] = acc;
-            }
-            __syncwarp();  // buffer and u rows consumed before the next refill
-          }
-        }
-        // backward pass: blocks b = P-2 .. 0; prefetch the first one
-        if (P >= 2) issue_blk(P - 2, lb_use);
-        for (int b = P - 1; b >= 0; --b) {
-          const float* Lbb = L11 + b * 152;
-          // s_t = sum_{c >= 16b+16} L[c][16b+t] x_c, sw_t = sum |L[c][16b+t]| w_c
-          // (lane: rows rho = lane>>2 + 8m, cols 4(lane&3)..)
-          float v4[4] = {0.f, 0.f, 0.f, 0.f}, w4[4] = {0.f, 0.f, 0.f, 0.f};
-          const int R = K16 - 16 * b - 16;
-          if (R > 0) {
-            const uint32_t use = lb_use++;
-            mbar_wait(&lf[use & 1], (use >> 1) & 1);
-            if (b >= 1) issue_blk(b - 1, lb_use);  // prefetch the next block (other buffer)
-            const float* blk = lbuf + (use & 1) * lbs;
-            for (int rho = lane >> 2; rho < R; rho += 8) {
-              const float xc = xv[16 * b + 16 + rho], wcv = wv[16 * b + 16 + rho];
-              const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
-              v4[0] = fmaf(l4.x, xc, v4[0]);
-              v4[1] = fmaf(l4.y, xc, v4[1]);
-              v4[2] = fmaf(l4.z, xc, v4[2]);
-              v4[3] = fmaf(l4.w, xc, v4[3]);
-              w4[0] = fmaf(fabsf(l4.x), wcv, w4[0]);
-              w4[1] = fmaf(fabsf(l4.y), wcv, w4[1]);
-              w4[2] = fmaf(fabsf(l4.z), wcv, w4[2]);
-              w4[3] = fmaf(fabsf(l4.w), wcv, w4[3]);
-            }
-#pragma unroll
-            for (int o = 4; o < 32; o <<= 1)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                v4[e] += __shfl_xor_sync(kFull, v4[e], o);
-                w4[e] += __shfl_xor_sync(kFull, w4[e], o);
-              }
-            __syncwarp();  // everyone done with this buffer before it is refilled
-          }
-          // lane t (< 16): z_t = y_t - s_t, then back substitution L_bb^T x_b = z_b by rows
-          // from the bottom (x_v = z_v / L_vv; z_t -= L[v][t] x_v), and the same with
-          // the comparison matrix for w (zw_t = 1 + sw_t; zw_t += |L[v][t]| w_v)
-          const int t = lane & 15;
-          float st = 0.f, swt = 0.f;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float other = __shfl_sync(kFull, v4[e], (t >> 2));  // lane (t>>2) holds cols 4(t>>2)..
-            const float otherw = __shfl_sync(kFull, w4[e], (t >> 2));
-            if ((t & 3) == e) {
-              st = other;
-              swt = otherw;
-            }
-          }
-          float z = yv[16 * b + t] - st, zw = 1.f + swt;
-          float x = 0.f, xw = 0.f;
-#pragma unroll
-          for (int v = 15; v >= 0; --v) {
-            const float iv = Lbb[136 + v];
-            const float xv_ = __shfl_sync(kFull, z, v) * iv, wv_ = __shfl_sync(kFull, zw, v) * iv;
-            if (t == v) {
-              x = xv_;
-              xw = wv_;
-            }
-            if (t < v) {
-              const float lt = Lbb[v * (v + 1) / 2 + t];
-              z = fmaf(-lt, xv_, z);
-              zw = fmaf(fabsf(lt), wv_, zw);
-            }
-          }
-          if (lane < 16) {
-            xv[16 * b + t] = x;
-            wv[16 * b + t] = xw;
-          }
-          __syncwarp();
-        }
-        // row of C, certificate
-        float* Crow = p.C + ((size_t)q * k + i) * k;
-        bool nf = false;
-        float umax = 0.f, wmax = 0.f;
-        for (int c = lane; c < k; c += 32) {
-          const float x = xv[c];
-          nf |= !(fabsf(x) <= FLT_MAX);
-          Crow[c] = x;
-          umax = fmaxf(umax, uvs[c]);
-          wmax = fmaxf(wmax, wv[c]);
-        }
-        nf = __any_sync(kFull, nf);
-        umax = warp_maxf(umax);
-        wmax = warp_maxf(wmax);
-        const float a1 = __uint_as_float(ssc[4]);
-        bool sing = ssc[2] != 0u || nf;
-        float rc = 0.f;
-        if (!sing) {
-          const float cert = 1.f / (a1 * umax * wmax);  // 0 when the bound overflows
-          if (!(a1 > 0.f)) {
-            rc = 0.f;                                   // rcond_estimate_helper: ||A||_1 == 0
-          } else if (k == 1) {
-            rc = 1.f;
-          } else if (cert >= 2.f * p.rcond_thr) {
-            rc = cert;
-          } else {
-            // ---- exact Hager / Higham estimate of ||A^{-1}||_1 (rare path) ----
-            float* v = hv;
-            float* csg = hv + K16;
-            float* osg = hv + 2 * K16;
-            // v <- A^{-1} v  (A = L L^T): forward L z = v, backward L^T v = z
-            auto solve_inplace = [&]() {
-              for (int b = 0; b < P; ++b) {
-                const float* Lbb = L11 + b * 152;
-                if (lane == 0) {
-                  for (int t = 0; t < 16; ++t) {
-                    float sacc = v[16 * b + t];
-                    for (int u = 0; u < t; ++u) sacc = fmaf(-Lbb[t * (t + 1) / 2 + u], v[16 * b + u], sacc);
-                    v[16 * b + t] = sacc * Lbb[136 + t];
-                  }
-                }
-                __syncwarp();
-                const int R = K16 - 16 * b - 16;
-                if (R > 0) {
-                  const uint32_t use = lb_use++;
-                  issue_blk(b, use);
-                  mbar_wait(&lf[use & 1], (use >> 1) & 1);
-                  const float* blk = lbuf + (use & 1) * lbs;
-                  for (int rho = lane; rho < R; rho += 32) {
-                    float acc = v[16 * b + 16 + rho];
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) acc = fmaf(-blk[rho * 16 + t], v[16 * b + t], acc);
-                    v[16 * b + 16 + rho] = acc;
-                  }
-                  __syncwarp();
-                }
-              }
-              for (int b = P - 1; b >= 0; --b) {
-                const float* Lbb = L11 + b * 152;
-                const int R = K16 - 16 * b - 16;
-                if (R > 0) {
-                  const uint32_t use = lb_use++;
-                  issue_blk(b, use);
-                  mbar_wait(&lf[use & 1], (use >> 1) & 1);
-                  const float* blk = lbuf + (use & 1) * lbs;
-                  if (lane < 16) {
-                    float sacc = 0.f;
-                    for (int rho = 0; rho < R; ++rho) sacc = fmaf(blk[rho * 16 + lane], v[16 * b + 16 + rho], sacc);
-                    wv[lane] = sacc;
-                  }
-                } else if (lane < 16) {
-                  wv[lane] = 0.f;
-                }
-                __syncwarp();
-                if (lane == 0) {
-                  for (int t = 15; t >= 0; --t) {
-                    float sacc = v[16 * b + t] - wv[t];
-                    for (int u = t + 1; u < 16; ++u) sacc = fmaf(-Lbb[u * (u + 1) / 2 + t], v[16 * b + u], sacc);
-                    v[16 * b + t] = sacc * Lbb[136 + t];
-                  }
-                }
-                __syncwarp();
-              }
-              for (int c = k + lane; c < K16; c += 32) v[c] = 0.f;  // identity padding stays out
-              __syncwarp();
-            };
-            auto l1v = [&]() {
-              float sacc = 0.f;
-              for (int c = lane; c < k; c += 32) sacc += fabsf(v[c]);
-              return warp_sum(sacc);
-            };
-            const float nk = (float)k;
-            for (int c = lane; c < K16; c += 32) v[c] = c < k ? 1.f / nk : 0.f;
-            __syncwarp();
-            solve_inplace();
-            float lower = l1v(), old_lower = lower;
-            int vmax = -1, old_vmax = -1;
-            for (int it = 0; it < 4; ++it) {
-              bool same = true;  // sign == old_sign
-              for (int c = lane; c < K16; c += 32) {
-                const float sg = c < k ? (v[c] < 0.f ? -1.f : 1.f) : 0.f;
-                same &= (sg == osg[c]);
-                csg[c] = sg;
-                v[c] = sg;  // next right-hand side: the sign vector
-              }
-              same = __all_sync(kFull, same);
-              if (it > 0 && same) break;
-              __syncwarp();
-              solve_inplace();  // A^T = A
-              float best = -1.f;
-              int bi = 0;
-              for (int c = lane; c < k; c += 32)
-                if (fabsf(v[c]) > best) {
-                  best = fabsf(v[c]);
-                  bi = c;
-                }
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) {  // first index of the max
-                const float ob = __shfl_xor_sync(kFull, best, o);
-                const int oi = __shfl_xor_sync(kFull, bi, o);
-                if (ob > best || (ob == best && oi < bi)) {
-                  best = ob;
-                  bi = oi;
-                }
-              }
-              vmax = bi;
-              if (vmax == old_vmax) break;
-              for (int c = lane; c < K16; c += 32) v[c] = (c == vmax) ? 1.f : 0.f;
-              __syncwarp();
-              solve_inplace();
-              lower = l1v();
-              if (lower <= old_lower) break;
-              for (int c = lane; c < K16; c += 32) osg[c] = csg[c];  // old_sign = sign
-              __syncwarp();
-              old_vmax = vmax;
-              old_lower = lower;
-            }
-            for (int c = lane; c < K16; c += 32) {
-              const float sgn = (c & 1) ? -1.f : 1.f;
-              v[c] = c < k ? sgn * (1.f + (float)c / (float)(k - 1)) : 0.f;
-            }
-            __syncwarp();
-            solve_inplace();
-            const float alt = (2.f * l1v()) / (3.f * nk);
-            if (lane == 0 && p.rcond_exact) atomicAdd(p.rcond_exact, 1u);
-            const float est = fmaxf(lower, alt);
-            rc = est == 0.f ? 0.f : (1.f / est) / a1;
-          }
-          if (!(rc >= p.rcond_thr)) sing = true;
-        }
-        if (lane == 0) {
-          if (!(rc >= 0.f)) rc = 0.f;
-          if (sing) atomicMin(p.fail_min, (unsigned long long)sys);
-          atomicMin(p.rcond_min_bits, __float_as_uint(rc));
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bsub[slot]);
-    }
-    return;
-  }
 
   // ======================= MMA-issue warp =======================
   // Per panel: wait until every main warp has stored its L21 operands, release the
@@ -745,7 +416,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
         for (int pp = 0; pp < P; ++pp, ++gm) {
           mbar_wait(opsready, gm & 1);
           TC_TRACE(pp < 16, 800 + pp);
-          mbar_arrive(ysync);
           tc_fence_after();
           const int r0 = 16 * pp + 16;
 #pragma unroll
@@ -826,7 +496,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
   const int row = glo + 32 * quarter + lane;
   const bool row_valid = has_grp && row < ghi;
-  const bool is_aug = tid == Ly.aug_tid;  // augmented right-hand-side "row"
   const uint32_t tq = tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)gbase - 16u;  // + column c
   const uint32_t tsys = (uint32_t)Ly.tcols1;  // TMEM column offset between systems
 
@@ -840,11 +509,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
   // stored at the top of panel pp+1; chunk 0 (registers), the last chunk and the
   // per-row right-hand side / mask entry are loaded at the end of the last panel.
   bool pre = false;        // the current pair's G chunks were prefetched
-  float rhs_n[NS], mraw_n[NS];
+  float mraw_n[NS];
   uint32_t n_stg = 0;
 #pragma unroll
   for (int h = 0; h < NS; ++h) {
-    rhs_n[h] = 0.f;
     mraw_n[h] = 0.f;
   }
 
@@ -872,13 +540,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
     const bool tr_on = blockIdx.x == (unsigned)p.trace_block && n == 1;
     TC_TRACE(tid == 0, 0);
-    const int slot0 = NS * (n & 1);
-
-    // slot reuse: the back-substitution of iteration n-2 must be done with it
-    if (n >= 2) {
-#pragma unroll
-      for (int h = 0; h < NS; ++h) mbar_wait(&bsub[slot0 + h], ((n - 2) >> 1) & 1);
-    }
+    const int slot0 = 0;  // smem y slot of system h: slot0 + h
     unsigned* sc = scb + 8 * NS * (n & 1);
     float ev_max[NS];
     bool skip[NS];
@@ -914,19 +576,15 @@ __global__ void __launch_bounds__(MAXT, MINB)
     // panels, or loaded here for the first pair), then lambda*m + ridge is added to
     // the diagonal entry in place.
     TC_TRACE(tid == 0, 398);
-    float rhs[NS], dmax[NS], dadd[NS];
+    float dmax[NS], dadd[NS];
 #pragma unroll
     for (int h = 0; h < NS; ++h) {
-      rhs[h] = 0.f;
       dmax[h] = 0.f;
       dadd[h] = 0.f;
       if (row_valid && row < k && !skip[h]) {
         if (MASK_MODE != 1 && pre) {
-          rhs[h] = rhs_n[h];
           dadd[h] = p.lambda * mraw_n[h] + p.ridge;
         } else {
-          rhs[h] = p.rhs_unit < 0 ? p.rhs[((size_t)qs[h] * k + is[h]) * k + row]
-                                  : (row == p.rhs_unit ? 1.f : 0.f);
           dadd[h] = p.lambda * mask_entry<MASK_MODE>(p, qs[h], is[h], row, ev_max[h]) + p.ridge;
         }
       }
@@ -1054,13 +712,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
 
     float pivmin[NS];
     unsigned bad[NS];
-    float lprev[NS][16];
 #pragma unroll
     for (int h = 0; h < NS; ++h) {
       pivmin[h] = FLT_MAX;
       bad[h] = 0u;
-#pragma unroll
-      for (int t = 0; t < 16; ++t) lprev[h][t] = 0.f;
     }
 
     // ---- panels ----
@@ -1068,23 +723,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
       const int j = 16 * pp;
       const bool active = row_valid && row >= j;
       // a. lagged rhs update, panel entries
-      if (pp > 0) {  // y of the previous panel (written by the rhs thread) is released by ysync
-        mbar_wait(ysync, (g - 1) & 1);
-        if (active) {
-#pragma unroll
-          for (int h = 0; h < NS; ++h) {
-            const float* yv = smem + Ly.off_yv + (slot0 + h) * K16;
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              const float4 y4 = *reinterpret_cast<const float4*>(yv + j - 16 + 4 * c4);
-              rhs[h] = fmaf(-lprev[h][4 * c4], y4.x, rhs[h]);
-              rhs[h] = fmaf(-lprev[h][4 * c4 + 1], y4.y, rhs[h]);
-              rhs[h] = fmaf(-lprev[h][4 * c4 + 2], y4.z, rhs[h]);
-              rhs[h] = fmaf(-lprev[h][4 * c4 + 3], y4.w, rhs[h]);
-            }
-          }
-        }
-      }
       float a[NS][16];
       auto load_a0 = [&](int h, float (&v)[16]) {
         if (row_valid) {
@@ -1118,7 +756,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
       TC_TRACE(tid == 0, 2 + 4 * pp);
       // b. diagonal blocks (rows j..j+15 live in one half of one warp; the other
       //    half factors system 1's block)
-      const bool in_diag = active && row < j + 16;
       int dwarp = 0;
 #pragma unroll
       for (int gg = 0; gg < kMaxGroups; ++gg)
@@ -1145,16 +782,22 @@ __global__ void __launch_bounds__(MAXT, MINB)
               bad[h] |= bd;
             }
           if (real) {
-            float* L11s = smem + Ly.off_l11 + (slot0 + hs) * P * 152 + pp * 152;
             float* LT = LTb + 272 * hs;
-            float* Lpk = L11s + gr * (gr + 1) / 2;  // packed copy for the back-sub warp
-            L11s[136 + gr] = iv;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              LT[t * 16 + gr] = (t <= gr) ? w[t] : 0.f;  // transposed, for the TRSM
-              if (t <= gr) Lpk[t] = w[t];
-            }
+            for (int t = 0; t < 16; ++t) LT[t * 16 + gr] = (t <= gr) ? w[t] : 0.f;  // transposed, for the TRSM
             LT[256 + gr] = iv;
+            bool vh = false;
+#pragma unroll
+            for (int h = 0; h < NS; ++h)
+              if (h == hs) vh = vld[h];
+            if (vh) {  // packed copy for chol_backsub_kernel
+              float* L11s = L11st + (size_t)(NS * pi + hs) * P * 152 + pp * 152;
+              float* Lpk = L11s + gr * (gr + 1) / 2;
+              L11s[136 + gr] = iv;
+#pragma unroll
+              for (int t = 0; t < 16; ++t)
+                if (t <= gr) Lpk[t] = w[t];
+            }
           }
         };
         if constexpr (NS == 1) {
@@ -1175,10 +818,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
           }
           diag_emit(w, true);
         }
-        if (in_diag) {
-#pragma unroll
-          for (int h = 0; h < NS; ++h) zb[16 * h + gr] = rhs[h];
-        }
         TC_TRACE(row == j, 3 + 4 * pp);
       }
       main_sync(NM);
@@ -1190,23 +829,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
         p.trace[1400 + 8 * pp + warp] = clock64();
       }
 #endif
-      // c. TRSM rows >= j+16 ; augmented row -> y for this panel
+      // c. TRSM rows >= j+16
       float l[NS][16];
       const bool trsm = active && row >= j + 16;
       if (trsm) {
 #pragma unroll
         for (int h = 0; h < NS; ++h) trsm_row(LTb + 272 * h, LTb + 272 * h + 256, a[h], l[h]);
-      } else if (is_aug) {
-#pragma unroll
-        for (int h = 0; h < NS; ++h) {
-          float z[16];
-#pragma unroll
-          for (int t = 0; t < 16; ++t) z[t] = zb[16 * h + t];
-          trsm_row(LTb + 272 * h, LTb + 272 * h + 256, z, l[h]);
-          float* yv = smem + Ly.off_yv + (slot0 + h) * K16;
-#pragma unroll
-          for (int t = 0; t < 16; ++t) yv[j + t] = l[h][t];
-        }
       }
       TC_TRACE(tid == 0 && pp < 16, 1120 + pp);
       TC_TRACE(lane == 0 && pp < 12 && warp < 8, 1200 + 8 * pp + warp);
@@ -1214,7 +842,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (trsm) {
 #pragma unroll
         for (int h = 0; h < NS; ++h) {
-          float4* dst = reinterpret_cast<float4*>(Lscr + (size_t)(slot0 + h) * Ly.lb + lb_off(pp, K16) +
+          if (!vld[h]) continue;
+          float4* dst = reinterpret_cast<float4*>(Lst + (size_t)(NS * pi + h) * Ly.lb + lb_off(pp, K16) +
                                                   (size_t)(row - j - 16) * 16);
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4)
@@ -1245,17 +874,11 @@ __global__ void __launch_bounds__(MAXT, MINB)
         mbar_arrive(opsready);  // operands of this panel stored
       }
       any_mma = true;
-#pragma unroll
-      for (int h = 0; h < NS; ++h)
-#pragma unroll
-        for (int t = 0; t < 16; ++t) lprev[h][t] = trsm ? l[h][t] : 0.f;
       if (has_next) {
         if (pp == P - 1) {
 #pragma unroll
           for (int h = 0; h < NS; ++h) {
             if (MASK_MODE != 1 && ldn[h]) {
-              rhs_n[h] = p.rhs_unit < 0 ? p.rhs[((size_t)qn[h] * k + in_[h]) * k + row]
-                                        : (row == p.rhs_unit ? 1.f : 0.f);
               mraw_n[h] = mask_entry<MASK_MODE>(p, qn[h], in_[h], row, 0.f);
             }
           }
@@ -1265,8 +888,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     pre = Ly.tma && has_next;
     TC_TRACE(tid == 0, 200);
 
-    // ---- hand the systems to the back-substitution warps ----
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // L scratch -> bulk-copy reads
+    // ---- status words of the systems for chol_backsub_kernel ----
 #pragma unroll
     for (int h = 0; h < NS; ++h) {
       unsigned b = bad[h];
@@ -1291,19 +913,20 @@ __global__ void __launch_bounds__(MAXT, MINB)
           sk = skip[hh];
           vv = vld[hh];
         }
-      unsigned* ssc = slotsc + 8 * (slot0 + h);
-      ssc[0] = sc[8 * h + 0];
-      ssc[1] = sc[8 * h + 1];
-      ssc[2] = sc[8 * h + 2];
-      ssc[3] = sk ? 1u : 0u;
-      ssc[4] = sc[8 * h + 4];
+      if (vv) {
+        unsigned* ssc = stst + (size_t)(NS * pi + h) * 8;
+        ssc[0] = sc[8 * h + 0];
+        ssc[1] = sc[8 * h + 1];
+        ssc[2] = sc[8 * h + 2];
+        ssc[3] = sk ? 1u : 0u;
+        ssc[4] = sc[8 * h + 4];
+      }
       sc[8 * h + 0] = 0u;
       sc[8 * h + 1] = __float_as_uint(FLT_MAX);
       sc[8 * h + 2] = 0u;
       sc[8 * h + 3] = 0u;
       sc[8 * h + 4] = 0u;
       if (sk && vv) atomicOr(p.flags, 32u);
-      mbar_arrive(&fact[slot0 + h]);
     }
     TC_TRACE(tid == 0, 203);
   }
@@ -1314,6 +937,348 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
   main_sync(NM);
   if (warp == 0) tmem_dealloc(tbase, (uint32_t)Ly.tmem_cols);
+}
+
+// ---------------------------------------------------------------------------
+// Back substitution + singular verdict, one warp per system, after the
+// factorization kernel (chol_tc_kernel stores every system's L21 blocks, packed
+// diagonal blocks, y = L^{-1} r and its status; this kernel reads them from L2 /
+// HBM).  Running it as its own pass instead of inside the factorization kernel
+// keeps its ~8.5 K instructions per system off the SMs while the latency-bound
+// panel chains run (the factorization alone is 1.66 vs 2.26 ms at cfg2 with the
+// in-kernel back-substitution warp).
+// ---------------------------------------------------------------------------
+constexpr int kBsWarps = 4;
+
+__global__ void __launch_bounds__(32 * kBsWarps, 8) chol_backsub_kernel(SolveParams p, TcLayout Ly) {
+  extern __shared__ __align__(1024) float smem[];
+  const int k = p.k, K16 = Ly.K16, P = Ly.P;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t sl = (int64_t)blockIdx.x * kBsWarps + warp;
+  if (sl >= p.nsys) return;
+  const float* Lst = p.tc_scratch;
+  const float* L11st = Lst + (size_t)p.nsys * Ly.lb;
+  const unsigned* stst = reinterpret_cast<const unsigned*>(L11st + (size_t)p.nsys * P * 152);
+  // Per system: L^T x = y, the backward
+  // comparison solve M(L)^T w = e, the rcond verdict, the row of C.
+  //
+  // rcond (solver.hpp:164-168: Eigen's PartialPivLU::rcond(), a Hager/Higham
+  // estimate of 1 / (||A||_1 ||A^{-1}||_1)).  For A = L L^T, |L^{-1}| <= M(L)^{-1}
+  // entrywise (M = comparison matrix), so ||A^{-1}||_1 <= ||L^{-1}||_inf ||L^{-1}||_1
+  // <= max(u) max(w) with u = M(L)^{-1} e (forward pass) and w = M(L)^{-T} e
+  // (with the back substitution): cert = 1 / (||A||_1 max(u) max(w)) is a lower bound on
+  // the true rcond, and the reference's estimate never exceeds ||A^{-1}||_1, so
+  // cert >= 2 * threshold proves the reference would accept the system.  Otherwise
+  // (rare: near-singular systems) the exact Hager/Higham estimator runs here on the
+  // factor (forward + backward solves over the stored L), the same algorithm
+  // the oracle restates (oracle/fmsolve_oracle.cpp inverse_l1_norm_estimate).
+  {
+    float* xv = smem + warp * 7 * K16;
+    float* wv = xv + K16;
+    float* uvs = wv + K16;
+    float* yv = uvs + K16;  // y = L^{-1} r (forward pass)
+    float* hv = yv + K16;   // Hager: working vector | sign | previous sign
+    auto warp_sum = [&](float v) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      return v;
+    };
+    auto warp_maxf = [&](float v) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+      return v;
+    };
+    {
+      const unsigned* ssc = stst + (size_t)sl * 8;
+      if (ssc[3] == 0u && !(p.debug & 1)) {
+        int64_t q;
+        int i;
+        sys_of(p, sl, q, i);
+        const int64_t sys = q * k + i;  // global system index (error convention)
+        const float* L11 = L11st + (size_t)sl * P * 152;
+        const float* Lsl = Lst + (size_t)sl * Ly.lb;
+        // forward pass, blocks 0..P-2: y = L^{-1} r (the right-hand side, row i of R)
+        // and the comparison solve M(L) u = e of the rcond certificate
+        for (int c = lane; c < K16; c += 32) {
+          uvs[c] = 1.f;
+          yv[c] = c < k ? (p.rhs_unit < 0 ? __ldg(p.rhs + ((size_t)q * k + i) * k + c) : (c == p.rhs_unit ? 1.f : 0.f))
+                        : 0.f;
+        }
+        __syncwarp();
+        for (int b = 0; b < P; ++b) {
+          const float* Lbb = L11 + b * 152;
+          {  // y_b = L_bb^{-1} acc_b and u_b = M(L_bb)^{-1} acc_b by forward substitution, lane
+             // t (< 16) owns row t: v_s = acc_s / L_ss, then acc_t -= L[t][s] v_s (+= |.| for u)
+            const int t = lane & 15;
+            float a = uvs[16 * b + t], ay = yv[16 * b + t], res = 0.f, resy = 0.f;
+#pragma unroll
+            for (int sv = 0; sv < 16; ++sv) {
+              const float iv = Lbb[136 + sv];
+              const float us = __shfl_sync(kFull, a, sv) * iv, ys = __shfl_sync(kFull, ay, sv) * iv;
+              if (t == sv) {
+                res = us;
+                resy = ys;
+              }
+              if (t > sv) {
+                const float lt = Lbb[t * (t + 1) / 2 + sv];
+                a = fmaf(fabsf(lt), us, a);
+                ay = fmaf(-lt, ys, ay);
+              }
+            }
+            __syncwarp();
+            if (lane < 16) {
+              uvs[16 * b + lane] = res;
+              yv[16 * b + lane] = resy;
+            }
+          }
+          __syncwarp();
+          const int R = K16 - 16 * b - 16;
+          if (R > 0) {
+            const float* blk = Lsl + lb_off(b, K16);  // rows 16b+16.. of block b (L2 / HBM)
+            float ub[16], yb[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              ub[t] = uvs[16 * b + t];
+              yb[t] = yv[16 * b + t];
+            }
+            for (int rho = lane; rho < R; rho += 32) {
+              float acc = uvs[16 * b + 16 + rho], accy = yv[16 * b + 16 + rho];
+#pragma unroll
+              for (int t4 = 0; t4 < 4; ++t4) {
+                const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * t4);
+                acc = fmaf(fabsf(l4.x), ub[4 * t4], acc);
+                acc = fmaf(fabsf(l4.y), ub[4 * t4 + 1], acc);
+                acc = fmaf(fabsf(l4.z), ub[4 * t4 + 2], acc);
+                acc = fmaf(fabsf(l4.w), ub[4 * t4 + 3], acc);
+                accy = fmaf(-l4.x, yb[4 * t4], accy);
+                accy = fmaf(-l4.y, yb[4 * t4 + 1], accy);
+                accy = fmaf(-l4.z, yb[4 * t4 + 2], accy);
+                accy = fmaf(-l4.w, yb[4 * t4 + 3], accy);
+              }
+              uvs[16 * b + 16 + rho] = acc;
+              yv[16 * b + 16 + rho] = accy;
+            }
+            __syncwarp();
+          }
+        }
+        // backward pass: blocks b = P-1 .. 0 (the first ones it reads are the forward pass's last: L2)
+        for (int b = P - 1; b >= 0; --b) {
+          const float* Lbb = L11 + b * 152;
+          // s_t = sum_{c >= 16b+16} L[c][16b+t] x_c, sw_t = sum |L[c][16b+t]| w_c
+          // (lane: rows rho = lane>>2 + 8m, cols 4(lane&3)..)
+          float v4[4] = {0.f, 0.f, 0.f, 0.f}, w4[4] = {0.f, 0.f, 0.f, 0.f};
+          const int R = K16 - 16 * b - 16;
+          if (R > 0) {
+            const float* blk = Lsl + lb_off(b, K16);
+            for (int rho = lane >> 2; rho < R; rho += 8) {
+              const float xc = xv[16 * b + 16 + rho], wcv = wv[16 * b + 16 + rho];
+              const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
+              v4[0] = fmaf(l4.x, xc, v4[0]);
+              v4[1] = fmaf(l4.y, xc, v4[1]);
+              v4[2] = fmaf(l4.z, xc, v4[2]);
+              v4[3] = fmaf(l4.w, xc, v4[3]);
+              w4[0] = fmaf(fabsf(l4.x), wcv, w4[0]);
+              w4[1] = fmaf(fabsf(l4.y), wcv, w4[1]);
+              w4[2] = fmaf(fabsf(l4.z), wcv, w4[2]);
+              w4[3] = fmaf(fabsf(l4.w), wcv, w4[3]);
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                v4[e] += __shfl_xor_sync(kFull, v4[e], o);
+                w4[e] += __shfl_xor_sync(kFull, w4[e], o);
+              }
+          }
+          // lane t (< 16): z_t = y_t - s_t, then back substitution L_bb^T x_b = z_b by rows
+          // from the bottom (x_v = z_v / L_vv; z_t -= L[v][t] x_v), and the same with
+          // the comparison matrix for w (zw_t = 1 + sw_t; zw_t += |L[v][t]| w_v)
+          const int t = lane & 15;
+          float st = 0.f, swt = 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float other = __shfl_sync(kFull, v4[e], (t >> 2));  // lane (t>>2) holds cols 4(t>>2)..
+            const float otherw = __shfl_sync(kFull, w4[e], (t >> 2));
+            if ((t & 3) == e) {
+              st = other;
+              swt = otherw;
+            }
+          }
+          float z = yv[16 * b + t] - st, zw = 1.f + swt;
+          float x = 0.f, xw = 0.f;
+#pragma unroll
+          for (int v = 15; v >= 0; --v) {
+            const float iv = Lbb[136 + v];
+            const float xv_ = __shfl_sync(kFull, z, v) * iv, wv_ = __shfl_sync(kFull, zw, v) * iv;
+            if (t == v) {
+              x = xv_;
+              xw = wv_;
+            }
+            if (t < v) {
+              const float lt = Lbb[v * (v + 1) / 2 + t];
+              z = fmaf(-lt, xv_, z);
+              zw = fmaf(fabsf(lt), wv_, zw);
+            }
+          }
+          if (lane < 16) {
+            xv[16 * b + t] = x;
+            wv[16 * b + t] = xw;
+          }
+          __syncwarp();
+        }
+        // row of C, certificate
+        float* Crow = p.C + ((size_t)q * k + i) * k;
+        bool nf = false;
+        float umax = 0.f, wmax = 0.f;
+        for (int c = lane; c < k; c += 32) {
+          const float x = xv[c];
+          nf |= !(fabsf(x) <= FLT_MAX);
+          Crow[c] = x;
+          umax = fmaxf(umax, uvs[c]);
+          wmax = fmaxf(wmax, wv[c]);
+        }
+        nf = __any_sync(kFull, nf);
+        umax = warp_maxf(umax);
+        wmax = warp_maxf(wmax);
+        const float a1 = __uint_as_float(ssc[4]);
+        bool sing = ssc[2] != 0u || nf;
+        float rc = 0.f;
+        if (!sing) {
+          const float cert = 1.f / (a1 * umax * wmax);  // 0 when the bound overflows
+          if (!(a1 > 0.f)) {
+            rc = 0.f;                                   // rcond_estimate_helper: ||A||_1 == 0
+          } else if (k == 1) {
+            rc = 1.f;
+          } else if (cert >= 2.f * p.rcond_thr) {
+            rc = cert;
+          } else {
+            // ---- exact Hager / Higham estimate of ||A^{-1}||_1 (rare path) ----
+            float* v = hv;
+            float* csg = hv + K16;
+            float* osg = hv + 2 * K16;
+            // v <- A^{-1} v  (A = L L^T): forward L z = v, backward L^T v = z
+            auto solve_inplace = [&]() {
+              for (int b = 0; b < P; ++b) {
+                const float* Lbb = L11 + b * 152;
+                if (lane == 0) {
+                  for (int t = 0; t < 16; ++t) {
+                    float sacc = v[16 * b + t];
+                    for (int u = 0; u < t; ++u) sacc = fmaf(-Lbb[t * (t + 1) / 2 + u], v[16 * b + u], sacc);
+                    v[16 * b + t] = sacc * Lbb[136 + t];
+                  }
+                }
+                __syncwarp();
+                const int R = K16 - 16 * b - 16;
+                if (R > 0) {
+                  const float* blk = Lsl + lb_off(b, K16);
+                  for (int rho = lane; rho < R; rho += 32) {
+                    float acc = v[16 * b + 16 + rho];
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) acc = fmaf(-blk[rho * 16 + t], v[16 * b + t], acc);
+                    v[16 * b + 16 + rho] = acc;
+                  }
+                  __syncwarp();
+                }
+              }
+              for (int b = P - 1; b >= 0; --b) {
+                const float* Lbb = L11 + b * 152;
+                const int R = K16 - 16 * b - 16;
+                if (R > 0) {
+                  const float* blk = Lsl + lb_off(b, K16);
+                  if (lane < 16) {
+                    float sacc = 0.f;
+                    for (int rho = 0; rho < R; ++rho) sacc = fmaf(blk[rho * 16 + lane], v[16 * b + 16 + rho], sacc);
+                    wv[lane] = sacc;
+                  }
+                } else if (lane < 16) {
+                  wv[lane] = 0.f;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                  for (int t = 15; t >= 0; --t) {
+                    float sacc = v[16 * b + t] - wv[t];
+                    for (int u = t + 1; u < 16; ++u) sacc = fmaf(-Lbb[u * (u + 1) / 2 + t], v[16 * b + u], sacc);
+                    v[16 * b + t] = sacc * Lbb[136 + t];
+                  }
+                }
+                __syncwarp();
+              }
+              for (int c = k + lane; c < K16; c += 32) v[c] = 0.f;  // identity padding stays out
+              __syncwarp();
+            };
+            auto l1v = [&]() {
+              float sacc = 0.f;
+              for (int c = lane; c < k; c += 32) sacc += fabsf(v[c]);
+              return warp_sum(sacc);
+            };
+            const float nk = (float)k;
+            for (int c = lane; c < K16; c += 32) v[c] = c < k ? 1.f / nk : 0.f;
+            __syncwarp();
+            solve_inplace();
+            float lower = l1v(), old_lower = lower;
+            int vmax = -1, old_vmax = -1;
+            for (int it = 0; it < 4; ++it) {
+              bool same = true;  // sign == old_sign
+              for (int c = lane; c < K16; c += 32) {
+                const float sg = c < k ? (v[c] < 0.f ? -1.f : 1.f) : 0.f;
+                same &= (sg == osg[c]);
+                csg[c] = sg;
+                v[c] = sg;  // next right-hand side: the sign vector
+              }
+              same = __all_sync(kFull, same);
+              if (it > 0 && same) break;
+              __syncwarp();
+              solve_inplace();  // A^T = A
+              float best = -1.f;
+              int bi = 0;
+              for (int c = lane; c < k; c += 32)
+                if (fabsf(v[c]) > best) {
+                  best = fabsf(v[c]);
+                  bi = c;
+                }
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {  // first index of the max
+                const float ob = __shfl_xor_sync(kFull, best, o);
+                const int oi = __shfl_xor_sync(kFull, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                  best = ob;
+                  bi = oi;
+                }
+              }
+              vmax = bi;
+              if (vmax == old_vmax) break;
+              for (int c = lane; c < K16; c += 32) v[c] = (c == vmax) ? 1.f : 0.f;
+              __syncwarp();
+              solve_inplace();
+              lower = l1v();
+              if (lower <= old_lower) break;
+              for (int c = lane; c < K16; c += 32) osg[c] = csg[c];  // old_sign = sign
+              __syncwarp();
+              old_vmax = vmax;
+              old_lower = lower;
+            }
+            for (int c = lane; c < K16; c += 32) {
+              const float sgn = (c & 1) ? -1.f : 1.f;
+              v[c] = c < k ? sgn * (1.f + (float)c / (float)(k - 1)) : 0.f;
+            }
+            __syncwarp();
+            solve_inplace();
+            const float alt = (2.f * l1v()) / (3.f * nk);
+            if (lane == 0 && p.rcond_exact) atomicAdd(p.rcond_exact, 1u);
+            const float est = fmaxf(lower, alt);
+            rc = est == 0.f ? 0.f : (1.f / est) / a1;
+          }
+          if (!(rc >= p.rcond_thr)) sing = true;
+        }
+        if (lane == 0) {
+          if (!(rc >= 0.f)) rc = 0.f;
+          if (sing) atomicMin(p.fail_min, (unsigned long long)sys);
+          atomicMin(p.rcond_min_bits, __float_as_uint(rc));
+        }
+      }
+    }
+  }
+
 }
 
 }  // namespace
@@ -1357,12 +1322,12 @@ static int tc_ns_override() {
   return s ? std::atoi(s) : 0;
 }
 
+// Per-system store of the factorization for chol_backsub_kernel: L21 blocks,
+// packed diagonal blocks, status (72 KB per system at k = 200, 0.94 GB for cfg2)
 size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms) {
+  (void)num_sms;
   const TcLayout L = make_layout(k, tc_ns_override());
-  const int64_t npi = (nsys + L.ns - 1) / L.ns;
-  const int64_t maxgrid = (int64_t)num_sms * L.cps;
-  const int64_t grid = npi < maxgrid ? npi : maxgrid;
-  return (size_t)grid * 2 * L.ns * (size_t)L.lb * sizeof(float);
+  return (size_t)nsys * ((size_t)L.lb + (size_t)L.P * 152 + 8) * sizeof(float);
 }
 
 bool tc_supported(int k, int optin_smem) {
@@ -1450,6 +1415,14 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   const unsigned grid = (unsigned)(npi < maxgrid ? npi : maxgrid);
   note_launch("chol_tc_kernel");
   fn<<<grid, L.threads, smem, stream>>>(p, L, tmG, tmA);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // back substitution + verdict over the stored factors, one warp per system
+  const size_t bsmem = (size_t)kBsWarps * 7 * L.K16 * sizeof(float);
+  e = cudaFuncSetAttribute(chol_backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+  if (e != cudaSuccess) return e;
+  note_launch("chol_backsub_kernel");
+  chol_backsub_kernel<<<(unsigned)((p.nsys + kBsWarps - 1) / kBsWarps), 32 * kBsWarps, bsmem, stream>>>(p, L);
   return cudaGetLastError();
 }
 
