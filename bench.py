@@ -258,7 +258,7 @@ def run_ours(args):
             "bound": "tensor",
             "achieved": round(achieved, 3), "peak": round(peak_max, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak_max, 4), "traffic": traffic,
-            "kernel": "chol_tc_kernel", "kernel_ms": round(kavg, 4),
+            "kernel": "chol_tc_kernel + chol_backsub_kernel (the solve: factorization, then y / back substitution / rcond verdict; kernel_ms = the solve's device time incl. validation)", "kernel_ms": round(kavg, 4),
             "flops_per_launch": flops,
             "peak_note": ("achieved counts the north_star's k^4/3 + k^3 flops per fmap; peak = FP32 "
                           "SIMT (north_star's denominator) derived as SMs x 128 lanes x 2 x 1965 MHz "
@@ -309,7 +309,7 @@ def run_ours(args):
                          "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes,
                          "ms_per_step": round(e2e_ms, 4),
                          "api": "fmap_solve_f32 with DEFAULT options (compute_residual=1, as the reference always "
-                                "reports max_residual_norm): host G,R,M pinned -> C, 8 pair chunks, H2D / "
+                                "reports max_residual_norm): host G,R,M pinned -> C, 4 pair chunks, H2D / "
                                 "validation+solve+residual / D2H overlapped on 2 copy + 2 compute streams"
                                 + ("; per rank on its pair range, max over ranks (no host-side gather)"
                                    if world > 1 else "")}

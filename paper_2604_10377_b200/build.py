@@ -34,10 +34,15 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "fmap_cuda.h"]
-    if not force and not _stale(LIB, deps):
-        return LIB
     objdir = PKG / "_build"
     objdir.mkdir(exist_ok=True)
+    stamp = objdir / "flags.txt"  # a change of FMAP_NVCC_FLAGS rebuilds every object
+    flags = os.environ.get("FMAP_NVCC_FLAGS", "")
+    if not stamp.exists() or stamp.read_text() != flags:
+        force = True
+        stamp.write_text(flags)
+    if not force and not _stale(LIB, deps):
+        return LIB
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", str(ROOT / "include"), "-Xptxas", "-v",
               *os.environ.get("FMAP_NVCC_FLAGS", "").split()]  # e.g. -DFMAP_TC_TRACE (phase stamps)

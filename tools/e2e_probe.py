@@ -18,7 +18,7 @@ hG, hR, hM = (torch.from_numpy(x).pin_memory() for x in (G, R, M))
 hC = torch.empty_like(hG).pin_memory()
 ctx = _lib.context(0)
 P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
-for chunks in ("8", "4", "16"):
+for chunks in ("4", "2", "8"):
     os.environ["FMAP_PIPELINE"] = chunks
     for res in (False, True):
         o = fm.SolverOptions(compute_residual=res).to_c()
@@ -26,8 +26,9 @@ for chunks in ("8", "4", "16"):
         for _ in range(3):
             ctx._lib.fmap_solve_f32(ctx.handle, 64, 200, P(hG), P(hR), P(hM), 100.0, C.byref(o), P(hC), C.byref(rep))
         t0 = time.perf_counter()
-        for _ in range(10):
+        for _ in range(40):
             st = ctx._lib.fmap_solve_f32(ctx.handle, 64, 200, P(hG), P(hR), P(hM), 100.0, C.byref(o), P(hC),
                                          C.byref(rep))
-        ms = (time.perf_counter() - t0) * 100
-        print(f"chunks={chunks} residual={res}: {ms:.3f} ms/step  st={st} launches={ctx.last_launches[:6]}...")
+        ms = (time.perf_counter() - t0) * 25
+        print(f"chunks={chunks} residual={res}: {ms:.3f} ms/step (device span {rep.wall_seconds * 1e3:.3f} ms)"
+              f"  st={st} launches={len(ctx.last_launches)}")

@@ -40,6 +40,11 @@ def main():
             for i, n in enumerate(names):
                 if n == want:
                     out[want] = f"{vals[i]} {units[i]}".strip()
+        # tensor-pipe activity (tcgen05 issue / UTC pipes), whatever names this ncu exposes
+        for i, n in enumerate(names):
+            if ("pipe_tensor" in n or "pipe_tc" in n or "pipe_uma" in n or "pipe_utc" in n) and (
+                    n.endswith(".pct_of_peak_sustained_active") or n.endswith(".sum")):
+                out[n] = f"{vals[i]} {units[i]}".strip()
     for k, v in out.items():
         print(f"{k:70s} {v}")
     sass = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
