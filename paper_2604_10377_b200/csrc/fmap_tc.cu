@@ -295,16 +295,14 @@ __global__ void __launch_bounds__(MAXT, MINB)
   float* opnd_lo = smem + Ly.off_lo;
   float* LTb = smem + Ly.off_lt;  // system h: LT = LTb + 272h, LT[t][c] = L[c][t]; inv = LT + 256
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + Ly.off_misc);
-  // mbar[0] LA, [1] REST, [2] opsready (one arrival per main warp), [3] ysync,
-  // [4 + s] fact (slot s), [4 + 2NS + s] bsub, [4 + 4NS + 2h + u] lfull (B warp h, buffer u),
-  // [4 + 6NS] chk (G chunk TMA), [+1] cpd (tcgen05.cp done), [+2] a0f (panel-0 TMA), [+3] stg
+  // mbar[0 .. 3) la[g]: lookahead MMA of row group g done; [3] REST MMAs done;
+  // [4 .. 7) ops[g]: operands of row group g stored (one arrival per warp of the group);
+  // [7] chk (G chunk TMA), [8] cpd (tcgen05.cp done), [9] a0f (panel-0 TMA), [10] stg
   // (next pair fully staged: MMA warp -> main warps)
-  uint64_t* opsready = mbar + 2;
-  uint64_t* ysync = mbar + 3;
-  uint64_t* fact = mbar + 4;
-  uint64_t* bsub = mbar + 4 + 2 * NS;
-  uint64_t* lfull = mbar + 4 + 4 * NS;
-  uint64_t* chk = mbar + 4 + 6 * NS;
+  uint64_t* la = mbar;
+  uint64_t* rest = mbar + 3;
+  uint64_t* ops = mbar + 4;
+  uint64_t* chk = mbar + 7;
   uint64_t* cpd = chk + 1;
   uint64_t* a0f = chk + 2;
   uint64_t* stg = chk + 3;
@@ -331,7 +329,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
     scb[8 * tid + 4] = 0u;
   }
   if (tid == 0) {
-    for (int e = 0; e < 8 + 6 * NS; ++e) mbar_init(&mbar[e], e == 2 ? (uint32_t)(Ly.nmain / 32) : 1u);
+    for (int e = 0; e < 11; ++e) {
+      uint32_t cnt = 1u;
+      if (e >= 4 && e < 4 + kMaxGroups)  // warps of row group e - 4 (4, the top group fewer)
+        cnt = e - 4 < Ly.G - 1 ? 4u : (e - 4 == Ly.G - 1 ? (uint32_t)(Ly.nmain / 32 - 4 * (Ly.G - 1)) : 1u);
+      mbar_init(&mbar[e], cnt);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, (uint32_t)Ly.tmem_cols);
@@ -414,16 +417,27 @@ __global__ void __launch_bounds__(MAXT, MINB)
         }
         bool cpd_pending = false;
         for (int pp = 0; pp < P; ++pp, ++gm) {
-          mbar_wait(opsready, gm & 1);
-          TC_TRACE(pp < 16, 800 + pp);
-          tc_fence_after();
           const int r0 = 16 * pp + 16;
+          // Lookahead per row group, the group holding the next diagonal block (rows
+          // r0..r0+15, the B operand of every group's lookahead) first: its warps'
+          // next panel waits only for its own lookahead, not for the slowest group's
+          // operand stores (early panels: the 128-row bottom group).
+          int gb = 0;
 #pragma unroll
-          for (int h = 0; h < NS; ++h)
+          for (int gg = 0; gg < kMaxGroups; ++gg)
+            if (gg < Ly.G && r0 >= Ly.lo[gg] && r0 < Ly.hi[gg]) gb = gg;
 #pragma unroll
-            for (int gg = 0; gg < kMaxGroups; ++gg)
-              if (gg < Ly.G && Ly.hi[gg] > r0) mma3(h, Ly.lo[gg], Ly.base[gg], r0, 16);
-          mma_commit(&mbar[0]);
+          for (int o = 0; o < kMaxGroups; ++o) {
+            const int gg = o == 0 ? gb : (o <= gb ? o - 1 : o);
+            if (gg >= Ly.G) continue;
+            mbar_wait(&ops[gg], gm & 1);
+            tc_fence_after();
+            if (Ly.hi[gg] > r0)
+#pragma unroll
+              for (int h = 0; h < NS; ++h) mma3(h, Ly.lo[gg], Ly.base[gg], r0, 16);
+            mma_commit(&la[gg]);
+          }
+          TC_TRACE(pp < 16, 800 + pp);
           TC_TRACE(pp < 16, 820 + pp);
           // next pair: panel-0 columns (a0s is free: every main warp is past panel 0)
           // and chunk pp into the tile (free once the previous chunk's copies are done)
@@ -457,7 +471,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
                 c0 += N;
               }
             }
-          mma_commit(&mbar[1]);
+          mma_commit(rest);
           TC_TRACE(pp < 16, 840 + pp);
           if (pf && pp >= 1) {  // chunk pp of the current pair was read at this panel's top
             mbar_wait(chk, n_chk & 1);
@@ -599,7 +613,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
     // previous systems' MMAs must be complete before TMEM is rewritten
     if (any_mma) {
-      mbar_wait(&mbar[1], (g - 1) & 1);
+      mbar_wait(rest, (g - 1) & 1);
       tc_fence_after();
     }
     TC_TRACE(tid == 0, 399);
@@ -743,7 +757,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
 #pragma unroll
         for (int h = 0; h < NS; ++h) load_a0(h, a[h]);
       } else if (has_grp && ghi > j) {  // panel columns updated by the previous lookahead MMA
-        mbar_wait(&mbar[0], (g - 1) & 1);
+        mbar_wait(&la[grp], (g - 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < NS; ++h) tmem_ld16(tq + tsys * h + (uint32_t)j, a[h]);
@@ -849,7 +863,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
           for (int c4 = 0; c4 < 4; ++c4)
             __stcg(dst + c4, make_float4(l[h][4 * c4], l[h][4 * c4 + 1], l[h][4 * c4 + 2], l[h][4 * c4 + 3]));
         }
-        if (pp > 0) mbar_wait(&mbar[1], (g - 1) & 1);  // previous REST MMA done reading
+        if (pp > 0) mbar_wait(rest, (g - 1) & 1);  // previous REST MMA done reading
         TC_TRACE(lane == 0 && pp < 12 && warp < 8, 1300 + 8 * pp + warp);
 #pragma unroll
         for (int h = 0; h < NS; ++h) {
@@ -871,7 +885,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
       __syncwarp();
       if (lane == 0) {
         TC_TRACE(pp < 12 && warp < 8, 700 + 8 * pp + warp);
-        mbar_arrive(opsready);  // operands of this panel stored
+        mbar_arrive(&ops[grp]);  // operands of this panel stored
       }
       any_mma = true;
       if (has_next) {
@@ -932,7 +946,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
   // ---- teardown ----
   if (any_mma) {
-    mbar_wait(&mbar[1], (g - 1) & 1);
+    mbar_wait(rest, (g - 1) & 1);
     tc_fence_after();
   }
   main_sync(NM);

@@ -178,6 +178,56 @@ __device__ __forceinline__ void dfE(float (&a)[16], float& inv, int g, float* xb
   }
 }
 
+// (G) 4 pivots per round, shuffles only: the pivot block's lower entries come from
+// lanes t..t+3 (10 SHFL), every lane factors it locally, transforms its own four
+// entries (o), and the rank-4 update takes each row c's transformed entries from
+// lane c (4 SHFL per row).
+template <int t>
+__device__ __forceinline__ void dfG_round(float (&a)[16], float& inv, int g) {
+  float B[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v <= u; ++v) B[u][v] = __shfl_sync(kFull, a[t + v], t + u, 16);
+  float rs[4], rd[4], f[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    rs[u] = rsqrt_fast(B[u][u]);
+    rd[u] = rs[u] * rs[u];
+#pragma unroll
+    for (int w = u + 1; w < 4; ++w) {
+      f[u][w] = B[w][u] * rd[u];
+#pragma unroll
+      for (int r = w; r < 4; ++r) B[r][w] = fmaf(-f[u][w], B[r][u], B[r][w]);
+    }
+  }
+  float o[4] = {a[t], a[t + 1], a[t + 2], a[t + 3]};
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+#pragma unroll
+    for (int w = u + 1; w < 4; ++w) o[w] = fmaf(-f[u][w], o[u], o[w]);
+  float m[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    m[u] = o[u] * rd[u];
+    a[t + u] = o[u] * rs[u];
+    if (g == t + u) inv = rs[u];
+  }
+#pragma unroll
+  for (int c = t + 4; c < 16; ++c) {
+    float acc = a[c];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = fmaf(-m[u], __shfl_sync(kFull, o[u], c, 16), acc);
+    a[c] = acc;
+  }
+}
+__device__ __forceinline__ void dfG(float (&a)[16], float& inv, int g) {
+  dfG_round<0>(a, inv, g);
+  dfG_round<4>(a, inv, g);
+  dfG_round<8>(a, inv, g);
+  dfG_round<12>(a, inv, g);
+}
+
 template <int V>
 __global__ void kern(long long* out, float* sink) {
   __shared__ __align__(16) float xb[256];
@@ -197,7 +247,8 @@ __global__ void kern(long long* out, float* sink) {
     else if (V == 1) dfB(b, inv, g, xb + 16 * (lane >> 4));
     else if (V == 2) dfC(b, inv, g, xb + 32 * (lane >> 4));
     else if (V == 3) dfD(b, inv, g, xb + 64 * (lane >> 4));
-    else dfE(b, inv, g, xb + 128 * (lane >> 4));
+    else if (V == 4) dfE(b, inv, g, xb + 128 * (lane >> 4));
+    else dfG(b, inv, g);
     float s = inv;
 #pragma unroll
     for (int c = 0; c < 16; ++c) s += b[c];
@@ -217,6 +268,7 @@ __global__ void kern(long long* out, float* sink) {
     else if (V == 2) dfC(b, iv, g, xb);
     else if (V == 3) dfD(b, iv, g, xb);
     else if (V == 4) dfE(b, iv, g, xb);
+    else if (V == 5) dfG(b, iv, g);
     for (int c = 0; c <= 5; ++c) sink[8 + 8 * V + c] = b[c];
   }
   if (acc == 1.2345f) sink[0] = acc;
@@ -226,18 +278,20 @@ int main() {
   long long* d;
   float* s;
   cudaMalloc(&d, 64);
-  cudaMalloc(&s, 64);
+  cudaMalloc(&s, 1024);
   kern<0><<<1, 32>>>(d, s);
   kern<1><<<1, 32>>>(d, s);
   kern<2><<<1, 32>>>(d, s);
   kern<3><<<1, 32>>>(d, s);
   kern<4><<<1, 32>>>(d, s);
-  long long h[5];
-  cudaMemcpy(h, d, 40, cudaMemcpyDeviceToHost);
+  kern<5><<<1, 32>>>(d, s);
+  long long h[6];
+  cudaMemcpy(h, d, 48, cudaMemcpyDeviceToHost);
+  printf("4-pivot shuffles (G): %lld cycles\n", h[5]);
   printf("4-pivot (E): %lld cycles\n", h[4]);
   float L[64];
   cudaMemcpy(L, s, 256, cudaMemcpyDeviceToHost);
-  for (int v = 0; v < 5; ++v) { if (v == 1) continue; printf("variant %d row5:", v); for (int c = 0; c <= 5; ++c) printf(" %.6f", L[8 + 8 * v + c]); printf("\n"); }
+  for (int v = 0; v < 6; ++v) { if (v == 1) continue; printf("variant %d row5:", v); for (int c = 0; c <= 5; ++c) printf(" %.6f", L[8 + 8 * v + c]); printf("\n"); }
   printf("diag16 shfl (A): %lld\nsmem-row LDLt div+shfl (B): %lld\nsmem-row LDLt rcp (C): %lld\n2-pivot (D): %lld cycles\n%s\n",
          h[0], h[1], h[2], h[3], cudaGetErrorString(cudaGetLastError()));
   return 0;
