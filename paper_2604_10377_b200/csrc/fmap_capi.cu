@@ -461,10 +461,16 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   p.mask = dM;
   p.C = dC;
   p.gram_rowsum = rowsum;
+  const char* dbg_env = std::getenv("FMAP_DEBUG");  // timing experiments only: 2 = no H2D, 4 = no D2H
+  const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   for (int c = 0; c < nchunk; ++c) {  // all H2D first: the copy stream never waits on the solver
     const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
     if (nq <= 0) break;
     const size_t off = (size_t)q0 * kk, nb = (size_t)nq * kk * sizeof(float);
+    if (dbg & 2) {
+      FMAP_CK(ctx, cudaEventRecord(ctx->cev[2 + 2 * c], ctx->copy));
+      continue;
+    }
     FMAP_CK(ctx, cudaMemcpyAsync(dG + off, gram + off, nb, cudaMemcpyHostToDevice, ctx->copy));
     FMAP_CK(ctx, cudaMemcpyAsync(dR + off, rhs + off, nb, cudaMemcpyHostToDevice, ctx->copy));
     FMAP_CK(ctx, cudaMemcpyAsync(dM + off, mask + off, nb, cudaMemcpyHostToDevice, ctx->copy));
@@ -488,7 +494,7 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
       FMAP_CK(ctx, launch_residual_tiles(dC + off, dG + off, dR + off, dM + off, nq, (int)k, lambda,
                                          partial + (size_t)q0 * residual_tile_count((int)k), s));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy2, done, 0));
-    FMAP_CK(ctx, cudaMemcpyAsync(C_out + off, dC + off, nb, cudaMemcpyDeviceToHost, ctx->copy2));
+    if (!(dbg & 4)) FMAP_CK(ctx, cudaMemcpyAsync(C_out + off, dC + off, nb, cudaMemcpyDeviceToHost, ctx->copy2));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[3 + 2 * nchunk], ctx->copy));  // all H2D done (stream join)
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[3 + 2 * nchunk], 0));

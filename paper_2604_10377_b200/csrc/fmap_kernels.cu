@@ -522,15 +522,22 @@ cudaError_t launch_project(const float* phi, const float* mass, const float* F, 
                            int64_t n, int k, int d, float* out, cudaStream_t st) {
   // tensor-core path (tcgen05, 3xTF32, accumulation folded into an fp32 sum every
   // 256 vertices so the tensor core's biased accumulation stays bounded: 2.0e-6 of
-  // max|A| at cfg2 vs 3.4e-6 for the FP32 kernel, 0.97 vs 1.25 ms) whenever d <= 256
-  // and its grid (one CTA per pair and 128 basis functions) covers at least half
-  // the SMs; FMAP_PROJ=simt / tc forces either kernel.
+  // max|A| at cfg2 vs 3.4e-6 for the FP32 kernel) whenever d <= 256 and its
+  // estimated time beats the FP32 SIMT kernel's: one CTA (pair of CTAs for
+  // 128 < k <= 256) per shape and 128 basis functions streams the n vertices in
+  // ~56 ns per vertex (43 ns for the pair kernel) per wave of SM-resident CTAs,
+  // the SIMT kernel runs ~9.5 TFLOP/s over the whole batch (cfg2: 0.22 vs 3.4 ms;
+  // cfg3 b = 16, n = 10000: 0.43 vs 1.73 ms; 2 pairs at k = 50: SIMT).  FMAP_PROJ=
+  // simt / tc forces either kernel.
   const char* sel = std::getenv("FMAP_PROJ");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t tc_grid = b * ((k + 127) / 128);
-  const bool want_tc = sel ? sel[0] == 't' : (d <= 256 && 2 * tc_grid >= sms);
+  const bool pair = k > 128 && k <= 256;
+  const int64_t tc_ctas = pair ? 2 * b : b * ((k + 127) / 128);
+  const double tc_s = (double)((tc_ctas + sms - 1) / sms) * (double)n * (pair ? 43e-9 : 56e-9);
+  const double simt_s = 2.0 * (double)b * (double)n * k * d / 9.5e12;
+  const bool want_tc = sel ? sel[0] == 't' : (d <= 256 && tc_s < simt_s);
   if (want_tc) {
     const cudaError_t e = launch_project_tc(phi, mass, F, b, n, k, d, out, st);
     if (e != cudaErrorNotSupported) return e;

@@ -1806,6 +1806,200 @@ __global__ void __launch_bounds__(kPjThreads, 2)
   __syncthreads();
   if (warp == 0) tmem_dealloc(tbase, tcols);
 }
+
+// CTA-pair projection for 128 < k <= 256: the two CTAs of a cluster hold basis
+// functions 0..127 / 128..255 (the A halves) and feature channels 0..N/2-1 /
+// N/2..N-1 (the B halves) of one shape, and the leader issues M = 256
+// tcgen05.mma.cta_group::2 -- each SM streams and converts half of F instead of
+// all of it, reads half of the B operand per MMA, and no M = 128 tile is padded
+// (k = 200: 72 of 128 rows in the second tile of proj_tma_kernel).  Per 16-vertex
+// stage and SM: ~112 KB of shared-memory traffic instead of ~168 KB.  Same TMA
+// ring, hi/lo conversion, 3xTF32 MMAs and chunk fold as proj_tma_kernel; the peer's
+// producers arrive on the leader's barriers through shared::cluster addresses and
+// the MMA commits are multicast to both CTAs.
+constexpr int kPpB = 4;  // operand stage buffers of the pair kernel
+#ifndef FMAP_PP_CHUNK
+#define FMAP_PP_CHUNK 16
+#endif
+constexpr int kPpChunk = FMAP_PP_CHUNK;  // stages per accumulator fold (pair kernel)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPjThreads, 1)
+    proj_pair_kernel(const __grid_constant__ CUtensorMap tmPhi, const __grid_constant__ CUtensorMap tmF,
+                     const __grid_constant__ CUtensorMap tmMass, int64_t n, int k, int d, int N,
+                     float* __restrict__ out) {
+  extern __shared__ __align__(1024) float smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_rank();
+  const int q = blockIdx.y;
+  const int i0 = (int)rank * 128;           // this CTA's basis functions (A half)
+  const int Nh = N / 2, c_off = (int)rank * Nh;  // this CTA's feature channels (B half)
+  const int abytes = 128 * kPjK, bbytes = Nh * kPjK;  // floats
+  const int sstride = 2 * abytes + 2 * bbytes;
+  const int rstride = (2048 + 16 * Nh + 16 + 31) & ~31;  // raw slot: Phi [16][128] | F [16][Nh] | Mass [16]
+  float* raw = smem + kPpB * sstride;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + kPjR * rstride);
+  uint64_t* opfull = bar;                 // [B] (leader) producer warps of both CTAs -> MMA
+  uint64_t* opempty = bar + kPpB;         // [B] MMA commit (multicast) -> producers
+  uint64_t* conv = bar + 2 * kPpB;        // [B] this CTA's producers -> this CTA's TMA refill
+  uint64_t* chunkdone = bar + 3 * kPpB;   // MMA commit (multicast) -> producers
+  uint64_t* folded = chunkdone + 1;       // (leader) producer warps of both CTAs -> MMA
+  uint64_t* rawfull = chunkdone + 2;      // [R] TMA -> producers
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rawfull + kPjR);
+  if (tid == 0) {
+    for (int u = 0; u < kPpB; ++u) {
+      mbar_init(&opfull[u], 16);
+      mbar_init(&opempty[u], 1);
+      mbar_init(&conv[u], 8);
+    }
+    mbar_init(chunkdone, 1);
+    mbar_init(folded, 16);
+    for (int r = 0; r < kPjR; ++r) mbar_init(&rawfull[r], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc2(tslot, 512u);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t sumoff = (uint32_t)N;
+  const int nst = (int)((n + kPjK - 1) / kPjK);
+  const uint32_t rawbytes = (uint32_t)(2048 + 16 * Nh + 16) * 4u;
+
+  if (warp == 8) {  // ---- TMA issue (both CTAs) + MMA issue (leader) ----
+    if (lane == 0) {
+      auto issue_raw = [&](int s2) {
+        const int slot = s2 % kPjR;
+        float* rs = raw + slot * rstride;
+        mbar_expect_tx(&rawfull[slot], rawbytes);
+        tma_load_3d(rs, &tmPhi, i0, s2 * kPjK, q, &rawfull[slot]);
+        tma_load_3d(rs + 2048, &tmF, c_off, s2 * kPjK, q, &rawfull[slot]);
+        tma_load_2d(rs + 2048 + 16 * Nh, &tmMass, s2 * kPjK, q, &rawfull[slot]);
+      };
+      for (int s2 = 0; s2 < kPjR && s2 < nst; ++s2) issue_raw(s2);
+      if (rank == 0) {
+        // D f32, A/B tf32 K-major, D += A*B, N, M = 256
+        const uint32_t id = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | (16u << 24);
+        for (int st = 0; st < nst; ++st) {
+          const int buf = st % kPpB;
+          const int cs = st % kPpChunk;
+          if (cs == 0 && st > 0) {
+            mbar_wait(folded, ((st / kPpChunk) - 1) & 1);
+            tc_fence_after();
+          }
+          mbar_wait(&opfull[buf], (st / kPpB) & 1);  // both CTAs converted stage st
+          tc_fence_after();
+          if (st + kPjR < nst) issue_raw(st + kPjR);
+          const uint32_t ah = su32(smem + buf * sstride), al = ah + abytes * 4;
+          const uint32_t bh = al + abytes * 4, bl = bh + bbytes * 4;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t ko = (uint32_t)ks * 256u;
+            mma_tf32_2sm(tbase, sdesc(ah + ko), sdesc(bh + ko), id, (cs > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32_2sm(tbase, sdesc(ah + ko), sdesc(bl + ko), id, 1u);
+            mma_tf32_2sm(tbase, sdesc(al + ko), sdesc(bh + ko), id, 1u);
+          }
+          mma_commit_pair(&opempty[buf]);
+          if (cs == kPpChunk - 1 || st == nst - 1) mma_commit_pair(chunkdone);
+        }
+      } else {
+        for (int st = 0; st < nst; ++st) {
+          mbar_wait(&conv[st % kPpB], (st / kPpB) & 1);  // this CTA converted stage st: slot st % R free
+          if (st + kPjR < nst) issue_raw(st + kPjR);
+        }
+      }
+    }
+  } else {  // ---- producers (256 threads): raw fp32 tiles -> hi/lo operands ----
+    const int ia = tid & 127, vg = tid >> 7;  // row ia (basis function / channel), vertices 8vg..8vg+7
+    const uint32_t opfull0 = mapa_rank(su32(opfull), 0);  // + 8 bytes per buffer
+    const uint32_t folded0 = mapa_rank(su32(folded), 0);
+    for (int st = 0; st < nst; ++st) {
+      const int buf = st % kPpB, slot = st % kPjR;
+      mbar_wait(&rawfull[slot], (st / kPjR) & 1);
+      if (st >= kPpB) mbar_wait(&opempty[buf], ((st - kPpB) / kPpB) & 1);  // MMAs of stage st-B done
+      const float* rp = raw + slot * rstride;
+      const float* rf = rp + 2048;
+      const float* rm = rp + 2048 + 16 * Nh;
+      float* S = smem + buf * sstride;
+#pragma unroll
+      for (int h4 = 0; h4 < 2; ++h4) {
+        const int v4 = 2 * vg + h4;
+        const int o = (ia >> 3) * 128 + v4 * 32 + (ia & 7) * 4;
+        float av[4], hv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          av[u] = rp[(4 * v4 + u) * 128 + ia];
+          hv[u] = tf32_hi(av[u]);
+        }
+        *reinterpret_cast<float4*>(S + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<float4*>(S + abytes + o) =
+            make_float4(av[0] - hv[0], av[1] - hv[1], av[2] - hv[2], av[3] - hv[3]);
+        if (ia < Nh) {
+          float bv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            bv[u] = rf[(4 * v4 + u) * Nh + ia] * rm[4 * v4 + u];
+            hv[u] = tf32_hi(bv[u]);
+          }
+          *reinterpret_cast<float4*>(S + 2 * abytes + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<float4*>(S + 2 * abytes + bbytes + o) =
+              make_float4(bv[0] - hv[0], bv[1] - hv[1], bv[2] - hv[2], bv[3] - hv[3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&conv[buf]);
+        mbar_arrive_cluster(opfull0 + 8u * (uint32_t)buf);
+      }
+      if (st % kPpChunk == kPpChunk - 1 || st == nst - 1) {
+        const int c = st / kPpChunk;
+        mbar_wait(chunkdone, c & 1);
+        tc_fence_after();
+        const int quarter = warp & 3, half = warp >> 2, nh = ((N / 2) + 15) & ~15;
+        const uint32_t tl = tbase + ((uint32_t)(32 * quarter) << 16);
+        for (int c0 = half * nh; c0 < min(N, (half + 1) * nh); c0 += 16) {
+          float v[16];
+          tmem_ld16(tl + (uint32_t)c0, v);
+          if (c > 0) {
+            float sv[16];
+            tmem_ld16(tl + sumoff + (uint32_t)c0, sv);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] += sv[t];
+          }
+          tmem_st16(tl + sumoff + (uint32_t)c0, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(folded0);
+      }
+    }
+    const int quarter = warp & 3, half = warp >> 2;
+    const int i = i0 + 32 * quarter + lane;
+    const int nh = ((N / 2) + 15) & ~15;
+    for (int c0 = half * nh; c0 < min(N, (half + 1) * nh); c0 += 16) {
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(32 * quarter) << 16) + sumoff + (uint32_t)c0, v);
+      if (i < k) {
+        float* o = out + ((size_t)q * k + i) * d + c0;
+        if (c0 + 16 <= d) {
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4)
+            *reinterpret_cast<float4*>(o + 4 * c4) = make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (c0 + t < d) o[t] = v[t];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer is done with this CTA's barriers and TMEM
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc2(tbase, 512u);
+}
 }  // namespace
 
 // Tensor-core projection (d <= 256); returns cudaErrorNotSupported otherwise.
@@ -1828,6 +2022,31 @@ cudaError_t launch_project_tc(const float* phi, const float* mass, const float* 
   if (d > 256 || d < 1 || k < 1 || n < 1 || b < 1) return cudaErrorNotSupported;
   const int N = (d + 15) & ~15;
   // TMA-streamed kernel when every row stride is 16-byte aligned
+  const char* pair_env = std::getenv("FMAP_PROJ_PAIR");  // "0": the one-CTA kernel below instead
+  if (k > 128 && k <= 256 && k % 4 == 0 && d % 4 == 0 && n % 4 == 0 && !(pair_env && pair_env[0] == '0') &&
+      !std::getenv("FMAP_PROJ_NOTMA")) {
+    // CTA-pair kernel: N a multiple of 32 (each CTA's half of the channels is a
+    // multiple of 16), TMA boxes of 128 basis functions / N/2 channels / 16 vertices
+    const int Np = (d + 31) & ~31;
+    CUtensorMap tp, tf, tm;
+    const cuuint64_t dp[3] = {(cuuint64_t)k, (cuuint64_t)n, (cuuint64_t)b};
+    const cuuint32_t bp[3] = {128, (cuuint32_t)kPjK, 1};
+    const cuuint64_t df[3] = {(cuuint64_t)d, (cuuint64_t)n, (cuuint64_t)b};
+    const cuuint32_t bf[3] = {(cuuint32_t)(Np / 2), (cuuint32_t)kPjK, 1};
+    const cuuint64_t dm[2] = {(cuuint64_t)n, (cuuint64_t)b};
+    const cuuint32_t bm[2] = {(cuuint32_t)kPjK, 1};
+    if (b <= 65535 && encode_plain_map(&tp, phi, 3, dp, bp) == 0 && encode_plain_map(&tf, F, 3, df, bf) == 0 &&
+        encode_plain_map(&tm, mass, 2, dm, bm) == 0) {
+      const int Nh = Np / 2;
+      const int rstride = (2048 + 16 * Nh + 16 + 31) & ~31;
+      const size_t smem = (size_t)(kPpB * (2 * 128 * kPjK + 2 * Nh * kPjK) + kPjR * rstride) * 4 + 256;
+      cudaError_t e = cudaFuncSetAttribute(proj_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      note_launch("proj_pair_kernel");
+      proj_pair_kernel<<<dim3(2, (unsigned)b), kPjThreads, smem, st>>>(tp, tf, tm, n, k, d, Np, out);
+      return cudaGetLastError();
+    }
+  }
   if (k % 4 == 0 && d % 4 == 0 && n % 4 == 0 && !std::getenv("FMAP_PROJ_NOTMA")) {
     CUtensorMap tp, tf, tm;
     const cuuint64_t dp[3] = {(cuuint64_t)k, (cuuint64_t)n, (cuuint64_t)b};

@@ -3,7 +3,7 @@ C ABI (fmap_project_f32_dev / fmap_pipeline_f32_dev), against float64 truth and
 the oracle (restated reference solver, oracle/).
 
 The kernels these shapes select are asserted from fmap_last_launches, so the
-default cfg2 projection kernel (proj_tma_kernel: tcgen05 3xTF32, TMA-streamed)
+default cfg2 projection kernel (proj_pair_kernel: CTA-pair tcgen05 3xTF32, TMA-streamed)
 and the k > 256 solver variant are the ones under test.  Bars: projection
 max|dA| <= 1e-5 * max|A| (f64 truth); solver max|dC| <= 1e-4 * ||C||_max
 (north_star) against the oracle's f64 route on the checked pairs; relative
@@ -56,22 +56,50 @@ def _check_direction(oracle, Cgpu, A, B, ev_src, ev_tgt, lam, sigma, check_pairs
             assert err <= TOL_REL * np.abs(ref).max(), f"{what} pair {q}: max|dC| {err:.3e}"
 
 
-def test_projection_default_kernel_at_cfg2_shape(fm):
-    # cfg2: 64 pairs, n = 5000, k = 200, d = 256 -> proj_tma_kernel (the kernel the
-    # pipeline number is made of); all 64 shapes checked against f64.
-    cfg, data = _batch("cfg2")
-    b, n, k, d = cfg.batch, cfg.n_src, cfg.k, cfg.d
-    t = {key: _dev(data[key]) for key in ("phi1", "mass1", "F1")}
+def _project(fm, b, n, k, d, phi, mass, F):
+    t = [_dev(x) for x in (phi, mass, F)]
     out = torch.empty((b, k, d), device="cuda")
     ctx = fm._lib.context(0)
-    st = ctx._lib.fmap_project_f32_dev(ctx.handle, b, n, k, d, C.c_void_p(t["phi1"].data_ptr()),
-                                       C.c_void_p(t["mass1"].data_ptr()), C.c_void_p(t["F1"].data_ptr()),
+    st = ctx._lib.fmap_project_f32_dev(ctx.handle, b, n, k, d, *(C.c_void_p(x.data_ptr()) for x in t),
                                        C.c_void_p(out.data_ptr()))
     assert st == 0, ctx.last_error()
-    assert ctx.last_launches == ["proj_tma_kernel"], ctx.last_launches
     torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64), ctx.last_launches
+
+
+@pytest.mark.parametrize("pair_env, kernel", [(None, "proj_pair_kernel"), ("0", "proj_tma_kernel")])
+def test_projection_default_kernel_at_cfg2_shape(fm, monkeypatch, pair_env, kernel):
+    # cfg2: 64 pairs, n = 5000, k = 200, d = 256 -> proj_pair_kernel (CTA pairs,
+    # tcgen05.mma.cta_group::2 with M = 256: the kernel the pipeline number is made
+    # of) or, with FMAP_PROJ_PAIR=0, the one-CTA proj_tma_kernel; all 64 shapes
+    # checked against f64.
+    if pair_env is not None:
+        monkeypatch.setenv("FMAP_PROJ_PAIR", pair_env)
+    cfg, data = _batch("cfg2")
+    b, n, k, d = cfg.batch, cfg.n_src, cfg.k, cfg.d
+    out, launches = _project(fm, b, n, k, d, data["phi1"], data["mass1"], data["F1"])
+    assert launches == [kernel], launches
     ref = _proj64(data["phi1"], data["mass1"], data["F1"])
-    err = np.abs(out.cpu().numpy().astype(np.float64) - ref).max(axis=(1, 2))
+    err = np.abs(out - ref).max(axis=(1, 2))
+    scale = np.abs(ref).max(axis=(1, 2))
+    assert np.all(err <= 1e-5 * scale), float((err / scale).max())
+
+
+@pytest.mark.parametrize("b, n, k, d", [(3, 1000, 132, 200), (2, 2048, 256, 256), (5, 700, 200, 36),
+                                        (148, 320, 140, 64)])
+def test_projection_pair_kernel_shapes(fm, monkeypatch, b, n, k, d):
+    # the CTA-pair kernel at the edges of its range (k just above 128, k = 256, d not
+    # a multiple of 32 so the channel halves are padded, n not a multiple of the
+    # 16-vertex stage, more clusters than fit the GPU at once)
+    monkeypatch.setenv("FMAP_PROJ", "tc")
+    rng = np.random.default_rng(b * 1000 + k)
+    phi = (rng.standard_normal((b, n, k)) / np.sqrt(n)).astype(np.float32)
+    mass = (rng.uniform(0.5, 1.5, (b, n)) / n).astype(np.float32)
+    F = rng.standard_normal((b, n, d)).astype(np.float32)
+    out, launches = _project(fm, b, n, k, d, phi, mass, F)
+    assert launches == ["proj_pair_kernel"], launches
+    ref = _proj64(phi, mass, F)
+    err = np.abs(out - ref).max(axis=(1, 2))
     scale = np.abs(ref).max(axis=(1, 2))
     assert np.all(err <= 1e-5 * scale), float((err / scale).max())
 
@@ -91,7 +119,7 @@ def test_pipeline_cfg2_full_batch(fm, oracle):
     # headline configuration, BASELINE generator: residual on all 64 pairs, 8 pairs
     # against the oracle's f64 route
     cfg, data, cxy, _, rep, launches, A, B = _pipeline(fm, "cfg2")
-    assert launches.count("proj_tma_kernel") == 2 and "chol_tc_kernel" in launches, launches
+    assert launches.count("proj_pair_kernel") == 2 and "chol_tc_kernel" in launches, launches
     _check_direction(oracle, cxy, A, B, data["ev1"], data["ev2"], cfg.lam, cfg.sigma, set(range(0, 64, 8)), "cfg2")
     assert rep.min_rcond > 1e-7
 

@@ -18,8 +18,9 @@ hG, hR, hM = (torch.from_numpy(x).pin_memory() for x in (G, R, M))
 hC = torch.empty_like(hG).pin_memory()
 ctx = _lib.context(0)
 P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
-for chunks in ("4", "2", "8"):
+for chunks, dbg in (("4", "0"), ("4", "2"), ("4", "6"), ("1", "0"), ("1", "6")):
     os.environ["FMAP_PIPELINE"] = chunks
+    os.environ["FMAP_DEBUG"] = dbg
     for res in (False, True):
         o = fm.SolverOptions(compute_residual=res).to_c()
         rep = _lib.ReportC()
@@ -30,5 +31,5 @@ for chunks in ("4", "2", "8"):
             st = ctx._lib.fmap_solve_f32(ctx.handle, 64, 200, P(hG), P(hR), P(hM), 100.0, C.byref(o), P(hC),
                                          C.byref(rep))
         ms = (time.perf_counter() - t0) * 25
-        print(f"chunks={chunks} residual={res}: {ms:.3f} ms/step (device span {rep.wall_seconds * 1e3:.3f} ms)"
+        print(f"chunks={chunks} dbg={dbg} residual={res}: {ms:.3f} ms/step (device span {rep.wall_seconds * 1e3:.3f} ms)"
               f"  st={st} launches={len(ctx.last_launches)}")
