@@ -47,7 +47,8 @@ struct fmap_ctx {
   int num_sms = 0;
   // host-buffer pipelining (fmap_solve_f32): second compute stream + copy stream
   cudaStream_t comp2 = nullptr, copy = nullptr, copy2 = nullptr;  // 2nd compute, H2D, D2H
-  cudaEvent_t cev[37] = {};  // start | done | per chunk: H2D done, solve done (x 16 chunks) | H2D join | compute join
+  // start | done | per chunk (<= 16): G+M landed, R landed, solve done | H2D join | compute join
+  cudaEvent_t cev[52] = {};
 };
 
 namespace {
@@ -399,13 +400,34 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
 // second copy stream (the other direction's copy engine) right after its solve.
 // Same checks as solve_core (device validation, lowest failing index); on any error
 // C_out is zero-filled, so no partial result is exposed.  Used when no fault
-// injection is requested; the residual (check_stationarity) runs per chunk.
+// injection is requested; the residual (check_stationarity) runs after the last chunk.
 int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const float* rhs,
                          const float* mask, float lambda, const fmap_solver_options& opts, float* C_out,
                          fmap_report* rep, int nchunk) {
   const size_t kk = (size_t)k * k;
   const size_t bytes = (size_t)b * kk * sizeof(float);
-  const int64_t cb = (b + nchunk - 1) / nchunk;  // pairs per chunk
+  // chunk boundaries: nchunk > 0 -> equal chunks; 0 -> ramp (2,3,3,3,3,2 sixteenths:
+  // a smaller first H2D and last D2H, the only copies not hidden behind a solve)
+  std::vector<int64_t> cq0, cnq;
+  if (nchunk <= 0) {
+    static const int cum[7] = {0, 2, 5, 8, 11, 14, 16};
+    for (int c = 0; c < 6; ++c) {
+      const int64_t lo = b * cum[c] / 16, hi = b * cum[c + 1] / 16;
+      if (hi > lo) {
+        cq0.push_back(lo);
+        cnq.push_back(hi - lo);
+      }
+    }
+  } else {
+    const int64_t cbq = (b + nchunk - 1) / nchunk;
+    for (int64_t q = 0; q < b; q += cbq) {
+      cq0.push_back(q);
+      cnq.push_back(std::min<int64_t>(cbq, b - q));
+    }
+  }
+  nchunk = (int)cq0.size();
+  int64_t cb = 0;
+  for (int64_t v : cnq) cb = std::max(cb, v);
   const int64_t csys = cb * k;
   const size_t tcb = tc_scratch_bytes((int)k, csys, ctx->num_sms);
   const size_t npart = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
@@ -463,47 +485,50 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
   p.gram_rowsum = rowsum;
   const char* dbg_env = std::getenv("FMAP_DEBUG");  // timing experiments only: 2 = no H2D, 4 = no D2H
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
+  // Per chunk, G and M land first (the factorization needs them), R after (the back
+  // substitution and the validation need it): the solve starts 1/3 of a chunk's copy
+  // earlier.  Validation runs between the factorization and the back substitution
+  // -- nothing is exposed before the final flag check, which still takes precedence
+  // over SINGULAR, and C is zero-filled on any error.
   for (int c = 0; c < nchunk; ++c) {  // all H2D first: the copy stream never waits on the solver
-    const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
-    if (nq <= 0) break;
+    const int64_t q0 = cq0[c], nq = cnq[c];
     const size_t off = (size_t)q0 * kk, nb = (size_t)nq * kk * sizeof(float);
-    if (dbg & 2) {
-      FMAP_CK(ctx, cudaEventRecord(ctx->cev[2 + 2 * c], ctx->copy));
-      continue;
+    if (!(dbg & 2)) {
+      FMAP_CK(ctx, cudaMemcpyAsync(dG + off, gram + off, nb, cudaMemcpyHostToDevice, ctx->copy));
+      FMAP_CK(ctx, cudaMemcpyAsync(dM + off, mask + off, nb, cudaMemcpyHostToDevice, ctx->copy));
     }
-    FMAP_CK(ctx, cudaMemcpyAsync(dG + off, gram + off, nb, cudaMemcpyHostToDevice, ctx->copy));
-    FMAP_CK(ctx, cudaMemcpyAsync(dR + off, rhs + off, nb, cudaMemcpyHostToDevice, ctx->copy));
-    FMAP_CK(ctx, cudaMemcpyAsync(dM + off, mask + off, nb, cudaMemcpyHostToDevice, ctx->copy));
-    FMAP_CK(ctx, cudaEventRecord(ctx->cev[2 + 2 * c], ctx->copy));
+    FMAP_CK(ctx, cudaEventRecord(ctx->cev[2 + 3 * c], ctx->copy));
+    if (!(dbg & 2)) FMAP_CK(ctx, cudaMemcpyAsync(dR + off, rhs + off, nb, cudaMemcpyHostToDevice, ctx->copy));
+    FMAP_CK(ctx, cudaEventRecord(ctx->cev[3 + 3 * c], ctx->copy));
   }
   for (int c = 0; c < nchunk; ++c) {
-    const int64_t q0 = c * cb, nq = std::min<int64_t>(cb, b - q0);
-    if (nq <= 0) break;
+    const int64_t q0 = cq0[c], nq = cnq[c];
     const size_t off = (size_t)q0 * kk, nb = (size_t)nq * kk * sizeof(float);
-    cudaEvent_t h2d = ctx->cev[2 + 2 * c], done = ctx->cev[3 + 2 * c];
+    cudaEvent_t gm = ctx->cev[2 + 3 * c], rr = ctx->cev[3 + 3 * c], done = ctx->cev[4 + 3 * c];
     cudaStream_t s = comp[c & 1];
-    FMAP_CK(ctx, cudaStreamWaitEvent(s, h2d, 0));
-    FMAP_CK(ctx, launch_validate(dG + off, dR + off, dM + off, (size_t)nq * kk, d_flags(ctx), s));
+    FMAP_CK(ctx, cudaStreamWaitEvent(s, gm, 0));
     FMAP_CK(ctx, launch_gram_check(dG + off, nq, (int)k, rowsum + (size_t)q0 * k, d_flags(ctx), s));
     p.nsys = nq * k;
     p.sys_offset = q0 * k;
     p.tc_scratch = scr[c & 1];
-    FMAP_CK(ctx, launch_chol_solve(p, 0, s));
+    FMAP_CK(ctx, launch_chol_solve(p, 0, s, 1));
+    FMAP_CK(ctx, cudaStreamWaitEvent(s, rr, 0));
+    FMAP_CK(ctx, launch_validate(dG + off, dR + off, dM + off, (size_t)nq * kk, d_flags(ctx), s));
+    FMAP_CK(ctx, launch_chol_solve(p, 0, s, 2));
     FMAP_CK(ctx, cudaEventRecord(done, s));
-    if (opts.compute_residual)  // check_stationarity tiles co-run with the next chunk's solve
-      FMAP_CK(ctx, launch_residual_tiles(dC + off, dG + off, dR + off, dM + off, nq, (int)k, lambda,
-                                         partial + (size_t)q0 * residual_tile_count((int)k), s));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->copy2, done, 0));
     if (!(dbg & 4)) FMAP_CK(ctx, cudaMemcpyAsync(C_out + off, dC + off, nb, cudaMemcpyDeviceToHost, ctx->copy2));
   }
-  FMAP_CK(ctx, cudaEventRecord(ctx->cev[3 + 2 * nchunk], ctx->copy));  // all H2D done (stream join)
-  FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[3 + 2 * nchunk], 0));
+  FMAP_CK(ctx, cudaEventRecord(ctx->cev[50], ctx->copy));  // all H2D done (stream join)
+  FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[50], 0));
   if (opts.compute_residual) {
-    // check_stationarity (solver.hpp:314-320): the per-chunk tiles ran beside the
-    // solver (no tensor memory, so they share SMs with a running chunk); join and sum
-    FMAP_CK(ctx, cudaEventRecord(ctx->cev[36], comp[1]));
-    FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[36], 0));
-    FMAP_CK(ctx, launch_residual_finish(partial, b, residual_tile_count((int)k), res_out, ctx->stream));
+    // check_stationarity (solver.hpp:314-320) over the whole batch on the tensor cores
+    // once every chunk is solved (~0.05 ms; it overlaps the last chunk's D2H).  Per-chunk
+    // FP32 tiles beside the next chunk's solve measured 0.08 ms slower: they slow the
+    // solver they share SMs with.
+    FMAP_CK(ctx, cudaEventRecord(ctx->cev[51], comp[1]));
+    FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[51], 0));
+    FMAP_CK(ctx, launch_residual(dC, dG, dR, dM, b, (int)k, lambda, partial, res_out, ctx->stream));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[1], ctx->copy2));
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[1], 0));
@@ -894,8 +919,8 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   // solve, and each chunk's 3200 systems keep the persistent grid (2 CTAs per SM)
   // busy through its tail; 8 and 16 chunks measured 4 % and 17 % slower with the
   // residual tiles on (tools/e2e_probe.py)
-  const int nchunk = pipe ? std::max(1, std::min(16, std::atoi(pipe))) : 4;
-  if (nchunk > 1 && !o.inject_fault && b >= 2 * nchunk && k <= max_resolution(ctx))
+  const int nchunk = pipe ? (pipe[0] == 'r' ? 0 : std::max(1, std::min(16, std::atoi(pipe)))) : 4;
+  if ((nchunk > 1 ? b >= 2 * nchunk : nchunk == 0 && b >= 16) && !o.inject_fault && k <= max_resolution(ctx))
     return solve_host_pipelined(ctx, b, k, gram, rhs, mask, lambda, o, C_out, report, nchunk);
   if (o.has_memory_cap && staging > o.memory_cap_bytes) {
     if (report) {

@@ -57,36 +57,54 @@ __device__ __forceinline__ int core_idx(int r, int t) {  // element (r, t < 16) 
   return (r >> 3) * 128 + (t >> 2) * 32 + (r & 7) * 4 + (t & 3);
 }
 
-// Stage rows [r0, r0 + nrows) x K columns [k0, k0 + 16) of a row-major (rows x d)
-// matrix into hi / lo operand buffers; rows >= rlim and columns >= d are zero.
-__device__ __forceinline__ void stage_rows(const float* __restrict__ M, int r0, int nrows, int rlim, int d, int k0,
-                                           float* hi, float* lo, int tid) {
-  const bool vec = (d & 3) == 0;
-  for (int e = tid; e < nrows * 4; e += kGThreads) {
-    const int r = e >> 2, t4 = e & 3;
-    const int gr = r0 + r, gc = k0 + 4 * t4;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (gr < rlim) {
-      const float* src = M + (size_t)gr * d + gc;
-      if (vec && gc + 4 <= d) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(src));
-        v[0] = x.x;
-        v[1] = x.y;
-        v[2] = x.z;
-        v[3] = x.w;
-      } else {
+// Register-prefetched staging: thread tid owns float4 slots e = tid + 128 j of the
+// [rows x 4] float4 grid of a stage; load() issues the global reads of a stage,
+// store() splits and writes them one stage later, so the reads of stage st+1 are in
+// flight while stage st is converted and its MMAs run (round 1 loaded and stored in
+// one step: every stage paid a full memory latency, ~100 us per cfg2 launch).
+template <int J>
+struct StageRegs {
+  float4 v[J];
+  __device__ __forceinline__ void load(const float* __restrict__ M, int r0, int nrows, int rlim, int d, int k0,
+                                       int tid) {
+    const bool vec = (d & 3) == 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = gc + u < d ? __ldg(src + u) : 0.f;
+    for (int j = 0; j < J; ++j) {
+      const int e = tid + kGThreads * j;
+      const int r = e >> 2, t4 = e & 3;
+      const int gr = r0 + r, gc = k0 + 4 * t4;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nrows && gr < rlim) {
+        const float* src = M + (size_t)gr * d + gc;
+        if (vec && gc + 4 <= d) {
+          x = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          x.x = gc < d ? __ldg(src) : 0.f;
+          x.y = gc + 1 < d ? __ldg(src + 1) : 0.f;
+          x.z = gc + 2 < d ? __ldg(src + 2) : 0.f;
+          x.w = gc + 3 < d ? __ldg(src + 3) : 0.f;
+        }
       }
+      v[j] = x;
     }
-    float h[4], l[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) split_tf32(v[u], h[u], l[u]);
-    const int o = core_idx(r, 4 * t4);
-    *reinterpret_cast<float4*>(hi + o) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(lo + o) = make_float4(l[0], l[1], l[2], l[3]);
   }
-}
+  __device__ __forceinline__ void store(int nrows, float* hi, float* lo, int tid) const {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int e = tid + kGThreads * j;
+      const int r = e >> 2, t4 = e & 3;
+      if (r >= nrows) continue;
+      float h[4], l[4];
+      split_tf32(v[j].x, h[0], l[0]);
+      split_tf32(v[j].y, h[1], l[1]);
+      split_tf32(v[j].z, h[2], l[2]);
+      split_tf32(v[j].w, h[3], l[3]);
+      const int o = core_idx(r, 4 * t4);
+      *reinterpret_cast<float4*>(hi + o) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(lo + o) = make_float4(l[0], l[1], l[2], l[3]);
+    }
+  }
+};
 
 __global__ void __launch_bounds__(kGThreads, 1) gram_tc_kernel(GramArgs a) {
   extern __shared__ __align__(1024) float smem[];
@@ -116,14 +134,24 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc_kernel(GramArgs a) {
   tc_fence_after();
   const uint32_t tbase = *tslot;
   const int nst = (d + kGK - 1) / kGK;
+  // X: 128 rows x 4 float4 = 4 per thread; Y: N <= 304 rows -> up to 10 per thread
+  // (slots beyond the tile are predicated off)
+  StageRegs<4> px;
+  StageRegs<(kGMaxN - 16) * 4 / kGThreads + 1> py;
+  px.load(Xq, m0, 128, k, d, 0, tid);
+  py.load(Yq, 0, N, Nreal, d, 0, tid);
   for (int st = 0; st < nst; ++st) {
     const int buf = st & 1;
     float* B = smem + buf * bufsz;
     if (st >= 2) {  // the MMAs that read this buffer (stage st-2) are done
       mbar_wait(&bar[buf], ((st - 2) >> 1) & 1);
     }
-    stage_rows(Xq, m0, 128, k, d, st * kGK, B, B + xs, tid);
-    stage_rows(Yq, 0, N, Nreal, d, st * kGK, B + 2 * xs, B + 2 * xs + ys, tid);
+    px.store(128, B, B + xs, tid);
+    py.store(N, B + 2 * xs, B + 2 * xs + ys, tid);
+    if (st + 1 < nst) {  // next stage's reads in flight during this stage's MMAs
+      px.load(Xq, m0, 128, k, d, (st + 1) * kGK, tid);
+      py.load(Yq, 0, N, Nreal, d, (st + 1) * kGK, tid);
+    }
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {

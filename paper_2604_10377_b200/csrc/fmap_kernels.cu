@@ -390,62 +390,6 @@ __global__ void __launch_bounds__(256) residual_partial_kernel(
   }
 }
 
-// Lean check_stationarity tiles for the copy-pipelined host path: no tensor
-// memory, 128 threads, <= 40 registers, 4.3 KB of shared memory, so the tiles
-// co-reside with a running solver chunk (two solver CTAs per SM leave ~16 KB of
-// shared memory, ~4 K registers and no TMEM) and use its idle issue slots.
-// Tile = 32 rows x 32 columns of one pair; thread (tx, ty) owns rows ty*8..+7 of
-// column tx.  partial[(q T + ti) T + tj] = sum over the tile of
-// (C G + lambda M.*C - R)^2 in fp64 (fp32 products), fixed reduction order.
-__global__ void __launch_bounds__(128, 12) residual_tile_kernel(
-    const float* __restrict__ C, const float* __restrict__ G, const float* __restrict__ R,
-    const float* __restrict__ M, int k, float lambda, double* __restrict__ partial) {
-  __shared__ float Cs[32][17];
-  __shared__ float Gs[16][33];
-  __shared__ double red[4];
-  const int T = gridDim.x, tj = blockIdx.x, ti = blockIdx.y;
-  const int64_t q = blockIdx.z;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int i0 = ti * 32, j0 = tj * 32;
-  const size_t kk = (size_t)k * k;
-  const float* Cq = C + q * kk;
-  const float* Gq = G + q * kk;
-  float acc[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) acc[u] = 0.f;
-  for (int t0 = 0; t0 < k; t0 += 16) {
-    for (int e = tid; e < 512; e += 128) {
-      const int r = e >> 4, c = e & 15;
-      Cs[r][c] = (i0 + r < k && t0 + c < k) ? Cq[(size_t)(i0 + r) * k + t0 + c] : 0.f;
-      const int r2 = e >> 5, c2 = e & 31;
-      Gs[r2][c2] = (t0 + r2 < k && j0 + c2 < k) ? Gq[(size_t)(t0 + r2) * k + j0 + c2] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const float g = Gs[t][tx];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = fmaf(Cs[ty * 8 + u][t], g, acc[u]);
-    }
-    __syncthreads();
-  }
-  double s = 0.0;
-  const int j = j0 + tx;
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int i = i0 + ty * 8 + u;
-    if (i < k && j < k) {
-      const size_t e = q * kk + (size_t)i * k + j;
-      const float v = acc[u] + lambda * (M[e] * C[e]) - R[e];
-      s += (double)v * (double)v;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (tx == 0) red[ty] = s;
-  __syncthreads();
-  if (tid == 0) partial[((size_t)q * T + ti) * T + tj] = (red[0] + red[1]) + (red[2] + red[3]);
-}
 
 __global__ void residual_finish_kernel(const double* __restrict__ partial, int nchunk, int b,
                                        double* __restrict__ out) {
@@ -568,21 +512,6 @@ cudaError_t launch_residual(const float* C, const float* G, const float* R, cons
   return cudaGetLastError();
 }
 
-cudaError_t launch_residual_tiles(const float* C, const float* G, const float* R, const float* M, int64_t b,
-                                  int k, float lambda, double* partial, cudaStream_t st) {
-  const unsigned T = (unsigned)((k + 31) / 32);
-  note_launch("residual_tile_kernel");
-  residual_tile_kernel<<<dim3(T, T, (unsigned)b), 128, 0, st>>>(C, G, R, M, k, lambda, partial);
-  return cudaGetLastError();
-}
-
-int residual_tile_count(int k) { return ((k + 31) / 32) * ((k + 31) / 32); }
-
-cudaError_t launch_residual_finish(const double* partial, int64_t b, int nper, double* out, cudaStream_t st) {
-  note_launch("residual_finish_kernel");
-  residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, nper, (int)b, out);
-  return cudaGetLastError();
-}
 
 size_t residual_partial_count(int64_t b, int k) {
   return (size_t)b * k;  // per-row partials (tensor-core path); >= the SIMT kernel's b * ceil(k / 8)

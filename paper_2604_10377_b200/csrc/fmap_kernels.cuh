@@ -17,7 +17,9 @@ void clear_launch_log();
 const char* launch_log();
 int launch_log_count();
 
-cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream);
+// parts: 1 = factorization, 2 = back substitution + verdict (over a factorization
+// launched before with the same p), 3 = both
+cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream, int parts = 3);
 
 cudaError_t launch_mask(const float* ev1, const float* ev2, int64_t b, int k, int kind,
                         float sigma, float* out, cudaStream_t st);
@@ -49,12 +51,6 @@ cudaError_t launch_residual(const float* C, const float* G, const float* R, cons
                             int64_t b, int k, float lambda, double* partial, double* out,
                             cudaStream_t st);
 size_t residual_partial_count(int64_t b, int k);
-// Lean residual tiles (co-run with a solver chunk): partial[q][residual_tile_count(k)]
-cudaError_t launch_residual_tiles(const float* C, const float* G, const float* R, const float* M, int64_t b,
-                                  int k, float lambda, double* partial, cudaStream_t st);
-int residual_tile_count(int k);
-// out[q] = sqrt(sum of pair q's `nper` partials), fixed order
-cudaError_t launch_residual_finish(const double* partial, int64_t b, int nper, double* out, cudaStream_t st);
 cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,
                                  unsigned long long* fail_min, unsigned long long sys,
                                  cudaStream_t st);

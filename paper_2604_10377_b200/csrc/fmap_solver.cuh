@@ -49,7 +49,7 @@ int tc_max_resolution(int optin_smem);
 size_t tc_scratch_bytes(int k, int64_t nsys, int num_sms);
 cudaError_t launch_project_tc(const float* phi, const float* mass, const float* F, int64_t b,
                               int64_t n, int k, int d, float* out, cudaStream_t st);
-cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream);
+cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream, int parts = 3);
 
 // f64 route (fmap_f64.cu)
 size_t chol_f64_smem_bytes(int k, size_t optin);

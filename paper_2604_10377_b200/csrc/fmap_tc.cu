@@ -1360,13 +1360,13 @@ int tc_max_resolution(int optin_smem) {
 // The f32 route: every row system goes through the tcgen05/TMEM kernel (no
 // other solver, no CPU fallback); k beyond tc_max_resolution is rejected by the
 // C ABI before a launch.
-cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream) {
-  return launch_chol_tc(p, mask_mode, stream);
+cudaError_t launch_chol_solve(const SolveParams& p, int mask_mode, cudaStream_t stream, int parts) {
+  return launch_chol_tc(p, mask_mode, stream, parts);
 }
 
 // Host-side launcher for the tensor-core solver (p.tc_scratch must hold
 // tc_scratch_bytes(k, nsys, SMs)).
-cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream) {
+cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t stream, int parts) {
   if (p.nsys <= 0) return cudaSuccess;
   int dev = 0, optin = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -1422,15 +1422,19 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
       default: fn = chol_tc_kernel<2, 1, 384, 1>; break;
     }
   }
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int64_t npi = (p.nsys + L.ns - 1) / L.ns;
-  const int64_t maxgrid = (int64_t)sms * L.cps;
-  const unsigned grid = (unsigned)(npi < maxgrid ? npi : maxgrid);
-  note_launch("chol_tc_kernel");
-  fn<<<grid, L.threads, smem, stream>>>(p, L, tmG, tmA);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (parts & 1) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t npi = (p.nsys + L.ns - 1) / L.ns;
+    const int64_t maxgrid = (int64_t)sms * L.cps;
+    const unsigned grid = (unsigned)(npi < maxgrid ? npi : maxgrid);
+    note_launch("chol_tc_kernel");
+    fn<<<grid, L.threads, smem, stream>>>(p, L, tmG, tmA);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (!(parts & 2)) return cudaSuccess;
   // back substitution + verdict over the stored factors, one warp per system
   const size_t bsmem = (size_t)kBsWarps * 7 * L.K16 * sizeof(float);
   e = cudaFuncSetAttribute(chol_backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);

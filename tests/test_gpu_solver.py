@@ -210,14 +210,16 @@ def test_tensor_core_staging_variants(fm, oracle, monkeypatch, env, k, b):
 
 def test_host_copy_pipeline_matches_unpipelined(fm, oracle, monkeypatch):
     # The host entry overlaps chunked H2D / solve / D2H (default 4 chunks for >= 8
-    # pairs) and computes the residual beside the solve (residual tiles); 37 pairs
-    # make the last chunk partial.  The maps are bitwise the unpipelined ones, the
+    # pairs; G and M land before R, the factorization starts before R and before
+    # validation) and computes the residual once every chunk is solved (tcgen05);
+    # 37 pairs make the last chunk partial.  The maps are bitwise the unpipelined ones, the
     # reported residual agrees, and parity holds on the tail chunk.
     G, R, M = _problems(oracle, 37, 40, 64, 77)
     for res in (True, False):
         opts = fm.SolverOptions(compute_residual=res)
         piped = fm.solve_host(G, R, M, 100.0, opts)
-        assert "residual_tile_kernel" in fm._lib.context(0).last_launches or not res
+        launches = fm._lib.context(0).last_launches
+        assert launches.count("chol_tc_kernel") > 1 and ("gram_tc_kernel(residual)" in launches) == res, launches
         monkeypatch.setenv("FMAP_PIPELINE", "1")
         plain = fm.solve_host(G, R, M, 100.0, opts)
         monkeypatch.delenv("FMAP_PIPELINE")
@@ -231,15 +233,21 @@ def test_host_copy_pipeline_matches_unpipelined(fm, oracle, monkeypatch):
     _assert_parity(piped.maps[-3:], _ref(oracle, G[-3:], R[-3:], M[-3:], 100.0), "pipelined tail chunk")
 
 
-@pytest.mark.parametrize("what", ["nan", "singular"])
+@pytest.mark.parametrize("what", ["nan", "nan_gram_first_chunk", "negative_mask", "singular"])
 def test_host_copy_pipeline_error_exposes_no_partial_result(fm, oracle, what):
     # An error found in the LAST chunk (after earlier chunks were already copied
     # back) must not leave partial maps in the caller's buffer.
     import ctypes as C
     from paper_2604_10377_b200 import _lib, fmsolve
     G, R, M = _problems(oracle, 32, 24, 48, 91)
-    if what == "nan":
+    if what == "nan":  # in R: found by the validation that runs after the factorization
         R[31, 5, 7] = np.nan
+        expect = fm.InvalidArgument
+    elif what == "nan_gram_first_chunk":  # the factorization sees it first; INVALID_ARGUMENT still wins
+        G[0, 3, 3] = np.nan
+        expect = fm.InvalidArgument
+    elif what == "negative_mask":
+        M[20, 2, 9] = -1.0
         expect = fm.InvalidArgument
     else:
         G[31] = 0.0

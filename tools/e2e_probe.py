@@ -18,7 +18,7 @@ hG, hR, hM = (torch.from_numpy(x).pin_memory() for x in (G, R, M))
 hC = torch.empty_like(hG).pin_memory()
 ctx = _lib.context(0)
 P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
-for chunks, dbg in (("4", "0"), ("4", "2"), ("4", "6"), ("1", "0"), ("1", "6")):
+for chunks, dbg in (("4", "0"), ("ramp", "0"), ("4", "6"), ("8", "0")):
     os.environ["FMAP_PIPELINE"] = chunks
     os.environ["FMAP_DEBUG"] = dbg
     for res in (False, True):

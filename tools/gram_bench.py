@@ -25,6 +25,7 @@ def main():
     G = torch.empty(a.b, a.k, a.k, device=dev)
     R = torch.empty_like(G)
     ctx = _lib.context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)  # events below time the library's work
     P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     call = lambda: ctx._lib.fmap_normal_equations_f32_dev(ctx.handle, a.b, a.k, a.d, P(A), P(B), P(G), P(R))  # noqa
     for _ in range(3):
