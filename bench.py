@@ -309,8 +309,9 @@ def run_ours(args):
                          "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes,
                          "ms_per_step": round(e2e_ms, 4),
                          "api": "fmap_solve_f32 with DEFAULT options (compute_residual=1, as the reference always "
-                                "reports max_residual_norm): host G,R,M pinned -> C, 4 pair chunks, H2D / "
-                                "validation+solve+residual / D2H overlapped on 2 copy + 2 compute streams"
+                                "reports max_residual_norm): host G,R,M pinned -> C, 4 pair chunks (2:5:6:3), "
+                                "H2D (G,M then R) / factorization, validation, back substitution / D2H "
+                                "overlapped on 2 copy + 2 compute streams, residual on tcgen05 after the last chunk"
                                 + ("; per rank on its pair range, max over ranks (no host-side gather)"
                                    if world > 1 else "")}
         result["pipeline"] = {"value": round(gb / (pipe_ms * 1e-3), 2), "unit": UNIT,

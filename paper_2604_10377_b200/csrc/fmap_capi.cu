@@ -406,13 +406,26 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
                          fmap_report* rep, int nchunk) {
   const size_t kk = (size_t)k * k;
   const size_t bytes = (size_t)b * kk * sizeof(float);
-  // chunk boundaries: nchunk > 0 -> equal chunks; 0 -> ramp (2,3,3,3,3,2 sixteenths:
-  // a smaller first H2D and last D2H, the only copies not hidden behind a solve)
+  // chunk boundaries: nchunk > 0 -> equal chunks; 0 -> weighted 2,5,6,3 sixteenths of
+  // the batch (b = 64: 8, 20, 24, 12 pairs): the first chunk's G + M copy and the last
+  // chunk's D2H are the only copies not hidden behind a solve, so those chunks are
+  // small, while every extra chunk boundary costs ~30 us of solver tail
+  // (tools/e2e_probe.py at cfg2: 2.19 ms vs 2.23 ms for 4 equal chunks, 2.27 for 6)
   std::vector<int64_t> cq0, cnq;
   if (nchunk <= 0) {
-    static const int cum[7] = {0, 2, 5, 8, 11, 14, 16};
-    for (int c = 0; c < 6; ++c) {
-      const int64_t lo = b * cum[c] / 16, hi = b * cum[c + 1] / 16;
+    int cum[17] = {0, 2, 7, 13, 16};
+    int nw = 4;
+    if (const char* w = std::getenv("FMAP_PIPELINE_W")) {  // experiments: weights "2,5,5,4" (sum 16)
+      nw = 0;
+      for (const char* c = w; *c && nw < 16;) {
+        cum[nw + 1] = cum[nw] + std::atoi(c);
+        ++nw;
+        while (*c && *c != ',') ++c;
+        if (*c == ',') ++c;
+      }
+    }
+    for (int c = 0; c < nw; ++c) {
+      const int64_t lo = b * cum[c] / cum[nw], hi = b * cum[c + 1] / cum[nw];
       if (hi > lo) {
         cq0.push_back(lo);
         cnq.push_back(hi - lo);
@@ -915,11 +928,10 @@ int fmap_solve_f32(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram, const
   // pipelined copies (tensor-core solver, >= 2 pairs per chunk, no fault injection /
   // residual); FMAP_PIPELINE=<chunks> overrides the default (1 = unpipelined)
   const char* pipe = std::getenv("FMAP_PIPELINE");
-  // 4 chunks: the copies of one chunk (~7.7 MB) hide behind the previous chunk's
-  // solve, and each chunk's 3200 systems keep the persistent grid (2 CTAs per SM)
-  // busy through its tail; 8 and 16 chunks measured 4 % and 17 % slower with the
-  // residual tiles on (tools/e2e_probe.py)
-  const int nchunk = pipe ? (pipe[0] == 'r' ? 0 : std::max(1, std::min(16, std::atoi(pipe)))) : 4;
+  // default: 4 weighted chunks for b >= 16 (solve_host_pipelined), 4 equal chunks for
+  // 8 <= b < 16; FMAP_PIPELINE=<n> forces n equal chunks (8: 5 % slower at cfg2),
+  // FMAP_PIPELINE=r with FMAP_PIPELINE_W="w1,w2,..." other weights (experiments)
+  const int nchunk = pipe ? (pipe[0] == 'r' ? 0 : std::max(1, std::min(16, std::atoi(pipe)))) : (b >= 16 ? 0 : 4);
   if ((nchunk > 1 ? b >= 2 * nchunk : nchunk == 0 && b >= 16) && !o.inject_fault && k <= max_resolution(ctx))
     return solve_host_pipelined(ctx, b, k, gram, rhs, mask, lambda, o, C_out, report, nchunk);
   if (o.has_memory_cap && staging > o.memory_cap_bytes) {
