@@ -41,6 +41,7 @@ struct fmap_ctx {
   unsigned char* h_ctrl = nullptr;  // pinned
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   unsigned last_exact = 0;     // systems of the last call that ran the exact rcond estimator
+  double last_resmax = 0.0;    // max check_stationarity residual of the last call (control block)
   int64_t launches = 0;        // kernels launched by the last call
   std::string launch_names;    // their names, comma-separated (fmap_last_launches)
   int max_smem_optin = 0;
@@ -72,6 +73,8 @@ unsigned long long* d_fail(fmap_ctx* c) { return reinterpret_cast<unsigned long 
 unsigned* d_rcond(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 8); }
 unsigned* d_flags(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 12); }
 unsigned* d_nexact(fmap_ctx* c) { return reinterpret_cast<unsigned*>(c->d_ctrl + 16); }
+// max over pairs of the check_stationarity residual (fp64 bits; residuals are >= 0)
+unsigned long long* d_resmax(fmap_ctx* c) { return reinterpret_cast<unsigned long long*>(c->d_ctrl + 24); }
 
 // Grow-only device arena.  Growth drops the old contents (the stream is drained
 // first, so no queued kernel still reads it): callers reserve BEFORE carving.
@@ -136,19 +139,19 @@ size_t carve_size(std::initializer_list<size_t> bytes) {
 }
 
 int reset_ctrl(fmap_ctx* ctx) {
-  unsigned char init[24];
+  unsigned char init[32];
   const unsigned long long nf = kNoFail;
   const unsigned fmax = 0x7f7fffffu;  // FLT_MAX bits
   std::memset(init, 0, sizeof init);
   std::memcpy(init, &nf, 8);
   std::memcpy(init + 8, &fmax, 4);
-  std::memcpy(ctx->h_ctrl, init, 24);
-  FMAP_CK(ctx, cudaMemcpyAsync(ctx->d_ctrl, ctx->h_ctrl, 24, cudaMemcpyHostToDevice, ctx->stream));
+  std::memcpy(ctx->h_ctrl, init, 32);
+  FMAP_CK(ctx, cudaMemcpyAsync(ctx->d_ctrl, ctx->h_ctrl, 32, cudaMemcpyHostToDevice, ctx->stream));
   return FMAP_OK;
 }
 
 int read_ctrl(fmap_ctx* ctx, unsigned long long* fail, float* rcond, unsigned* flags) {
-  FMAP_CK(ctx, cudaMemcpyAsync(ctx->h_ctrl + 32, ctx->d_ctrl, 24, cudaMemcpyDeviceToHost,
+  FMAP_CK(ctx, cudaMemcpyAsync(ctx->h_ctrl + 32, ctx->d_ctrl, 32, cudaMemcpyDeviceToHost,
                                ctx->stream));
   FMAP_CK(ctx, cudaStreamSynchronize(ctx->stream));
   std::memcpy(fail, ctx->h_ctrl + 32, 8);
@@ -157,6 +160,7 @@ int read_ctrl(fmap_ctx* ctx, unsigned long long* fail, float* rcond, unsigned* f
   std::memcpy(rcond, &rb, 4);
   std::memcpy(flags, ctx->h_ctrl + 44, 4);
   std::memcpy(&ctx->last_exact, ctx->h_ctrl + 48, 4);
+  std::memcpy(&ctx->last_resmax, ctx->h_ctrl + 56, 8);
   return FMAP_OK;
 }
 
@@ -358,7 +362,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
                                ctx->stream));
       Muse = mask_scratch;
     }
-    FMAP_CK(ctx, launch_residual(C, G, R, Muse, b, (int)k, lambda, partial, res_out, ctx->stream));
+    FMAP_CK(ctx, launch_residual(C, G, R, Muse, b, (int)k, lambda, partial, res_out, ctx->stream, d_resmax(ctx)));
   }
 
   unsigned long long fail;
@@ -380,13 +384,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
                        " is numerically singular (Cholesky pivot / rcond estimate / non-finite "
                        "solution)");
   }
-  if (opts.compute_residual && rep) {
-    std::vector<double> res(b);
-    FMAP_CK(ctx, cudaMemcpy(res.data(), res_out, b * sizeof(double), cudaMemcpyDeviceToHost));
-    double mx = 0.0;
-    for (double v : res) mx = std::max(mx, v);
-    rep->max_residual = mx;
-  }
+  if (opts.compute_residual && rep) rep->max_residual = ctx->last_resmax;  // read with the control block
   ctx->last_error.clear();
   return FMAP_OK;
 }
@@ -541,7 +539,7 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
     // solver they share SMs with.
     FMAP_CK(ctx, cudaEventRecord(ctx->cev[51], comp[1]));
     FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[51], 0));
-    FMAP_CK(ctx, launch_residual(dC, dG, dR, dM, b, (int)k, lambda, partial, res_out, ctx->stream));
+    FMAP_CK(ctx, launch_residual(dC, dG, dR, dM, b, (int)k, lambda, partial, res_out, ctx->stream, d_resmax(ctx)));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->cev[1], ctx->copy2));
   FMAP_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->cev[1], 0));
@@ -565,13 +563,7 @@ int solve_host_pipelined(fmap_ctx* ctx, int64_t b, int64_t k, const float* gram,
                    "row system " + std::to_string(fail) +
                        " is numerically singular (Cholesky pivot / rcond estimate / non-finite solution)");
   }
-  if (opts.compute_residual && rep) {
-    std::vector<double> res(b);
-    FMAP_CK(ctx, cudaMemcpy(res.data(), res_out, b * sizeof(double), cudaMemcpyDeviceToHost));
-    double mx = 0.0;
-    for (double v : res) mx = std::max(mx, v);
-    rep->max_residual = mx;
-  }
+  if (opts.compute_residual && rep) rep->max_residual = ctx->last_resmax;  // read with the control block
   ctx->last_error.clear();
   return FMAP_OK;
 }

@@ -392,12 +392,15 @@ __global__ void __launch_bounds__(256) residual_partial_kernel(
 
 
 __global__ void residual_finish_kernel(const double* __restrict__ partial, int nchunk, int b,
-                                       double* __restrict__ out) {
+                                       double* __restrict__ out, unsigned long long* maxbits) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= b) return;
   double t = 0.0;
   for (int c = 0; c < nchunk; ++c) t += partial[(size_t)q * nchunk + c];
-  out[q] = sqrt(t);
+  const double r = sqrt(t);
+  out[q] = r;
+  // r >= 0: the bit patterns order like the values
+  if (maxbits) atomicMax(maxbits, (unsigned long long)__double_as_longlong(r));
 }
 
 // x' = x - z * (alpha * x_w) / (1 + alpha * z_w)  — the exact solution of the
@@ -494,7 +497,7 @@ cudaError_t launch_project(const float* phi, const float* mass, const float* F, 
 
 cudaError_t launch_residual(const float* C, const float* G, const float* R, const float* M,
                             int64_t b, int k, float lambda, double* partial, double* out,
-                            cudaStream_t st) {
+                            cudaStream_t st, unsigned long long* maxbits) {
   // C G on the tensor cores (3xTF32) with the mask / rhs terms and the squares in
   // the epilogue (per-row fp64 partials); FP32 SIMT kernel for shapes it does not serve
   int nchunk = k;
@@ -508,7 +511,7 @@ cudaError_t launch_residual(const float* C, const float* G, const float* R, cons
   }
   if (e != cudaSuccess) return e;
   note_launch("residual_finish_kernel");
-  residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, nchunk, (int)b, out);
+  residual_finish_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(partial, nchunk, (int)b, out, maxbits);
   return cudaGetLastError();
 }
 

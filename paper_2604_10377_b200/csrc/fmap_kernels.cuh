@@ -49,7 +49,8 @@ cudaError_t launch_project(const float* phi, const float* mass, const float* F, 
                            int64_t n, int k, int d, float* out, cudaStream_t st);
 cudaError_t launch_residual(const float* C, const float* G, const float* R, const float* M,
                             int64_t b, int k, float lambda, double* partial, double* out,
-                            cudaStream_t st);
+                            cudaStream_t st,
+                            unsigned long long* maxbits = nullptr);
 size_t residual_partial_count(int64_t b, int k);
 cudaError_t launch_fault_combine(float* x, const float* z, int k, int w, float alpha,
                                  unsigned long long* fail_min, unsigned long long sys,
