@@ -815,14 +815,13 @@ __global__ void __launch_bounds__(MAXT, MINB)
           }
         };
         if constexpr (NS == 1) {
-          diag_emit(a[0], own);
+          // factor a copy: the other half-warp's rows (this panel's TRSM rows when the
+          // block sits in lanes 0..15) keep their entries without a TMEM reload
+          float w[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) w[t] = a[0][t];
+          diag_emit(w, own);
           TC_TRACE(lane == 0 && pp < 16, 900 + 4 * pp + 2);
-          // the other half-warp's rows were clobbered by the factorization: reload
-          if (pp == 0) {
-            load_a0(0, a[0]);
-          } else {
-            tmem_ld16(tq + (uint32_t)j, a[0]);
-          }
         } else {
           float w[16];
 #pragma unroll
