@@ -774,6 +774,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
 #pragma unroll
       for (int gg = 0; gg < kMaxGroups; ++gg)
         if (gg < Ly.G && j >= Ly.lo[gg] && j < Ly.hi[gg]) dwarp = 4 * gg + ((j - Ly.lo[gg]) >> 5);
+      float dw[16], dinv = 0.f;  // (NS == 1) the diagonal warp's factored rows, for the packed store
+      bool dkeep = false;
       if (warp == dwarp) {
         TC_TRACE(lane == 0 && pp < 16, 900 + 4 * pp + 1);
         const bool upper = ((j - glo) & 31) != 0;         // diagonal rows in lanes 16..31
@@ -800,27 +802,31 @@ __global__ void __launch_bounds__(MAXT, MINB)
 #pragma unroll
             for (int t = 0; t < 16; ++t) LT[t * 16 + gr] = (t <= gr) ? w[t] : 0.f;  // transposed, for the TRSM
             LT[256 + gr] = iv;
-            bool vh = false;
+            if constexpr (NS == 1) {
+              dinv = iv;  // the packed copy is stored after this panel's arrival (below)
+            } else {
+              bool vh = false;
 #pragma unroll
-            for (int h = 0; h < NS; ++h)
-              if (h == hs) vh = vld[h];
-            if (vh) {  // packed copy for chol_backsub_kernel
-              float* L11s = L11st + (size_t)(NS * pi + hs) * P * 152 + pp * 152;
-              float* Lpk = L11s + gr * (gr + 1) / 2;
-              L11s[136 + gr] = iv;
+              for (int h = 0; h < NS; ++h)
+                if (h == hs) vh = vld[h];
+              if (vh) {  // packed copy for chol_backsub_kernel
+                float* L11s = L11st + (size_t)(NS * pi + hs) * P * 152 + pp * 152;
+                float* Lpk = L11s + gr * (gr + 1) / 2;
+                L11s[136 + gr] = iv;
 #pragma unroll
-              for (int t = 0; t < 16; ++t)
-                if (t <= gr) Lpk[t] = w[t];
+                for (int t = 0; t < 16; ++t)
+                  if (t <= gr) Lpk[t] = w[t];
+              }
             }
           }
         };
         if constexpr (NS == 1) {
           // factor a copy: the other half-warp's rows (this panel's TRSM rows when the
           // block sits in lanes 0..15) keep their entries without a TMEM reload
-          float w[16];
 #pragma unroll
-          for (int t = 0; t < 16; ++t) w[t] = a[0][t];
-          diag_emit(w, own);
+          for (int t = 0; t < 16; ++t) dw[t] = a[0][t];
+          diag_emit(dw, own);
+          dkeep = own;
           TC_TRACE(lane == 0 && pp < 16, 900 + 4 * pp + 2);
         } else {
           float w[16];
@@ -885,6 +891,15 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (lane == 0) {
         TC_TRACE(pp < 12 && warp < 8, 700 + 8 * pp + warp);
         mbar_arrive(&ops[grp]);  // operands of this panel stored
+      }
+      if (NS == 1 && dkeep && vld[0]) {  // packed diagonal block for chol_backsub_kernel, off the chain
+        const int gr = lane & 15;
+        float* L11s = L11st + (size_t)pi * P * 152 + pp * 152;
+        float* Lpk = L11s + gr * (gr + 1) / 2;
+        L11s[136 + gr] = dinv;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t <= gr) Lpk[t] = dw[t];
       }
       any_mma = true;
       if (has_next) {
