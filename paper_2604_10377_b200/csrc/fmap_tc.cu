@@ -857,17 +857,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
       }
       TC_TRACE(tid == 0 && pp < 16, 1120 + pp);
       TC_TRACE(lane == 0 && pp < 12 && warp < 8, 1200 + 8 * pp + warp);
-      // d. store L21: scratch (back substitution), operand hi/lo
+      // d. store L21: operand hi/lo (the fp32 copy for the back substitution after
+      //    the arrival, off the chain)
       if (trsm) {
-#pragma unroll
-        for (int h = 0; h < NS; ++h) {
-          if (!vld[h]) continue;
-          float4* dst = reinterpret_cast<float4*>(Lst + (size_t)(NS * pi + h) * Ly.lb + lb_off(pp, K16) +
-                                                  (size_t)(row - j - 16) * 16);
-#pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4)
-            __stcg(dst + c4, make_float4(l[h][4 * c4], l[h][4 * c4 + 1], l[h][4 * c4 + 2], l[h][4 * c4 + 3]));
-        }
         if (pp > 0) mbar_wait(rest, (g - 1) & 1);  // previous REST MMA done reading
         TC_TRACE(lane == 0 && pp < 12 && warp < 8, 1300 + 8 * pp + warp);
 #pragma unroll
@@ -891,6 +883,17 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (lane == 0) {
         TC_TRACE(pp < 12 && warp < 8, 700 + 8 * pp + warp);
         mbar_arrive(&ops[grp]);  // operands of this panel stored
+      }
+      if (trsm) {
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+          if (!vld[h]) continue;
+          float4* dst = reinterpret_cast<float4*>(Lst + (size_t)(NS * pi + h) * Ly.lb + lb_off(pp, K16) +
+                                                  (size_t)(row - j - 16) * 16);
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4)
+            __stcg(dst + c4, make_float4(l[h][4 * c4], l[h][4 * c4 + 1], l[h][4 * c4 + 2], l[h][4 * c4 + 3]));
+        }
       }
       if (NS == 1 && dkeep && vld[0]) {  // packed diagonal block for chol_backsub_kernel, off the chain
         const int gr = lane & 15;
