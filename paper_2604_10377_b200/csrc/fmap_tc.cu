@@ -70,14 +70,13 @@ struct TcLayout {
   int lo[kMaxGroups], hi[kMaxGroups], base[kMaxGroups];
   int ns;  // systems factored in lockstep per CTA (same row -> same thread)
   int tma; // next pair's G staged by TMA + tcgen05.cp during the current pair's panels
-  int nmain, bwarp, mwarp, threads, aug_tid;
+  int nmain, mwarp, threads;
   int tcols1;     // TMEM columns of one system
   int tmem_cols;  // allocated (ns * tcols1, power of two)
   int Rop;  // operand buffer rows
   int cps;  // CTAs per SM
   // offsets in floats from the dynamic smem base
-  int off_hi, off_lo, off_lt, off_l11, off_yv, off_xv, off_lb, off_zb, off_a0, off_stg, off_misc;
-  int off_uv, off_wv, off_hv;  // rcond (back-substitution warp): comparison solves u, w; Hager vectors
+  int off_hi, off_lo, off_lt, off_a0, off_stg, off_misc;
   int floats;
   long long lb;  // floats of one L scratch slot (global memory)
 };
@@ -114,9 +113,7 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.ns = ns;
   L.tmem_cols = ns * c;
   const int ntop = L.hi[L.G - 1] - L.lo[L.G - 1];
-  L.aug_tid = kTL * (L.G - 1) + ntop;
   L.nmain = 32 * (4 * (L.G - 1) + (ntop + 31) / 32);
-  L.bwarp = -1;                // back substitution: chol_backsub_kernel (own launch)
   L.mwarp = L.nmain / 32;      // MMA-issue warp
   L.threads = L.nmain + 32;
   L.Rop = L.K16 > kTL ? L.K16 : kTL;
@@ -124,14 +121,6 @@ __host__ inline TcLayout make_layout(int k, int ns = 0) {
   L.off_hi = o;  o += ns * L.Rop * 16;          // per system
   L.off_lo = o;  o += ns * L.Rop * 16;
   L.off_lt = o;  o += ns * (256 + 16);          // per system: diagonal block (transposed) + 1/L_tt
-  L.off_l11 = o;                                // (packed L_bb: per-system global store)
-  L.off_yv = o;                                 // (y = L^{-1} r: chol_backsub_kernel's forward pass)
-  L.off_xv = o;                                 // (back substitution: chol_backsub_kernel)
-  L.off_lb = o;
-  L.off_zb = o;
-  L.off_uv = o;
-  L.off_wv = o;
-  L.off_hv = o;
   o = (o + 31) & ~31;                           // 128 B aligned (TMA destination)
   L.off_a0 = o;  o += ns * L.K16 * 16;          // panel-0 columns of every row (float4 [h][t4][row])
   o = (o + 255) & ~255;                         // 1 KB aligned (TMA destination)
@@ -277,10 +266,10 @@ __device__ __forceinline__ void load_cols(const float* __restrict__ Gq, int k, i
 // CTA iteration n handles NS systems (sl = NS*pi + h) in lockstep: thread `row`
 // owns row `row` of every one of them (system h in TMEM columns h*tcols1 + ...,
 // its own operand buffers, L scratch and slot NS*(n&1)+h).  Main warps
-// (0..nmain/32-1): staging + blocked factorization; back-substitution warp
-// bwarp+h solves L^T x = y for system h of iteration n-1 meanwhile and writes the
-// row of C.  The 16x16 diagonal factor of system 1 runs on the half-warp that
-// does not hold the diagonal rows, so both blocks cost one dependency chain.
+// (0..nmain/32-1): staging + blocked factorization (the back substitution is
+// chol_backsub_kernel, over the stored factors).  The 16x16 diagonal factor of
+// system 1 runs on the half-warp that does not hold the diagonal rows, so both
+// blocks cost one dependency chain.
 // ---------------------------------------------------------------------------
 template <int MASK_MODE, int NS, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
@@ -427,16 +416,17 @@ __global__ void __launch_bounds__(MAXT, MINB)
           for (int gg = 0; gg < kMaxGroups; ++gg)
             if (gg < Ly.G && r0 >= Ly.lo[gg] && r0 < Ly.hi[gg]) gb = gg;
 #pragma unroll
-          for (int o = 0; o < kMaxGroups; ++o) {
-            const int gg = o == 0 ? gb : (o <= gb ? o - 1 : o);
-            if (gg >= Ly.G) continue;
-            mbar_wait(&ops[gg], gm & 1);
-            tc_fence_after();
-            if (Ly.hi[gg] > r0)
+          for (int pass = 0; pass < 2; ++pass)  // group gb, then the others (static indices)
 #pragma unroll
-              for (int h = 0; h < NS; ++h) mma3(h, Ly.lo[gg], Ly.base[gg], r0, 16);
-            mma_commit(&la[gg]);
-          }
+            for (int gg = 0; gg < kMaxGroups; ++gg) {
+              if (gg >= Ly.G || ((gg == gb) != (pass == 0))) continue;
+              mbar_wait(&ops[gg], gm & 1);
+              tc_fence_after();
+              if (Ly.hi[gg] > r0)
+#pragma unroll
+                for (int h = 0; h < NS; ++h) mma3(h, Ly.lo[gg], Ly.base[gg], r0, 16);
+              mma_commit(&la[gg]);
+            }
           TC_TRACE(pp < 16, 800 + pp);
           TC_TRACE(pp < 16, 820 + pp);
           // next pair: panel-0 columns (a0s is free: every main warp is past panel 0)
