@@ -11,7 +11,7 @@ ncu --set full --clock-control none --import-source on -k regex:chol_tc_kernel -
     python tools/prof_solver.py --reps 2 > gpurun_out/ncu_solver_$T.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:chol_backsub -s 1 -c 1 -o gpurun_out/backsub_$T -f \
     python tools/prof_solver.py --reps 2 > gpurun_out/ncu_backsub_$T.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:proj_tma -s 2 -c 1 -o gpurun_out/proj_$T -f \
+ncu --set full --clock-control none --import-source on -k regex:proj_pair -s 2 -c 1 -o gpurun_out/proj_$T -f \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_proj_$T.log 2>&1
 if [ -f paper_2604_10377_b200/libfmap_cuda_t.so ]; then
   FMAP_LIB_VARIANT=t FMAP_TRACE_FILE=gpurun_out/trace_$T.bin FMAP_TRACE_BLOCK=5 python tools/prof_solver.py --reps 2 > /dev/null 2>&1
