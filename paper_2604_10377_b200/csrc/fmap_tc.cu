@@ -1,43 +1,42 @@
 // Batched Cholesky solver with the trailing update on the 5th-generation tensor
 // cores (tcgen05, kind::tf32, 3xTF32 split) and the trailing matrix resident in
-// tensor memory (TMEM) — sm_100a.
-//
-// One CTA owns one row system at a time (persistent over systems, 2 CTAs per SM
-// for k <= 256):
+// tensor memory (TMEM) -- sm_100a.  For every shape pair q and row i:
 //     (G_q + lambda*diag(M_q[i,:]) + ridge*I) x = R_q[i,:]^T,   C_q[i,:] = x^T
 // replacing the reference's per-system PartialPivLU
 // (/root/reference/proj/include/fmsolve/solver.hpp:147-170) driven by
-// solve_batched_many (:220-322).  The system is SPD by construction.
+// solve_batched_many (:220-322), with the reference's rcond test (:164-168).
 //
-// Storage (K16 = k rounded up to 16; rows/cols k..K16-1 are identity padding):
-//   * tile A (TMEM): the LAST min(128, K16) rows, r = s + lane (s = K16 - 128 or
-//     0), all K16 columns (lane = row, TMEM column = matrix column).  The tensor
-//     core updates it in place: D[r][c] -= sum_t L[r][j+t] L[c][j+t].  Factored
-//     L values are written back into their own columns (never touched again).
-//   * top-left rows 0..s-1 (shared memory, packed lower triangle, fp32): these
-//     rows only have columns < s; their trailing update is SIMT.
-//   * operand buffers (shared memory): the current panel's L21 split into TF32
-//     hi/lo parts, K-major core-matrix layout (8 rows x 16 B per core matrix),
-//     used as BOTH the A operand (rows s..s+127) and the B operand (rows j+16..).
+// Two kernels per solve:
 //
-// Per 16-column panel p (j = 16 p), one CTA-wide pass:
-//   a  rows >= j load their 16 panel entries (TMEM ld / smem) after the
-//      lookahead MMA of panel p-1 has landed; lagged right-hand-side update.
-//   b  the warp holding rows j..j+15 factors the 16x16 diagonal block (lane per
-//      row, one shuffle per pivot on the critical chain).            | barrier
-//   c  every row >= j+16 solves its L21 row (TRSM against L11); the augmented
-//      right-hand-side "row" gives y = L^{-1} r for the panel.
-//   d  L rows -> TMEM (kept for the back substitution), hi/lo -> operand
-//      buffers; fence.proxy.async.                                  | barrier
-//   e  one thread issues the lookahead MMA (next panel's 16 columns) and the
-//      rest of the trailing update, each committed to its own mbarrier; the
-//      top-left rows run their SIMT trailing update meanwhile.
-// Back substitution L^T x = y in 16-row blocks from the bottom (diagonal blocks
-// inverted up front; per block one TMEM load, a warp reduction and a 16x16
-// mat-vec), then a coalesced write of the row of C.
+// chol_tc_kernel -- factorization.  One CTA owns one row system at a time
+// (persistent over systems; two CTAs per SM for K16 <= 208, K16 = k rounded up to
+// 16, rows/cols k..K16-1 identity padding).
+//   * TMEM: rows split into groups of <= 128 from the bottom; group g keeps rows
+//     [lo_g, hi_g) on TMEM lanes and matrix columns [16, hi_g) (panel 0's columns
+//     stay in shared memory).  k = 200: 192 + 64 = 256 columns per system.
+//   * Operand buffers (shared memory): the current panel's L21 rows split into
+//     TF32 hi/lo parts, K-major core matrices, used as both MMA operands.
+//   * Per 16-column panel p (j = 16 p):
+//       a  rows >= j load their 16 panel entries from TMEM once their group's
+//          lookahead MMA (panel p-1) has landed;
+//       b  the warp holding rows j..j+15 factors a copy of the 16x16 diagonal
+//          block (lane per row, shuffles) and publishes L11^T and 1/L_tt;  | barrier
+//       c  every row >= j+16 solves its L21 row against L11 (TRSM);
+//       d  hi/lo operands to shared memory, per-group "operands ready" arrival;
+//          then, off the chain, the fp32 L21 row and the packed diagonal block
+//          go to the per-system store for the back substitution;
+//       e  one MMA-issue thread: per row group (the group holding the next
+//          diagonal block first) the lookahead MMA (next panel's 16 columns),
+//          then the rest of the trailing update, each committed to an mbarrier;
+//          the next system's G is staged into dead TMEM columns by TMA +
+//          tcgen05.cp meanwhile.
+// chol_backsub_kernel -- one warp per system over the stored factor: forward
+// pass y = L^{-1} r with the rcond certificate's u = M(L)^{-1} e, backward pass
+// x = L^{-T} y with w = M(L)^{-T} e, the verdict (certificate, or the exact
+// Hager/Higham estimate on the rare systems it does not clear), the row of C.
 //
-// Singular = non-positive / non-finite pivot, rcond estimate min(pivot)/max|diag|
-// below the threshold, or a non-finite solution (lowest failing index wins).
+// Singular = non-positive / non-finite pivot, rcond below the threshold, or a
+// non-finite solution (the lowest failing system index wins).
 #include "fmap_kernels.cuh"
 #include "fmap_solver.cuh"
 #include "tc_ptx.cuh"
@@ -333,10 +332,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const uint32_t tbase = *tslot;
 
   // ======================= MMA-issue warp =======================
-  // Per panel: wait until every main warp has stored its L21 operands, release the
-  // panel's y to the main warps (ysync), then issue the tensor-core trailing update
-  // of every group of every system: lookahead (next panel's 16 columns, committed
-  // to LA) first, then the rest (REST).
+  // Per panel: per row group, wait until its warps have stored their L21 operands
+  // and issue its lookahead MMA (next panel's 16 columns, committed to la[g]), the
+  // group holding the next diagonal block first; then the rest of the trailing
+  // update of every group (REST).
   if (warp == Ly.mwarp) {
     if (lane == 0) {
       auto mma3 = [&](int h, int glo_, int gbase_, int c0, int N) {
@@ -574,7 +573,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
 
     // ---- staging: row r of (G + lambda*diag(m_i) + ridge*I), identity padding ----
     // Row r of G (read as column r, G[c][r]: coalesced; the lower triangle used is
-    // G's upper triangle, as the SIMT solver; G = A A^T is symmetric by
+    // G's upper triangle; G = A A^T is symmetric by
     // construction).  Columns 0..15 stay in registers (panel 0), the rest go to the
     // group's TMEM region.  Raw G first (prefetched during the previous pair's
     // panels, or loaded here for the first pair), then lambda*m + ridge is added to
@@ -963,11 +962,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
 // ---------------------------------------------------------------------------
 // Back substitution + singular verdict, one warp per system, after the
 // factorization kernel (chol_tc_kernel stores every system's L21 blocks, packed
-// diagonal blocks, y = L^{-1} r and its status; this kernel reads them from L2 /
-// HBM).  Running it as its own pass instead of inside the factorization kernel
-// keeps its ~8.5 K instructions per system off the SMs while the latency-bound
-// panel chains run (the factorization alone is 1.66 vs 2.26 ms at cfg2 with the
-// in-kernel back-substitution warp).
+// diagonal blocks and status; this kernel reads them from HBM and forms y itself).
+// Running it as its own pass instead of inside the factorization kernel keeps its
+// ~8.5 K instructions per system off the SMs while the latency-bound panel chains
+// run (2.27 -> 2.00 ms at cfg2 when it moved out).
 // ---------------------------------------------------------------------------
 constexpr int kBsWarps = 4;
 
