@@ -1414,11 +1414,11 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
         default: fn = chol_tc_kernel<2, 2, 384, 1>; break;
       }
     }
-  } else if (L.cps >= 2 && L.threads <= 288) {  // two CTAs per SM
+  } else if (L.cps >= 2 && L.threads <= 256) {  // two CTAs per SM: 16 warps, up to 128 registers
     switch (mask_mode) {
-      case 0: fn = chol_tc_kernel<0, 1, 288, 2>; break;
-      case 1: fn = chol_tc_kernel<1, 1, 288, 2>; break;
-      default: fn = chol_tc_kernel<2, 1, 288, 2>; break;
+      case 0: fn = chol_tc_kernel<0, 1, 256, 2>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 256, 2>; break;
+      default: fn = chol_tc_kernel<2, 1, 256, 2>; break;
     }
   } else {
     switch (mask_mode) {
