@@ -196,16 +196,32 @@ __device__ __forceinline__ void diag_factor(float (&a)[16], float& inv, int g, b
 // broadcast LDS.128 run); chain 16 x (FMUL + FFMA).  `a` is consumed.
 __device__ __forceinline__ void trsm_row(const float* __restrict__ LT, const float* __restrict__ inv,
                                          float (&a)[16], float (&l)[16]) {
+  // software-pipelined: column t+1 of LT (and 1/L_{t+1,t+1}) is loaded while step t
+  // runs, so the shared-memory latency stays off the 16-step FMUL + FFMA chain
+  float4 cur[4], nxt[4];
+  float ivc = inv[0], ivn = 0.f;
+#pragma unroll
+  for (int c4 = 0; c4 < 4; ++c4) cur[c4] = *reinterpret_cast<const float4*>(LT + 4 * c4);
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
-    l[t] = a[t] * inv[t];
+    if (t < 15) {
+      ivn = inv[t + 1];
+#pragma unroll
+      for (int c4 = (t + 2) >> 2; c4 < 4; ++c4) nxt[c4] = *reinterpret_cast<const float4*>(LT + (t + 1) * 16 + 4 * c4);
+    }
+    l[t] = a[t] * ivc;
 #pragma unroll
     for (int c4 = (t + 1) >> 2; c4 < 4; ++c4) {
-      const float4 col = *reinterpret_cast<const float4*>(LT + t * 16 + 4 * c4);
+      const float4 col = cur[c4];
       if (4 * c4 > t) a[4 * c4] = fmaf(-l[t], col.x, a[4 * c4]);
       if (4 * c4 + 1 > t) a[4 * c4 + 1] = fmaf(-l[t], col.y, a[4 * c4 + 1]);
       if (4 * c4 + 2 > t) a[4 * c4 + 2] = fmaf(-l[t], col.z, a[4 * c4 + 2]);
       if (4 * c4 + 3 > t) a[4 * c4 + 3] = fmaf(-l[t], col.w, a[4 * c4 + 3]);
+    }
+    if (t < 15) {
+#pragma unroll
+      for (int c4 = (t + 2) >> 2; c4 < 4; ++c4) cur[c4] = nxt[c4];
+      ivc = ivn;
     }
   }
 }
