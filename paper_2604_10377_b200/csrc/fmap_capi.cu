@@ -224,7 +224,8 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   const size_t tc_bytes = tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms);
   const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
                                      need_mask_scratch ? (size_t)b * kk * sizeof(float) : 0,
-                                     (size_t)k * sizeof(float), tc_bytes, (size_t)b * k * sizeof(float)});
+                                     (size_t)k * sizeof(float), tc_bytes, (size_t)b * k * sizeof(float),
+                                     mask_mode == 1 ? (size_t)b * sizeof(float) : 0});
   const uint64_t required = (uint64_t)scratch + host_staging_bytes;
   if (rep) rep->peak_extra_bytes = required;
   if (opts.has_memory_cap && required > opts.memory_cap_bytes) {
@@ -246,6 +247,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   float* zrow = cv.take<float>((size_t)k);
   float* tc_scr = cv.take<float>(tc_bytes / sizeof(float));
   float* rowsum = cv.take<float>((size_t)b * k);
+  float* evmax = cv.take<float>(mask_mode == 1 ? (size_t)b : 0);
 
   if ((st = reset_ctrl(ctx))) return st;
   if (device_validate) {
@@ -258,6 +260,9 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   }
   // symmetry check + row 1-norms of G (rcond certificate input)
   FMAP_CK(ctx, launch_gram_check(G, b, (int)k, rowsum, d_flags(ctx), ctx->stream));
+  // the resolvent mask's per-pair normaliser (masks.hpp:58-59), once per pair instead
+  // of once per row system inside the solver; an all-zero spectrum is flagged
+  if (mask_mode == 1) FMAP_CK(ctx, launch_ev_max_check(ev1, ev2, b, (int)k, d_flags(ctx), ctx->stream, evmax));
 
   SolveParams p{};
   p.gram = G;
@@ -265,6 +270,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   p.mask = M;
   p.ev1 = ev1;
   p.ev2 = ev2;
+  p.ev_max = evmax;
   p.C = C;
   p.k = (int)k;
   p.K4 = ((int)k + 3) & ~3;

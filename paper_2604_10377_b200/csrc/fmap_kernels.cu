@@ -120,14 +120,17 @@ __global__ void validate_ev_kernel(const float* __restrict__ e1, const float* __
 // all-zero spectrum is rejected (bit 5) instead of producing a NaN mask.  One
 // warp per pair.
 __global__ void ev_max_check_kernel(const float* __restrict__ e1, const float* __restrict__ e2, int64_t b,
-                                    int k, unsigned* flags) {
+                                    int k, unsigned* flags, float* __restrict__ out) {
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= b) return;
   float m = 0.f;
   for (int c = threadIdx.x & 31; c < k; c += 32)
     m = fmaxf(m, fmaxf(e1[(size_t)q * k + c], e2[(size_t)q * k + c]));
   m = warp_max(m);
-  if ((threadIdx.x & 31) == 0 && !(m > 0.f)) atomicOr(flags, 32u);
+  if ((threadIdx.x & 31) == 0) {
+    if (!(m > 0.f)) atomicOr(flags, 32u);
+    if (out) out[q] = m;  // the fused-mask solver's per-pair normaliser
+  }
 }
 
 // Per pair q, 32 rows per CTA: S[q][r] = sum_c |G[q][r][c]| (the row 1-norms the
@@ -445,9 +448,9 @@ cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsig
 }
 
 cudaError_t launch_ev_max_check(const float* e1, const float* e2, int64_t b, int k, unsigned* flags,
-                                cudaStream_t st) {
+                                cudaStream_t st, float* out) {
   note_launch("ev_max_check_kernel");
-  ev_max_check_kernel<<<(unsigned)((b + 7) / 8), 256, 0, st>>>(e1, e2, b, k, flags);
+  ev_max_check_kernel<<<(unsigned)((b + 7) / 8), 256, 0, st>>>(e1, e2, b, k, flags, out);
   return cudaGetLastError();
 }
 

@@ -28,7 +28,8 @@ cudaError_t launch_validate(const float* g, const float* r, const float* m, size
 cudaError_t launch_validate_ev(const float* e1, const float* e2, size_t n, unsigned* flags,
                                cudaStream_t st);
 cudaError_t launch_ev_max_check(const float* e1, const float* e2, int64_t b, int k, unsigned* flags,
-                                cudaStream_t st);
+                                cudaStream_t st,
+                                float* out = nullptr);
 cudaError_t launch_gram_check(const float* G, int64_t b, int k, float* S, unsigned* flags, cudaStream_t st);
 // tcgen05 3xTF32 normal equations (fmap_gram.cu): nprod <= 4 products
 // out_i[q] = X_i[q] Y_i[q]^T (k x d operands), sym_i = 1 for X_i == Y_i (mirrored).

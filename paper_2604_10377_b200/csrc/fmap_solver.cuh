@@ -19,6 +19,7 @@ struct SolveParams {
   const float* mask;  // [b][k][k]        (mask_mode == 0)
   const float* ev1;   // [b][k]           (mask_mode != 0)
   const float* ev2;   // [b][k]
+  const float* ev_max;  // [b] max(ev1, ev2) of each pair (mask_mode == 1)
   float* C;           // [b][k][k]
   int k;
   int K4;

@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   float4* a0s = reinterpret_cast<float4*>(smem + Ly.off_a0);  // panel-0 columns: [(h*4 + t4)*K16 + row]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Ly.off_misc + 48);
   unsigned* scb = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 56);  // [n&1][h][8]
-  // sc[8h+0] dmax bits, [1] pivmin bits, [2] bad, [3] ev_max bits, [4] ||A||_1 bits (current
+  // sc[8h+0] dmax bits, [1] pivmin bits, [2] bad, [3] (unused), [4] ||A||_1 bits (current
   // systems); double-buffered by iteration parity, reset right after the hand-off
   unsigned* slotsc = reinterpret_cast<unsigned*>(smem + Ly.off_misc + 88);  // [slot][8]
   // per-system store for chol_backsub_kernel (launch-local system sl): L21 blocks,
@@ -568,21 +568,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
       ev_max[h] = 0.f;
       skip[h] = !vld[h];
     }
-    if constexpr (MASK_MODE == 1) {
-      main_sync(NM);
+    if constexpr (MASK_MODE == 1) {  // the pair's normaliser max(ev1, ev2), from ev_max_check_kernel
 #pragma unroll
       for (int h = 0; h < NS; ++h) {
-        float m = 0.f;
-        for (int c = tid; c < k; c += NM)
-          m = fmaxf(m, fmaxf(p.ev1[(size_t)qs[h] * k + c], p.ev2[(size_t)qs[h] * k + c]));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-        if (lane == 0) atomicMax(&sc[8 * h + 3], __float_as_uint(m));
-      }
-      main_sync(NM);
-#pragma unroll
-      for (int h = 0; h < NS; ++h) {
-        ev_max[h] = __uint_as_float(sc[8 * h + 3]);
+        ev_max[h] = __ldg(p.ev_max + qs[h]);
         skip[h] = skip[h] || !(ev_max[h] > 0.f);
       }
     }
