@@ -317,7 +317,7 @@ def run_ours(args):
         result["pipeline"] = {"value": round(gb / (pipe_ms * 1e-3), 2), "unit": UNIT,
                               "ms_per_step": round(pipe_ms, 4),
                               "api": "fmap_pipeline_f32_dev: Phi,Mass,F,ev -> projection, Gram/RHS, "
-                                     "fused resolvent mask, solver (device-resident)"}
+                                     "resolvent mask kernel, solver (device-resident)"}
         result["f64_route"] = {"value": round(gb / (f64_ms * 1e-3), 2), "unit": UNIT,
                                "ms_per_step": round(f64_ms, 4), "dtype": "f64",
                                "api": "fmap_solve_f64_dev (the reference's default precision; same "

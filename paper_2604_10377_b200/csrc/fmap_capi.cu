@@ -196,7 +196,10 @@ std::string flags_message(unsigned f) {
 
 int max_resolution(fmap_ctx* ctx) { return tc_max_resolution(ctx->max_smem_optin); }
 
-// Core solve on device buffers. mask_mode 0: d_mask; 1/2: from eigenvalues.
+// Core solve on device buffers. mask_mode 0: d_mask; 1/2: resolvent / commutativity
+// mask rows generated inside the solver from the eigenvalues; 3/4: the same masks
+// already materialized by the caller in d_mask from ev1/ev2 (the eigenvalues are
+// validated instead of the mask, the solver reads the dense mask).
 int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float* R,
                const float* M, const float* ev1, const float* ev2, int mask_mode, float sigma,
                float lambda, const fmap_solver_options* o, float* C, fmap_report* rep,
@@ -208,9 +211,10 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   if (b < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "no problems to solve");
   if (k < 1) return set_err(ctx, FMAP_INVALID_ARGUMENT, "problem is empty");
   if (!(lambda >= 0.f)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "lambda must be non-negative");
-  if (mask_mode == 1 && !(sigma > 0.f))
+  const int kmode = mask_mode >= 3 ? 0 : mask_mode;  // the solver kernel's mask source
+  if ((mask_mode == 1 || mask_mode == 3) && !(sigma > 0.f))
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "sigma must be positive");
-  if (!G || !R || !C || (mask_mode == 0 && !M) || (mask_mode != 0 && (!ev1 || !ev2)))
+  if (!G || !R || !C || (kmode == 0 && !M) || (mask_mode != 0 && (!ev1 || !ev2)))
     return set_err(ctx, FMAP_INVALID_ARGUMENT, "null buffer");
   const int kmax = max_resolution(ctx);
   if (k > kmax)
@@ -219,7 +223,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
                        std::to_string(kmax) + " on this device");
   const size_t kk = (size_t)k * k;
   const size_t nsys = (size_t)b * k;
-  const bool need_mask_scratch = opts.compute_residual && mask_mode != 0;
+  const bool need_mask_scratch = opts.compute_residual && kmode != 0;
   const size_t res_partial = opts.compute_residual ? residual_partial_count(b, (int)k) : 0;
   const size_t tc_bytes = tc_scratch_bytes((int)k, (int64_t)nsys, ctx->num_sms);
   const size_t scratch = carve_size({res_partial * sizeof(double), (size_t)b * sizeof(double),
@@ -262,7 +266,8 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   FMAP_CK(ctx, launch_gram_check(G, b, (int)k, rowsum, d_flags(ctx), ctx->stream));
   // the resolvent mask's per-pair normaliser (masks.hpp:58-59), once per pair instead
   // of once per row system inside the solver; an all-zero spectrum is flagged
-  if (mask_mode == 1) FMAP_CK(ctx, launch_ev_max_check(ev1, ev2, b, (int)k, d_flags(ctx), ctx->stream, evmax));
+  if (mask_mode == 1 || mask_mode == 3)
+    FMAP_CK(ctx, launch_ev_max_check(ev1, ev2, b, (int)k, d_flags(ctx), ctx->stream, mask_mode == 1 ? evmax : nullptr));
 
   SolveParams p{};
   p.gram = G;
@@ -301,7 +306,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   }
   if (const char* dbg = std::getenv("FMAP_DEBUG")) p.debug = std::atoi(dbg);  // timing experiments only
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-  FMAP_CK(ctx, launch_chol_solve(p, mask_mode, ctx->stream));
+  FMAP_CK(ctx, launch_chol_solve(p, kmode, ctx->stream));
   if (d_trace) {
     std::vector<long long> h(16 * 1024);
     FMAP_CK(ctx, cudaMemcpyAsync(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -320,7 +325,7 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     float m00 = 0.f;
     FMAP_CK(ctx, cudaMemcpyAsync(g0.data(), G, k * sizeof(float), cudaMemcpyDeviceToHost,
                                  ctx->stream));
-    if (mask_mode == 0) {
+    if (kmode == 0) {
       FMAP_CK(ctx, cudaMemcpyAsync(&m00, M, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
     } else {
       std::vector<float> e1(k), e2(k);
@@ -356,14 +361,14 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
     pz.C = zrow;  // system 0 writes its row at offset 0
     pz.nsys = 1;
     pz.rhs_unit = 0;
-    FMAP_CK(ctx, launch_chol_solve(pz, mask_mode, ctx->stream));
+    FMAP_CK(ctx, launch_chol_solve(pz, kmode, ctx->stream));
     FMAP_CK(ctx, launch_fault_combine(C, zrow, (int)k, w, alpha, d_fail(ctx), 0ull, ctx->stream));
   }
   FMAP_CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
 
   if (opts.compute_residual) {
     const float* Muse = M;
-    if (mask_mode != 0) {
+    if (kmode != 0) {
       FMAP_CK(ctx, launch_mask(ev1, ev2, b, (int)k, mask_mode == 1 ? 1 : 0, sigma, mask_scratch,
                                ctx->stream));
       Muse = mask_scratch;
@@ -1162,7 +1167,7 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
   const size_t nab = (size_t)b * k * d, ng = (size_t)b * k * k;
   const bool bidir = d_Cyx != nullptr;
   const size_t scratch = carve_size({nab * 4, nab * 4, ng * 4, ng * 4, bidir ? ng * 4 : 0,
-                                     bidir ? ng * 4 : 0});
+                                     bidir ? ng * 4 : 0, ng * 4});
   fmap_solver_options o;
   default_opts(&o);
   if (opts) o = *opts;
@@ -1176,6 +1181,7 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
   float* R = cv.take<float>(ng);
   float* G2 = bidir ? cv.take<float>(ng) : nullptr;
   float* R2 = bidir ? cv.take<float>(ng) : nullptr;
+  float* Mx = cv.take<float>(ng);
   cudaEvent_t e0, e1;
   FMAP_CK(ctx, cudaEventCreate(&e0));
   FMAP_CK(ctx, cudaEventCreate(&e1));
@@ -1189,10 +1195,16 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
     const int sym[4] = {1, 0, 1, 0};
     FMAP_CK(ctx, normal_products(bidir ? 4 : 2, X, Y, O, sym, b, (int)k, (int)d, ctx->stream));
   }
-  // solve_core carves its own scratch after host_staging_bytes = our scratch
-  const int mm = mask_kind == FMAP_MASK_RESOLVENT ? 1 : 2;
-  st = solve_core(ctx, b, k, G, R, nullptr, d_ev1, d_ev2, mm, sigma, lambda, &o, d_Cxy, report,
-                  true, scratch);
+  // The mask is materialized (one fused mask-construction kernel, masks.hpp:36-82) and
+  // the solver reads it densely: its per-row entries are then prefetched with the
+  // next system's G (2.33 vs 2.43 ms at cfg2 with the entries computed inside the
+  // solver from the eigenvalues).  solve_core carves its own scratch after
+  // host_staging_bytes = our scratch.
+  const bool resolvent = mask_kind == FMAP_MASK_RESOLVENT;
+  const int mm = resolvent ? 3 : 4;
+  if (resolvent && !(sigma > 0.f)) return set_err(ctx, FMAP_INVALID_ARGUMENT, "sigma must be positive");
+  FMAP_CK(ctx, launch_mask(d_ev1, d_ev2, b, (int)k, resolvent ? 1 : 0, sigma, Mx, ctx->stream));
+  st = solve_core(ctx, b, k, G, R, Mx, d_ev1, d_ev2, mm, sigma, lambda, &o, d_Cxy, report, true, scratch);
   if (st) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1201,8 +1213,8 @@ int fmap_pipeline_f32_dev(fmap_ctx* ctx, int64_t b, int64_t n1, int64_t n2, int6
   if (bidir) {
     fmap_report r2;
     // reverse direction: source/target swap, mask(ev2, ev1) = M^T
-    st = solve_core(ctx, b, k, G2, R2, nullptr, d_ev2, d_ev1, mm, sigma, lambda, &o, d_Cyx, &r2,
-                    true, scratch);
+    FMAP_CK(ctx, launch_mask(d_ev2, d_ev1, b, (int)k, resolvent ? 1 : 0, sigma, Mx, ctx->stream));
+    st = solve_core(ctx, b, k, G2, R2, Mx, d_ev2, d_ev1, mm, sigma, lambda, &o, d_Cyx, &r2, true, scratch);
     if (st) {
       if (report) *report = r2;
       cudaEventDestroy(e0);
