@@ -750,16 +750,26 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (pp == 0) {
 #pragma unroll
         for (int h = 0; h < NS; ++h) load_a0(h, a[h]);
-      } else if (has_grp && ghi > j) {  // panel columns updated by the previous lookahead MMA
-        mbar_wait(&la[grp], (g - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int h = 0; h < NS; ++h) tmem_ld16(tq + tsys * h + (uint32_t)j, a[h]);
       } else {
+        // Every warp waits for its group's lookahead commit of the previous panel, also
+        // once its group has no rows left: that commit follows the MMA warp's wait on the
+        // group's "operands ready" barrier, so no group's arrivals can run two phases
+        // ahead of that wait (a finished group otherwise arrives right after each
+        // diagonal barrier, and the MMA warp, still in its second pass of the previous
+        // panel, would wait for a phase that needs the next one: a deadlock).
+        if (has_grp) {
+          mbar_wait(&la[grp], (g - 1) & 1);
+          tc_fence_after();
+        }
+        if (has_grp && ghi > j) {  // panel columns updated by the previous lookahead MMA
 #pragma unroll
-        for (int h = 0; h < NS; ++h)
+          for (int h = 0; h < NS; ++h) tmem_ld16(tq + tsys * h + (uint32_t)j, a[h]);
+        } else {
 #pragma unroll
-          for (int t = 0; t < 16; ++t) a[h][t] = 0.f;
+          for (int h = 0; h < NS; ++h)
+#pragma unroll
+            for (int t = 0; t < 16; ++t) a[h][t] = 0.f;
+        }
       }
       TC_TRACE(tid == 0, 2 + 4 * pp);
       // b. diagonal blocks (rows j..j+15 live in one half of one warp; the other
