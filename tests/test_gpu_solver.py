@@ -265,3 +265,28 @@ def test_host_copy_pipeline_error_exposes_no_partial_result(fm, oracle, what):
         fmsolve._raise(ctx, st, rep)
     assert "chol_tc_kernel" in ctx.last_launches and ctx.last_launches.count("chol_tc_kernel") > 1  # pipelined
     assert np.all(out == 0.0)  # earlier chunks were copied back: zero-filled, no partial result
+
+
+@pytest.mark.timeout(240, method="thread")
+def test_repeated_cfg2_solves_terminate_and_repeat_bitwise(fm):
+    # Hundreds of back-to-back cfg2-sized solves through the device entry, the fused
+    # eigenvalue-mask entry and the copy-pipelined host entry (residual on), as the
+    # bench runs them: the mbarrier protocol of the solver must never deadlock (a
+    # phase race between finished row groups and the MMA warp once hung about one
+    # host solve in fifty), and every repetition returns the same maps.
+    import torch
+    from paper_2604_10377_b200 import synth
+    G, R, e1, e2 = synth.random_normal_equations(64, 200, 256, 7)
+    M = fm.build_mask(fm.MaskKind.Resolvent, e1, e2, 0.5)
+    dev = torch.device("cuda", 0)
+    tG, tR, tM, t1, t2 = (torch.from_numpy(x).to(dev) for x in (G, R, M, e1, e2))
+    opts = fm.SolverOptions(compute_residual=False)
+    base, _ = fm.solve_device(tG, tR, tM, lam=100.0, opts=opts)
+    for _ in range(100):
+        C, _ = fm.solve_device(tG, tR, tM, lam=100.0, opts=opts)
+        assert torch.equal(C, base)
+    for _ in range(50):
+        fm.solve_device(tG, tR, lam=100.0, ev1=t1, ev2=t2, opts=opts)
+    host = fm.solve_host(G, R, M, 100.0).maps
+    for _ in range(100):
+        assert np.array_equal(fm.solve_host(G, R, M, 100.0).maps, host)
