@@ -49,6 +49,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 
 namespace fmap {
 
@@ -1372,8 +1373,15 @@ bool tc_supported(int k, int optin_smem) {
 }
 
 int tc_max_resolution(int optin_smem) {
+  // a pure function of the device's shared-memory limit, asked on every solve:
+  // computed once (the search walks ~300 layouts: ~18 us of host time per call,
+  // GPU idle before the first kernel, measured with tools/step_probe.py)
+  static std::atomic<int> cached_optin{-1}, cached_k{0};
+  if (cached_optin.load(std::memory_order_acquire) == optin_smem) return cached_k.load(std::memory_order_relaxed);
   int k = 1;
   while (k < 4096 && tc_supported(k + 1, optin_smem)) ++k;
+  cached_k.store(k, std::memory_order_relaxed);
+  cached_optin.store(optin_smem, std::memory_order_release);
   return k;
 }
 
