@@ -18,11 +18,7 @@ hG, hR, hM = (torch.from_numpy(x).pin_memory() for x in (G, R, M))
 hC = torch.empty_like(hG).pin_memory()
 ctx = _lib.context(0)
 P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
-for chunks, dbg in (("r2563", "0"), ("r2563", "0r"), ("r2563", "0"), ("r2563", "0r")):
-    os.environ.pop("FMAP_TC_REG96", None)
-    if dbg.endswith("r"):
-        os.environ["FMAP_TC_REG96"] = "1"
-        dbg = dbg[:-1]
+for chunks, dbg in (("r2563", "0"), ("r2563", "6")):
     os.environ["FMAP_PIPELINE"] = chunks
     if chunks[0] == "r":
         os.environ["FMAP_PIPELINE_W"] = ",".join(chunks[1:])
