@@ -1437,6 +1437,24 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
         default: fn = chol_tc_kernel<2, 2, 384, 1>; break;
       }
     }
+  } else if (L.cps >= 5 && L.threads > 96 && L.threads <= 128) {  // k = 65..96: 96 registers, 5 CTAs per SM
+    switch (mask_mode) {
+      case 0: fn = chol_tc_kernel<0, 1, 128, 5>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 128, 5>; break;
+      default: fn = chol_tc_kernel<2, 1, 128, 5>; break;
+    }
+  } else if (L.cps >= 4 && L.threads <= 160) {  // k = 97..128: 96 registers, 4 CTAs per SM
+    switch (mask_mode) {
+      case 0: fn = chol_tc_kernel<0, 1, 160, 4>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 160, 4>; break;
+      default: fn = chol_tc_kernel<2, 1, 160, 4>; break;
+    }
+  } else if (L.cps >= 3 && L.threads <= 192) {  // k = 129..144: 96 registers, 3 CTAs per SM
+    switch (mask_mode) {
+      case 0: fn = chol_tc_kernel<0, 1, 192, 3>; break;
+      case 1: fn = chol_tc_kernel<1, 1, 192, 3>; break;
+      default: fn = chol_tc_kernel<2, 1, 192, 3>; break;
+    }
   } else if (L.cps >= 2 && L.threads <= 256) {  // two CTAs per SM: 16 warps, up to 128 registers
     switch (mask_mode) {
       case 0: fn = chol_tc_kernel<0, 1, 256, 2>; break;
@@ -1455,7 +1473,32 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t npi = (p.nsys + L.ns - 1) / L.ns;
-    const int64_t maxgrid = (int64_t)sms * L.cps;
+    // The persistent grid is what is actually resident at once: a CTA beyond the
+    // registers' limit would only start when another exits, and its share of the
+    // systems (static stride) would run as a second wave.
+    struct OccMemo {
+      const void* fn;
+      size_t smem;
+      int threads, occ;
+    };
+    thread_local OccMemo memo[8] = {};  // the query costs host time on every launch otherwise
+    int occ = 0;
+    for (const OccMemo& m : memo)
+      if (m.fn == (const void*)fn && m.smem == smem && m.threads == L.threads) occ = m.occ;
+    if (occ == 0) {  // the register file's limit (TMEM and shared memory are in L.cps)
+      cudaFuncAttributes fa{};
+      int rpsm = 65536;
+      cudaDeviceGetAttribute(&rpsm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+      if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess && fa.numRegs > 0) {
+        const int per_warp = (fa.numRegs * 32 + 255) / 256 * 256;  // allocation unit: 256 registers per warp
+        occ = rpsm / (per_warp * ((L.threads + 31) / 32));
+      }
+      if (occ < 1) occ = 1;
+      thread_local int next = 0;
+      memo[next] = OccMemo{(const void*)fn, smem, L.threads, occ};
+      next = (next + 1) & 7;
+    }
+    const int64_t maxgrid = (int64_t)sms * std::min(L.cps, occ);
     const unsigned grid = (unsigned)(npi < maxgrid ? npi : maxgrid);
     note_launch("chol_tc_kernel");
     fn<<<grid, L.threads, smem, stream>>>(p, L, tmG, tmA);

@@ -290,3 +290,17 @@ def test_repeated_cfg2_solves_terminate_and_repeat_bitwise(fm):
     host = fm.solve_host(G, R, M, 100.0).maps
     for _ in range(100):
         assert np.array_equal(fm.solve_host(G, R, M, 100.0).maps, host)
+
+
+@pytest.mark.parametrize("k,b", [(80, 24), (100, 24), (128, 20), (144, 16)])
+def test_register_capped_residency_variants(fm, oracle, k, b):
+    # k = 65..144 run 96-register builds of the solver so the register file holds as
+    # many CTAs per SM as tensor memory allows (5 / 4 / 3 instead of 4 / 3 / 2), on a
+    # persistent grid of exactly the resident CTAs; enough systems here for several
+    # per CTA, so the next system's staging path runs as well.
+    G, R, M = _problems(oracle, b, k, 128, 4000 + k)
+    lam = 100.0
+    out = fm.solve_host(G, R, M, lam)
+    sub = slice(0, 2)
+    _assert_parity(out.maps[sub], _ref(oracle, G[sub], R[sub], M[sub], lam), f"k={k}")
+    assert _rel_residual(oracle, out.maps, G, R, M, lam) <= RES_REL
