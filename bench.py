@@ -201,7 +201,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
 
-    total_ms, kernel_ms = 0.0, []
+    total_ms, kernel_ms, factor_ms = 0.0, [], []
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(device)
         for _ in range(args.steps):
@@ -217,6 +217,7 @@ def run_ours(args):
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
             kernel_ms.append(rep.wall_seconds * 1e3)
+            factor_ms.append(rep.factor_seconds * 1e3)
         torch.cuda.synchronize(device)
     if world > 1:
         tt = torch.tensor([total_ms], device=device, dtype=torch.float64)
@@ -245,25 +246,47 @@ def run_ours(args):
     result = None
     if rank == 0:
         kavg = statistics.mean(kernel_ms)
+        favg = statistics.mean(factor_ms)
         flops = b * flops_per_fmap(k)
+        fflops = b * k ** 4 / 3.0   # the factorization's share: k systems of k^3/3 per fmap
         sms = torch.cuda.get_device_properties(device).multi_processor_count
         clocks = clk.summary()
         peak_max = sms * 128 * 2 * 1965e6 / 1e12   # FP32 SIMT at clocks.max.sm
-        achieved = flops / (kavg * 1e-3) / 1e12
-        traffic = _ncu_traffic()
+        achieved = fflops / (favg * 1e-3) / 1e12
+        solve_achieved = flops / (kavg * 1e-3) / 1e12
+        traffic = _ncu_traffic("factorization")
         bf16_peak = _measured_bf16_peak()
+        hbm_peak = _measured_hbm_peak()
+        # the back substitution reads each system's stored factor twice (forward and
+        # backward pass: 16-wide blocks of L21 + packed 16x16 diagonal blocks) plus its
+        # right-hand side row, and writes the row of C
+        K16 = (k + 15) // 16 * 16
+        P16 = K16 // 16
+        lfloats = 16 * P16 * (K16 - 16) - 128 * P16 * (P16 - 1) + P16 * 152  # lb_off(P) + packed diagonal blocks
+        bs_bytes = b * k * (2 * 4 * lfloats + 2 * 4 * k)
+        bs_ms = max(kavg - favg, 1e-9)
         roofline = {
-            # compute-bound kernel: the trailing updates run on tcgen05 (3xTF32), the
-            # panel chain on the FP32 pipe; the north_star's denominator is FP32 peak
+            # dominant kernel: chol_tc_kernel, the blocked Cholesky (trailing updates on
+            # tcgen05 3xTF32, the panel chain on the FP32 pipe); the north_star's
+            # denominator is FP32 peak "in the Cholesky kernel"
             "bound": "tensor",
             "achieved": round(achieved, 3), "peak": round(peak_max, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak_max, 4), "traffic": traffic,
-            "kernel": "chol_tc_kernel + chol_backsub_kernel (the solve: factorization, then y / back substitution / rcond verdict; kernel_ms = the solve's device time incl. validation)", "kernel_ms": round(kavg, 4),
-            "flops_per_launch": flops,
-            "peak_note": ("achieved counts the north_star's k^4/3 + k^3 flops per fmap; peak = FP32 "
-                          "SIMT (north_star's denominator) derived as SMs x 128 lanes x 2 x 1965 MHz "
-                          "(MEASURED_PEAKS.json has no FP32 figure); frac_at_sampled_clock uses the "
-                          "median SM clock sampled during the timed region"),
+            "kernel": "chol_tc_kernel (the factorization: 1 launch per step, timed live with CUDA events on the solver's stream around that launch alone)",
+            "kernel_ms": round(favg, 4), "flops_per_launch": fflops,
+            "peak_note": ("achieved counts the factorization's k^4/3 flops per fmap (k systems x k^3/3); "
+                          "peak = FP32 SIMT (north_star's denominator) derived as SMs x 128 lanes x 2 x "
+                          "1965 MHz (MEASURED_PEAKS.json has no FP32 figure); frac_at_sampled_clock uses "
+                          "the median SM clock sampled during the timed region"),
+            "solve": {"kernels": "chol_tc_kernel + chol_backsub_kernel (events around both)",
+                      "kernel_ms": round(kavg, 4), "flops_per_launch": flops,
+                      "achieved": round(solve_achieved, 3), "frac": round(solve_achieved / peak_max, 4),
+                      "note": "north_star's k^4/3 + k^3 flops per fmap over the whole solve"},
+            "backsub": {"bound": "hbm", "kernel_ms": round(bs_ms, 4), "bytes_per_launch": bs_bytes,
+                        "achieved": round(bs_bytes / (bs_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+                        "peak": hbm_peak, "frac": round(bs_bytes / (bs_ms * 1e-3) / 1e9 / hbm_peak, 4) if hbm_peak else None,
+                        "traffic": _ncu_traffic("backsub"),
+                        "note": "chol_backsub_kernel: the stored factor read twice (forward, backward pass) + r and C rows; kernel_ms = solve - factorization"},
         }
         if bf16_peak:
             roofline["frac_of_measured_bf16_tensor"] = round(achieved / bf16_peak, 5)
@@ -337,11 +360,19 @@ def _measured_bf16_peak():
         return None
 
 
-def _ncu_traffic():
-    """dram bytes per launch of the solver from the committed ncu --set full summary."""
+def _measured_hbm_peak():
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return None
+
+
+def _ncu_traffic(kernel: str):
+    """dram bytes per launch of one solver kernel ("factorization" / "backsub") from the
+    newest committed ncu --set full summary."""
     for p in sorted((ROOT / "profiles").glob("ncu_solver_*.json"), reverse=True):
         try:
-            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+            return json.loads(p.read_text())[kernel]["dram_bytes_per_launch"]
         except Exception:
             continue
     return None

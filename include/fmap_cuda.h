@@ -75,6 +75,8 @@ typedef struct fmap_report {
                              /* certificate (a lower bound) or, where that was          */
                              /* inconclusive, the exact Hager/Higham estimate           */
   int64_t rcond_exact_systems; /* systems that needed the exact estimator               */
+  double factor_seconds;     /* f32 route: device time of the factorization kernel     */
+                             /* (chol_tc_kernel) alone, CUDA events; 0 elsewhere       */
 } fmap_report;
 
 typedef struct fmap_ctx fmap_ctx;

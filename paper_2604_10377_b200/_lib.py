@@ -58,6 +58,7 @@ class ReportC(C.Structure):
         ("cap_bytes", C.c_uint64),
         ("min_rcond", C.c_double),
         ("rcond_exact_systems", C.c_int64),
+        ("factor_seconds", C.c_double),
     ]
 
 

@@ -39,7 +39,7 @@ struct fmap_ctx {
   // [16] systems whose rcond needed the exact Hager/Higham estimator (u32)
   unsigned char* d_ctrl = nullptr;
   unsigned char* h_ctrl = nullptr;  // pinned
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evf = nullptr;  // evf: factorization done
   unsigned last_exact = 0;     // systems of the last call that ran the exact rcond estimator
   double last_resmax = 0.0;    // max check_stationarity residual of the last call (control block)
   int64_t launches = 0;        // kernels launched by the last call
@@ -306,7 +306,9 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   }
   if (const char* dbg = std::getenv("FMAP_DEBUG")) p.debug = std::atoi(dbg);  // timing experiments only
   FMAP_CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-  FMAP_CK(ctx, launch_chol_solve(p, kmode, ctx->stream));
+  FMAP_CK(ctx, launch_chol_solve(p, kmode, ctx->stream, 1));  // factorization
+  FMAP_CK(ctx, cudaEventRecord(ctx->evf, ctx->stream));
+  FMAP_CK(ctx, launch_chol_solve(p, kmode, ctx->stream, 2));  // back substitution + verdict
   if (d_trace) {
     std::vector<long long> h(16 * 1024);
     FMAP_CK(ctx, cudaMemcpyAsync(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -380,10 +382,12 @@ int solve_core(fmap_ctx* ctx, int64_t b, int64_t k, const float* G, const float*
   float rcond;
   unsigned flags;
   if ((st = read_ctrl(ctx, &fail, &rcond, &flags))) return st;
-  float ms = 0.f;
+  float ms = 0.f, fms = 0.f;
   FMAP_CK(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  FMAP_CK(ctx, cudaEventElapsedTime(&fms, ctx->ev0, ctx->evf));
   if (rep) {
     rep->wall_seconds = ms * 1e-3;
+    rep->factor_seconds = fms * 1e-3;
     rep->min_rcond = rcond;
     rep->rcond_exact_systems = ctx->last_exact;
   }
@@ -776,6 +780,7 @@ int fmap_ctx_create(int device, fmap_ctx** out) {
   if ((e = cudaMallocHost(&ctx->h_ctrl, 64)) != cudaSuccess) return fail(e);
   if ((e = cudaEventCreate(&ctx->ev0)) != cudaSuccess) return fail(e);
   if ((e = cudaEventCreate(&ctx->ev1)) != cudaSuccess) return fail(e);
+  if ((e = cudaEventCreate(&ctx->evf)) != cudaSuccess) return fail(e);
   if ((e = cudaDeviceGetAttribute(&ctx->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                   device)) != cudaSuccess)
     return fail(e);
@@ -796,6 +801,7 @@ int fmap_ctx_destroy(fmap_ctx* ctx) {
   if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->evf) cudaEventDestroy(ctx->evf);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->comp2) cudaStreamDestroy(ctx->comp2);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
