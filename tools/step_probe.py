@@ -10,7 +10,8 @@ import torch  # noqa: E402
 import paper_2604_10377_b200 as fm  # noqa: E402
 from paper_2604_10377_b200 import _lib, synth  # noqa: E402
 
-G, R, e1, e2 = synth.random_normal_equations(64, 200, 256, 7)
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+G, R, e1, e2 = synth.random_normal_equations(B, 200, 256, 7)
 M = fm.build_mask(fm.MaskKind.Resolvent, e1, e2, 0.5)
 dev = torch.device("cuda", 0)
 tG, tR, tM = (torch.from_numpy(x).to(dev) for x in (G, R, M))
@@ -29,11 +30,11 @@ for it in range(n + 5):
     with torch.cuda.stream(stream):
         e0.record(stream)
     rep = _lib.ReportC()
-    st = L.fmap_solve_f32_dev(h, 64, 200, P(tG), P(tR), P(tM), 100.0, C.byref(opts), P(C_out), C.byref(rep))
+    st = L.fmap_solve_f32_dev(h, B, 200, P(tG), P(tR), P(tM), 100.0, C.byref(opts), P(C_out), C.byref(rep))
     with torch.cuda.stream(stream):
         e1_.record(stream)
     e1_.synchronize()
     if it >= 5:
         tot += e0.elapsed_time(e1_)
         ker += rep.wall_seconds * 1e3
-print(f"step {tot / n:.4f} ms, report span {ker / n:.4f} ms, overhead {(tot - ker) / n * 1e3:.1f} us")
+print(f"b={B}: step {tot / n:.4f} ms, report span {ker / n:.4f} ms, overhead {(tot - ker) / n * 1e3:.1f} us")
