@@ -985,7 +985,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
 // ---------------------------------------------------------------------------
 constexpr int kBsWarps = 4;
 
-__global__ void __launch_bounds__(32 * kBsWarps, 8) chol_backsub_kernel(SolveParams p, TcLayout Ly) {
+// MINB = 8: 64 registers, 8 CTAs (32 warps) per SM -- the HBM-bound regime of a full
+// batch; MINB = 4: 128 registers, the row loops unrolled so more of each block's
+// loads are in flight -- batches of at most ~4 CTAs per SM, where one system's
+// latency is the whole pass (8 pairs at k = 200: one system per warp).
+template <int MINB>
+__global__ void __launch_bounds__(32 * kBsWarps, MINB) chol_backsub_kernel(SolveParams p, TcLayout Ly) {
   extern __shared__ __align__(1024) float smem[];
   const int k = p.k, K16 = Ly.K16, P = Ly.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1076,22 +1081,43 @@ __global__ void __launch_bounds__(32 * kBsWarps, 8) chol_backsub_kernel(SolvePar
               ub[t] = uvs[16 * b + t];
               yb[t] = yv[16 * b + t];
             }
-            for (int rho = lane; rho < R; rho += 32) {
-              float acc = uvs[16 * b + 16 + rho], accy = yv[16 * b + 16 + rho];
+            if constexpr (MINB == 8) {  // the 64-register build keeps its schedule
+              for (int rho = lane; rho < R; rho += 32) {
+                float acc = uvs[16 * b + 16 + rho], accy = yv[16 * b + 16 + rho];
 #pragma unroll
-              for (int t4 = 0; t4 < 4; ++t4) {
-                const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * t4);
-                acc = fmaf(fabsf(l4.x), ub[4 * t4], acc);
-                acc = fmaf(fabsf(l4.y), ub[4 * t4 + 1], acc);
-                acc = fmaf(fabsf(l4.z), ub[4 * t4 + 2], acc);
-                acc = fmaf(fabsf(l4.w), ub[4 * t4 + 3], acc);
-                accy = fmaf(-l4.x, yb[4 * t4], accy);
-                accy = fmaf(-l4.y, yb[4 * t4 + 1], accy);
-                accy = fmaf(-l4.z, yb[4 * t4 + 2], accy);
-                accy = fmaf(-l4.w, yb[4 * t4 + 3], accy);
+                for (int t4 = 0; t4 < 4; ++t4) {
+                  const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * t4);
+                  acc = fmaf(fabsf(l4.x), ub[4 * t4], acc);
+                  acc = fmaf(fabsf(l4.y), ub[4 * t4 + 1], acc);
+                  acc = fmaf(fabsf(l4.z), ub[4 * t4 + 2], acc);
+                  acc = fmaf(fabsf(l4.w), ub[4 * t4 + 3], acc);
+                  accy = fmaf(-l4.x, yb[4 * t4], accy);
+                  accy = fmaf(-l4.y, yb[4 * t4 + 1], accy);
+                  accy = fmaf(-l4.z, yb[4 * t4 + 2], accy);
+                  accy = fmaf(-l4.w, yb[4 * t4 + 3], accy);
+                }
+                uvs[16 * b + 16 + rho] = acc;
+                yv[16 * b + 16 + rho] = accy;
               }
-              uvs[16 * b + 16 + rho] = acc;
-              yv[16 * b + 16 + rho] = accy;
+            } else {
+#pragma unroll 2
+              for (int rho = lane; rho < R; rho += 32) {
+                float acc = uvs[16 * b + 16 + rho], accy = yv[16 * b + 16 + rho];
+#pragma unroll
+                for (int t4 = 0; t4 < 4; ++t4) {
+                  const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * t4);
+                  acc = fmaf(fabsf(l4.x), ub[4 * t4], acc);
+                  acc = fmaf(fabsf(l4.y), ub[4 * t4 + 1], acc);
+                  acc = fmaf(fabsf(l4.z), ub[4 * t4 + 2], acc);
+                  acc = fmaf(fabsf(l4.w), ub[4 * t4 + 3], acc);
+                  accy = fmaf(-l4.x, yb[4 * t4], accy);
+                  accy = fmaf(-l4.y, yb[4 * t4 + 1], accy);
+                  accy = fmaf(-l4.z, yb[4 * t4 + 2], accy);
+                  accy = fmaf(-l4.w, yb[4 * t4 + 3], accy);
+                }
+                uvs[16 * b + 16 + rho] = acc;
+                yv[16 * b + 16 + rho] = accy;
+              }
             }
             __syncwarp();
           }
@@ -1105,17 +1131,33 @@ __global__ void __launch_bounds__(32 * kBsWarps, 8) chol_backsub_kernel(SolvePar
           const int R = K16 - 16 * b - 16;
           if (R > 0) {
             const float* blk = Lsl + lb_off(b, K16);
-            for (int rho = lane >> 2; rho < R; rho += 8) {
-              const float xc = xv[16 * b + 16 + rho], wcv = wv[16 * b + 16 + rho];
-              const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
-              v4[0] = fmaf(l4.x, xc, v4[0]);
-              v4[1] = fmaf(l4.y, xc, v4[1]);
-              v4[2] = fmaf(l4.z, xc, v4[2]);
-              v4[3] = fmaf(l4.w, xc, v4[3]);
-              w4[0] = fmaf(fabsf(l4.x), wcv, w4[0]);
-              w4[1] = fmaf(fabsf(l4.y), wcv, w4[1]);
-              w4[2] = fmaf(fabsf(l4.z), wcv, w4[2]);
-              w4[3] = fmaf(fabsf(l4.w), wcv, w4[3]);
+            if constexpr (MINB == 8) {  // the 64-register build keeps its schedule
+              for (int rho = lane >> 2; rho < R; rho += 8) {
+                const float xc = xv[16 * b + 16 + rho], wcv = wv[16 * b + 16 + rho];
+                const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
+                v4[0] = fmaf(l4.x, xc, v4[0]);
+                v4[1] = fmaf(l4.y, xc, v4[1]);
+                v4[2] = fmaf(l4.z, xc, v4[2]);
+                v4[3] = fmaf(l4.w, xc, v4[3]);
+                w4[0] = fmaf(fabsf(l4.x), wcv, w4[0]);
+                w4[1] = fmaf(fabsf(l4.y), wcv, w4[1]);
+                w4[2] = fmaf(fabsf(l4.z), wcv, w4[2]);
+                w4[3] = fmaf(fabsf(l4.w), wcv, w4[3]);
+              }
+            } else {
+#pragma unroll 4
+              for (int rho = lane >> 2; rho < R; rho += 8) {
+                const float xc = xv[16 * b + 16 + rho], wcv = wv[16 * b + 16 + rho];
+                const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
+                v4[0] = fmaf(l4.x, xc, v4[0]);
+                v4[1] = fmaf(l4.y, xc, v4[1]);
+                v4[2] = fmaf(l4.z, xc, v4[2]);
+                v4[3] = fmaf(l4.w, xc, v4[3]);
+                w4[0] = fmaf(fabsf(l4.x), wcv, w4[0]);
+                w4[1] = fmaf(fabsf(l4.y), wcv, w4[1]);
+                w4[2] = fmaf(fabsf(l4.z), wcv, w4[2]);
+                w4[3] = fmaf(fabsf(l4.w), wcv, w4[3]);
+              }
             }
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1)
@@ -1508,10 +1550,14 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   if (!(parts & 2)) return cudaSuccess;
   // back substitution + verdict over the stored factors, one warp per system
   const size_t bsmem = (size_t)kBsWarps * 7 * L.K16 * sizeof(float);
-  e = cudaFuncSetAttribute(chol_backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+  const int64_t bctas = (p.nsys + kBsWarps - 1) / kBsWarps;
+  bool lat = bctas <= 4ll * sms;  // at most ~4 CTAs per SM: one system's latency is the pass
+  if (const char* v = std::getenv("FMAP_BS")) lat = std::atoi(v) == 4;  // experiments: 4 / 8
+  void (*bfn)(SolveParams, TcLayout) = lat ? chol_backsub_kernel<4> : chol_backsub_kernel<8>;
+  e = cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
   if (e != cudaSuccess) return e;
   note_launch("chol_backsub_kernel");
-  chol_backsub_kernel<<<(unsigned)((p.nsys + kBsWarps - 1) / kBsWarps), 32 * kBsWarps, bsmem, stream>>>(p, L);
+  bfn<<<(unsigned)bctas, 32 * kBsWarps, bsmem, stream>>>(p, L);
   return cudaGetLastError();
 }
 
