@@ -304,3 +304,22 @@ def test_register_capped_residency_variants(fm, oracle, k, b):
     sub = slice(0, 2)
     _assert_parity(out.maps[sub], _ref(oracle, G[sub], R[sub], M[sub], lam), f"k={k}")
     assert _rel_residual(oracle, out.maps, G, R, M, lam) <= RES_REL
+
+
+def test_report_factor_seconds(fm, oracle):
+    # fmap_report.factor_seconds: CUDA events around the factorization launch alone
+    # (bench.py's roofline on the dominant kernel), inside wall_seconds (whole solve)
+    import torch
+    G, R, M = _problems(oracle, 4, 120, 96, 77)
+    dev = torch.device("cuda", 0)
+    tG, tR, tM = (torch.from_numpy(x).to(dev) for x in (G, R, M))
+    from paper_2604_10377_b200 import _lib
+    import ctypes as C
+    ctx = _lib.context(0)
+    out = torch.empty_like(tG)
+    rep = _lib.ReportC()
+    o = fm.SolverOptions(compute_residual=False).to_c()
+    P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    st = ctx._lib.fmap_solve_f32_dev(ctx.handle, 4, 120, P(tG), P(tR), P(tM), 100.0, C.byref(o), P(out), C.byref(rep))
+    assert st == 0
+    assert 0.0 < rep.factor_seconds < rep.wall_seconds
