@@ -1234,50 +1234,80 @@ __global__ void __launch_bounds__(32 * kBsWarps, MINB) chol_backsub_kernel(Solve
             float* csg = hv + K16;
             float* osg = hv + 2 * K16;
             // v <- A^{-1} v  (A = L L^T): forward L z = v, backward L^T v = z
+            // v <- A^{-1} v on the stored factor, with the main passes' lane-parallel
+            // block scheme (16-lane shuffle chains for the diagonal blocks, lanes over
+            // rows / column quads for the off-diagonal ones): a lane-0 serial version
+            // cost ~1 ms per system on this path (k = 260-300 with d = 256 Grams,
+            // where the certificate is inconclusive for up to ~20 % of the systems).
             auto solve_inplace = [&]() {
-              for (int b = 0; b < P; ++b) {
+              const int t = lane & 15;
+              for (int b = 0; b < P; ++b) {  // forward: L z = v
                 const float* Lbb = L11 + b * 152;
-                if (lane == 0) {
-                  for (int t = 0; t < 16; ++t) {
-                    float sacc = v[16 * b + t];
-                    for (int u = 0; u < t; ++u) sacc = fmaf(-Lbb[t * (t + 1) / 2 + u], v[16 * b + u], sacc);
-                    v[16 * b + t] = sacc * Lbb[136 + t];
-                  }
+                float a = v[16 * b + t], res = 0.f;
+#pragma unroll
+                for (int sv = 0; sv < 16; ++sv) {
+                  const float zs = __shfl_sync(kFull, a, sv) * Lbb[136 + sv];
+                  if (t == sv) res = zs;
+                  if (t > sv) a = fmaf(-Lbb[t * (t + 1) / 2 + sv], zs, a);
                 }
+                __syncwarp();
+                if (lane < 16) v[16 * b + lane] = res;
                 __syncwarp();
                 const int R = K16 - 16 * b - 16;
                 if (R > 0) {
                   const float* blk = Lsl + lb_off(b, K16);
+                  float vb[16];
+#pragma unroll
+                  for (int u = 0; u < 16; ++u) vb[u] = v[16 * b + u];
                   for (int rho = lane; rho < R; rho += 32) {
                     float acc = v[16 * b + 16 + rho];
 #pragma unroll
-                    for (int t = 0; t < 16; ++t) acc = fmaf(-blk[rho * 16 + t], v[16 * b + t], acc);
+                    for (int u4 = 0; u4 < 4; ++u4) {
+                      const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * u4);
+                      acc = fmaf(-l4.x, vb[4 * u4], acc);
+                      acc = fmaf(-l4.y, vb[4 * u4 + 1], acc);
+                      acc = fmaf(-l4.z, vb[4 * u4 + 2], acc);
+                      acc = fmaf(-l4.w, vb[4 * u4 + 3], acc);
+                    }
                     v[16 * b + 16 + rho] = acc;
                   }
                   __syncwarp();
                 }
               }
-              for (int b = P - 1; b >= 0; --b) {
+              for (int b = P - 1; b >= 0; --b) {  // backward: L^T v = z
                 const float* Lbb = L11 + b * 152;
                 const int R = K16 - 16 * b - 16;
-                if (R > 0) {
+                float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                if (R > 0) {  // s_t = sum_rho L[16b+16+rho][16b+t] v_rho (lanes: rows x column quads)
                   const float* blk = Lsl + lb_off(b, K16);
-                  if (lane < 16) {
-                    float sacc = 0.f;
-                    for (int rho = 0; rho < R; ++rho) sacc = fmaf(blk[rho * 16 + lane], v[16 * b + 16 + rho], sacc);
-                    wv[lane] = sacc;
+                  for (int rho = lane >> 2; rho < R; rho += 8) {
+                    const float vc = v[16 * b + 16 + rho];
+                    const float4 l4 = *reinterpret_cast<const float4*>(blk + rho * 16 + 4 * (lane & 3));
+                    s4[0] = fmaf(l4.x, vc, s4[0]);
+                    s4[1] = fmaf(l4.y, vc, s4[1]);
+                    s4[2] = fmaf(l4.z, vc, s4[2]);
+                    s4[3] = fmaf(l4.w, vc, s4[3]);
                   }
-                } else if (lane < 16) {
-                  wv[lane] = 0.f;
+#pragma unroll
+                  for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) s4[e] += __shfl_xor_sync(kFull, s4[e], o);
+                }
+                float st = 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float other = __shfl_sync(kFull, s4[e], t >> 2);
+                  if ((t & 3) == e) st = other;
+                }
+                float z = v[16 * b + t] - st, x = 0.f;
+#pragma unroll
+                for (int vv = 15; vv >= 0; --vv) {
+                  const float xs = __shfl_sync(kFull, z, vv) * Lbb[136 + vv];
+                  if (t == vv) x = xs;
+                  if (t < vv) z = fmaf(-Lbb[vv * (vv + 1) / 2 + t], xs, z);
                 }
                 __syncwarp();
-                if (lane == 0) {
-                  for (int t = 15; t >= 0; --t) {
-                    float sacc = v[16 * b + t] - wv[t];
-                    for (int u = t + 1; u < 16; ++u) sacc = fmaf(-Lbb[u * (u + 1) / 2 + t], v[16 * b + u], sacc);
-                    v[16 * b + t] = sacc * Lbb[136 + t];
-                  }
-                }
+                if (lane < 16) v[16 * b + lane] = x;
                 __syncwarp();
               }
               for (int c = k + lane; c < K16; c += 32) v[c] = 0.f;  // identity padding stays out
