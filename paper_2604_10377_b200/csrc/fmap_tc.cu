@@ -1000,14 +1000,14 @@ __global__ void __launch_bounds__(32 * kBsWarps, MINB) chol_backsub_kernel(Solve
   const float* L11st = Lst + (size_t)p.nsys * Ly.lb;
   const unsigned* stst = reinterpret_cast<const unsigned*>(L11st + (size_t)p.nsys * P * 152);
   // Per system: L^T x = y, the backward
-  // comparison solve M(L)^T w = e, the rcond verdict, the row of C.
+  // comparison solve M(L)^T w = u, the rcond verdict, the row of C.
   //
   // rcond (solver.hpp:164-168: Eigen's PartialPivLU::rcond(), a Hager/Higham
   // estimate of 1 / (||A||_1 ||A^{-1}||_1)).  For A = L L^T, |L^{-1}| <= M(L)^{-1}
-  // entrywise (M = comparison matrix), so ||A^{-1}||_1 <= ||L^{-1}||_inf ||L^{-1}||_1
-  // <= max(u) max(w) with u = M(L)^{-1} e (forward pass) and w = M(L)^{-T} e
-  // (with the back substitution): cert = 1 / (||A||_1 max(u) max(w)) is a lower bound on
-  // the true rcond, and the reference's estimate never exceeds ||A^{-1}||_1, so
+  // entrywise (M = comparison matrix), so ||A^{-1}||_1 <= || |L^{-T}| |L^{-1}| ||_1 =
+  // max(|L^{-T}| |L^{-1}| e) <= max(w) with u = M(L)^{-1} e (forward pass) and
+  // w = M(L)^{-T} u (with the back substitution; tighter than max(u) * max(M(L)^{-T} e),
+  // which it replaced): cert = 1 / (||A||_1 max(w)) is a lower bound on the true rcond, and the reference's estimate never exceeds ||A^{-1}||_1, so
   // cert >= 2 * threshold proves the reference would accept the system.  Otherwise
   // (rare: near-singular systems) the exact Hager/Higham estimator runs here on the
   // factor (forward + backward solves over the stored L), the same algorithm
@@ -1169,7 +1169,7 @@ __global__ void __launch_bounds__(32 * kBsWarps, MINB) chol_backsub_kernel(Solve
           }
           // lane t (< 16): z_t = y_t - s_t, then back substitution L_bb^T x_b = z_b by rows
           // from the bottom (x_v = z_v / L_vv; z_t -= L[v][t] x_v), and the same with
-          // the comparison matrix for w (zw_t = 1 + sw_t; zw_t += |L[v][t]| w_v)
+          // the comparison matrix for w (zw_t = u_t + sw_t; zw_t += |L[v][t]| w_v)
           const int t = lane & 15;
           float st = 0.f, swt = 0.f;
 #pragma unroll
@@ -1181,7 +1181,7 @@ __global__ void __launch_bounds__(32 * kBsWarps, MINB) chol_backsub_kernel(Solve
               swt = otherw;
             }
           }
-          float z = yv[16 * b + t] - st, zw = 1.f + swt;
+          float z = yv[16 * b + t] - st, zw = uvs[16 * b + t] + swt;
           float x = 0.f, xw = 0.f;
 #pragma unroll
           for (int v = 15; v >= 0; --v) {
@@ -1206,22 +1206,20 @@ __global__ void __launch_bounds__(32 * kBsWarps, MINB) chol_backsub_kernel(Solve
         // row of C, certificate
         float* Crow = p.C + ((size_t)q * k + i) * k;
         bool nf = false;
-        float umax = 0.f, wmax = 0.f;
+        float wmax = 0.f;
         for (int c = lane; c < k; c += 32) {
           const float x = xv[c];
           nf |= !(fabsf(x) <= FLT_MAX);
           Crow[c] = x;
-          umax = fmaxf(umax, uvs[c]);
           wmax = fmaxf(wmax, wv[c]);
         }
         nf = __any_sync(kFull, nf);
-        umax = warp_maxf(umax);
         wmax = warp_maxf(wmax);
         const float a1 = __uint_as_float(ssc[4]);
         bool sing = ssc[2] != 0u || nf;
         float rc = 0.f;
         if (!sing) {
-          const float cert = 1.f / (a1 * umax * wmax);  // 0 when the bound overflows
+          const float cert = 1.f / (a1 * wmax);  // 0 when the bound overflows
           if (!(a1 > 0.f)) {
             rc = 0.f;                                   // rcond_estimate_helper: ||A||_1 == 0
           } else if (k == 1) {
