@@ -988,7 +988,8 @@ constexpr int kBsWarps = 4;
 // MINB = 8: 64 registers, 8 CTAs (32 warps) per SM -- the HBM-bound regime of a full
 // batch; MINB = 4: 128 registers, the row loops unrolled so more of each block's
 // loads are in flight -- batches of at most ~4 CTAs per SM, where one system's
-// latency is the whole pass (8 pairs at k = 200: one system per warp).
+// latency is the whole pass (8 pairs at k = 200: one system per warp); MINB = 6:
+// 80 registers and the unrolled loops for k > 208 (longer blocks).
 template <int MINB>
 __global__ void __launch_bounds__(32 * kBsWarps, MINB) chol_backsub_kernel(SolveParams p, TcLayout Ly) {
   extern __shared__ __align__(1024) float smem[];
@@ -1632,9 +1633,13 @@ cudaError_t launch_chol_tc(const SolveParams& p, int mask_mode, cudaStream_t str
   // back substitution + verdict over the stored factors, one warp per system
   const size_t bsmem = (size_t)kBsWarps * 7 * L.K16 * sizeof(float);
   const int64_t bctas = (p.nsys + kBsWarps - 1) / kBsWarps;
-  bool lat = bctas <= 4ll * sms;  // at most ~4 CTAs per SM: one system's latency is the pass
-  if (const char* v = std::getenv("FMAP_BS")) lat = std::atoi(v) == 4;  // experiments: 4 / 8
-  void (*bfn)(SolveParams, TcLayout) = lat ? chol_backsub_kernel<4> : chol_backsub_kernel<8>;
+  // 4: at most ~4 CTAs per SM, one system's latency is the pass (128 registers);
+  // 6: k > 208, where the factor's blocks are longer (80 registers, fewer spills:
+  //    4-6 % faster at k = 240-280 than 8); 8: the 64-register bandwidth build
+  int minb = bctas <= 4ll * sms ? 4 : (L.K16 > 208 ? 6 : 8);
+  if (const char* v = std::getenv("FMAP_BS")) minb = std::atoi(v);  // experiments: 4 / 6 / 8
+  void (*bfn)(SolveParams, TcLayout) =
+      minb == 4 ? chol_backsub_kernel<4> : (minb == 6 ? chol_backsub_kernel<6> : chol_backsub_kernel<8>);
   e = cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
   if (e != cudaSuccess) return e;
   note_launch("chol_backsub_kernel");
